@@ -1,0 +1,108 @@
+"""ctypes bindings for the two native libraries (built in-tree by ``csrc/Makefile``).
+
+``libmb_sm100.so``   sm_100a data-plane kernels, C-ABI in ``include/mb_kernels.h``
+``libmb_planner.so`` C++ host planners,        C-ABI in ``include/mb_planner.h``
+
+There is no fallback: if a library is missing the import of the op that needs it raises
+``NativeLibraryError``.  Nonzero status codes raise ``ValueError`` (invalid argument) or
+``RuntimeError`` (CUDA / solver failure) with the library's thread-local message.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+LIB_DIR = Path(__file__).resolve().parent / "lib"
+
+c_i32 = ctypes.c_int32
+c_i64 = ctypes.c_int64
+c_u64 = ctypes.c_uint64
+c_dbl = ctypes.c_double
+c_vp = ctypes.c_void_p
+c_int = ctypes.c_int
+c_char_p = ctypes.c_char_p
+
+
+class NativeLibraryError(RuntimeError):
+    """A required native library is missing or failed to load."""
+
+
+class LPError(RuntimeError):
+    """Numerical failure or malformed input in the simplex solver (mirrors moebalance.lp.LPError)."""
+
+
+_KERNEL_SIGS = {
+    "mb_last_error": (c_char_p, []),
+    "mb_version": (c_int, []),
+    "mb_expert_histogram": (c_int, [c_vp, c_i64, c_i64, c_i32, c_i32, c_vp, c_vp, c_i32, c_vp]),
+    "mb_grouped_gemm": (
+        c_int,
+        [c_int, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_int, c_int, c_int, c_int,
+         c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp],
+    ),
+}
+
+_PLANNER_SIGS: dict = {}
+
+_libs: dict[str, ctypes.CDLL] = {}
+
+
+def _load(name: str, sigs: dict) -> ctypes.CDLL:
+    if name in _libs:
+        return _libs[name]
+    path = LIB_DIR / name
+    if not path.is_file():
+        raise NativeLibraryError(
+            f"{path} is missing: build it with `make -C {LIB_DIR.parent / 'csrc'}` "
+            "(or __graft_entry__.build()); there is no CPU fallback")
+    try:
+        lib = ctypes.CDLL(str(path), mode=os.RTLD_LOCAL)
+    except OSError as err:
+        raise NativeLibraryError(f"failed to load {path}: {err}") from err
+    for fn, (res, args) in sigs.items():
+        f = getattr(lib, fn)
+        f.restype = res
+        f.argtypes = args
+    _libs[name] = lib
+    return lib
+
+
+def kernels() -> ctypes.CDLL:
+    return _load("libmb_sm100.so", _KERNEL_SIGS)
+
+
+def planner() -> ctypes.CDLL:
+    return _load("libmb_planner.so", _PLANNER_SIGS)
+
+
+def register_planner_sigs(sigs: dict) -> None:
+    _PLANNER_SIGS.update(sigs)
+
+
+def check(status: int, lib: ctypes.CDLL, what: str) -> None:
+    if status == 0:
+        return
+    msg = lib.mb_last_error() if hasattr(lib, "mb_last_error") else None
+    msg = msg.decode() if isinstance(msg, bytes) else str(msg)
+    if status == 1:
+        raise ValueError(f"{what}: {msg}")
+    if status == 5:
+        raise LPError(f"{what}: {msg}")
+    raise RuntimeError(f"{what} failed (status {status}): {msg}")
+
+
+def ptr(t) -> int | None:
+    """Raw pointer of a torch tensor / numpy array (None for None)."""
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        return t.data_ptr()
+    return t.ctypes.data
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream

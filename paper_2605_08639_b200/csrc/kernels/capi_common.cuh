@@ -1,0 +1,87 @@
+// Host-side helpers shared by the kernel C-ABI: status codes, thread-local last error,
+// TMA tensor-map encoding through the driver entry point (no libcuda link dependency,
+// so the library also loads on GPU-less hosts).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+namespace mb {
+
+enum Status : int { MB_OK = 0, MB_EINVAL = 1, MB_ECUDA = 2, MB_EUNSUPPORTED = 3, MB_ETIMEOUT = 4 };
+
+inline thread_local std::string g_last_error;
+
+inline int set_error(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define MB_CUDA_TRY(expr)                                                                   \
+  do {                                                                                      \
+    cudaError_t _e = (expr);                                                                \
+    if (_e != cudaSuccess)                                                                  \
+      return ::mb::set_error(::mb::MB_ECUDA, "%s failed: %s (%s:%d)", #expr,                \
+                             cudaGetErrorString(_e), __FILE__, __LINE__);                  \
+  } while (0)
+
+#define MB_CHECK_ARG(cond, ...)                                                             \
+  do {                                                                                      \
+    if (!(cond)) return ::mb::set_error(::mb::MB_EINVAL, __VA_ARGS__);                      \
+  } while (0)
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline PFN_encodeTiled get_encode_tiled() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor map, SWIZZLE_128B: dims {inner, outer}, row pitch in bytes, box {box_inner, box_outer}.
+inline int make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                             uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_outer) {
+  PFN_encodeTiled enc = get_encode_tiled();
+  if (!enc) return set_error(MB_ECUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
+  if (outer == 0) outer = 1;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_pitch_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estride[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estride,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(MB_ECUDA, "cuTensorMapEncodeTiled failed (%d): inner=%llu outer=%llu pitch=%llu box=%ux%u", (int)r,
+                     (unsigned long long)inner, (unsigned long long)outer, (unsigned long long)row_pitch_bytes,
+                     box_inner, box_outer);
+  return MB_OK;
+}
+
+inline int device_sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+}  // namespace mb

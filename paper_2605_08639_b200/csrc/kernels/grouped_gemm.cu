@@ -1,0 +1,77 @@
+// Host launcher + C-ABI for the K4 tcgen05 grouped GEMM (see grouped_gemm.cuh).
+#include "grouped_gemm.cuh"
+#include "capi_common.cuh"
+#include "../../../include/mb_kernels.h"
+
+namespace mb {
+
+template <bool kW, bool kAmn, bool kBmn, int BN, int kEpi>
+static int launch_gemm(const GemmParams& p, cudaStream_t stream) {
+  auto kern = grouped_gemm_kernel<kW, kAmn, kBmn, BN, kEpi>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    MB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::kSmemBytes));
+    attr_set = true;
+  }
+  kern<<<device_sm_count(), 192, GemmCfg<BN>::kSmemBytes, stream>>>(p);
+  MB_CUDA_TRY(cudaGetLastError());
+  return MB_OK;
+}
+
+}  // namespace mb
+
+using namespace mb;
+
+extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t a_cols, const void* B0,
+                               int64_t b0_rows, const void* B1, int64_t b1_rows, int64_t b_cols,
+                               const void* groups, int num_groups, int M, int N, int K, void* C, int64_t ldc,
+                               int64_t c_slot_stride, void* C2, int64_t ldc2, const void* aux, int64_t ld_aux,
+                               void* stream) {
+  MB_CHECK_ARG(num_groups >= 0 && num_groups <= kMaxGroups, "num_groups %d outside [0, %d]", num_groups, kMaxGroups);
+  MB_CHECK_ARG(A && B0 && C && groups, "null operand pointer");
+  MB_CHECK_ARG(a_cols % 64 == 0 && b_cols % 64 == 0, "operand widths must be multiples of 64");
+  if (num_groups == 0) return MB_OK;
+  if (!B1) { B1 = B0; b1_rows = b0_rows; }
+  GemmParams p{};
+  p.groups = reinterpret_cast<const GemmGroup*>(groups);
+  p.num_groups = num_groups;
+  p.M = M; p.N = N; p.K = K;
+  p.C = C; p.ldc = ldc; p.c_slot_stride = c_slot_stride;
+  p.C2 = C2; p.ldc2 = ldc2; p.aux = aux; p.ld_aux = ld_aux;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int rc;
+  switch (mode) {
+    case MB_GEMM_FWD_STORE:
+    case MB_GEMM_FWD_SWIGLU: {
+      MB_CHECK_ARG(N % 256 == 0 && K % 64 == 0 && a_cols == K && b_cols == K, "fwd GEMM shape N=%d K=%d", N, K);
+      if ((rc = make_tmap_bf16_2d(&p.tmA, A, a_cols, a_rows, a_cols * 2, 64, 128))) return rc;
+      if ((rc = make_tmap_bf16_2d(&p.tmB0, B0, b_cols, b0_rows, b_cols * 2, 64, 256))) return rc;
+      if ((rc = make_tmap_bf16_2d(&p.tmB1, B1, b_cols, b1_rows, b_cols * 2, 64, 256))) return rc;
+      if (mode == MB_GEMM_FWD_STORE) return launch_gemm<false, false, false, 256, EPI_STORE_BF16>(p, s);
+      MB_CHECK_ARG(C2 != nullptr, "SwiGLU epilogue needs the activation output");
+      return launch_gemm<false, false, false, 256, EPI_SWIGLU>(p, s);
+    }
+    case MB_GEMM_DGRAD_STORE:
+    case MB_GEMM_DGRAD_DSWIGLU: {
+      MB_CHECK_ARG(K % 64 == 0 && a_cols == K && b_cols == N, "dgrad GEMM shape N=%d K=%d", N, K);
+      if ((rc = make_tmap_bf16_2d(&p.tmA, A, a_cols, a_rows, a_cols * 2, 64, 128))) return rc;
+      if ((rc = make_tmap_bf16_2d(&p.tmB0, B0, b_cols, b0_rows, b_cols * 2, 64, 64))) return rc;
+      if ((rc = make_tmap_bf16_2d(&p.tmB1, B1, b_cols, b1_rows, b_cols * 2, 64, 64))) return rc;
+      if (mode == MB_GEMM_DGRAD_STORE) {
+        MB_CHECK_ARG(N % 256 == 0, "dgrad N=%d must be a multiple of 256", N);
+        return launch_gemm<false, false, true, 256, EPI_STORE_BF16>(p, s);
+      }
+      MB_CHECK_ARG(N % 128 == 0 && aux != nullptr, "dSwiGLU epilogue needs N%%128==0 and H");
+      return launch_gemm<false, false, true, 128, EPI_DSWIGLU>(p, s);
+    }
+    case MB_GEMM_WGRAD: {
+      MB_CHECK_ARG(M % 128 == 0 && N % 256 == 0 && a_cols == M && b_cols == N, "wgrad GEMM shape M=%d N=%d", M, N);
+      if ((rc = make_tmap_bf16_2d(&p.tmA, A, a_cols, a_rows, a_cols * 2, 64, 64))) return rc;
+      if ((rc = make_tmap_bf16_2d(&p.tmB0, B0, b_cols, b0_rows, b_cols * 2, 64, 64))) return rc;
+      p.tmB1 = p.tmB0;
+      return launch_gemm<true, true, true, 256, EPI_ACC_F32>(p, s);
+    }
+    default:
+      return set_error(MB_EINVAL, "unknown grouped GEMM mode %d", mode);
+  }
+}

@@ -1,0 +1,87 @@
+"""Thin Python wrappers over the sm_100a data-plane C-ABI (``include/mb_kernels.h``).
+
+Every wrapper takes CUDA tensors, launches on the current torch stream and returns
+immediately.  Shapes/dtypes are checked here; the kernels themselves never allocate.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native as nat
+
+GEMM_FWD_STORE = 0
+GEMM_FWD_SWIGLU = 1
+GEMM_DGRAD_STORE = 2
+GEMM_DGRAD_DSWIGLU = 3
+GEMM_WGRAD = 4
+
+GROUP_FIELDS = 4  # int32 rows, a0, slot, flags
+FLAG_ACCUMULATE = 1
+FLAG_REPLICA = 2
+
+
+def _lib():
+    return nat.kernels()
+
+
+def _need_cuda(*tensors):
+    for t in tensors:
+        if t is not None and not t.is_cuda:
+            raise ValueError("data-plane ops take CUDA tensors (there is no CPU path)")
+
+
+def make_groups(rows, a0, slot, flags=None, device="cuda") -> torch.Tensor:
+    """Pack per-group (rows, a0, slot, flags) into the int32 [G, 4] device table."""
+    n = len(rows)
+    flags = [0] * n if flags is None else flags
+    tab = np.stack([np.asarray(rows), np.asarray(a0), np.asarray(slot), np.asarray(flags)], axis=1).astype(np.int32)
+    return torch.from_numpy(tab.reshape(n, GROUP_FIELDS)).to(device)
+
+
+def expert_histogram(idx: torch.Tensor, num_experts: int, chunk_tokens: int = 32,
+                     counts: torch.Tensor | None = None, chunk_counts: torch.Tensor | None = None):
+    """K1: idx [NB, T, k] int32 -> counts [NB, E] int32 (u32 values), chunk counts [NB, chunks, E]."""
+    _need_cuda(idx)
+    if idx.dim() == 2:
+        idx = idx.unsqueeze(0)
+    if idx.dtype != torch.int32 or not idx.is_contiguous():
+        raise ValueError("idx must be a contiguous int32 [NB, T, k] tensor")
+    nb, t, k = idx.shape
+    chunks = (t + chunk_tokens - 1) // chunk_tokens
+    if counts is None:
+        counts = torch.empty((nb, num_experts), dtype=torch.int32, device=idx.device)
+    if chunk_counts is None:
+        chunk_counts = torch.empty((nb, max(chunks, 1), num_experts), dtype=torch.int32, device=idx.device)
+    lib = _lib()
+    nat.check(lib.mb_expert_histogram(idx.data_ptr(), nb, t, k, num_experts, counts.data_ptr(),
+                                      chunk_counts.data_ptr(), chunk_tokens, nat.stream_ptr()),
+              lib, "mb_expert_histogram")
+    return counts, chunk_counts
+
+
+def grouped_gemm(mode: int, A: torch.Tensor, B0: torch.Tensor, groups: torch.Tensor, *, M: int = 0, N: int,
+                 K: int = 0, C: torch.Tensor, C2: torch.Tensor | None = None, aux: torch.Tensor | None = None,
+                 B1: torch.Tensor | None = None, c_slot_stride: int = 0) -> None:
+    """K4: tcgen05 grouped GEMM; see include/mb_kernels.h for the five modes."""
+    _need_cuda(A, B0, groups, C, C2, aux, B1)
+    for t in (A, B0, B1):
+        if t is not None and (t.dtype != torch.bfloat16 or not t.is_contiguous()):
+            raise ValueError("GEMM operands must be contiguous bf16")
+    if groups.dtype != torch.int32 or groups.dim() != 2 or groups.shape[1] != GROUP_FIELDS:
+        raise ValueError("groups must be an int32 [G, 4] table")
+    a_cols = A.shape[-1]
+    a_rows = A.numel() // a_cols
+    b_cols = B0.shape[-1]
+    b0_rows = B0.numel() // b_cols
+    b1_rows = 0 if B1 is None else B1.numel() // b_cols
+    ldc = C.shape[-1]
+    ldc2 = 0 if C2 is None else C2.shape[-1]
+    ld_aux = 0 if aux is None else aux.shape[-1]
+    lib = _lib()
+    nat.check(lib.mb_grouped_gemm(mode, A.data_ptr(), a_rows, a_cols, B0.data_ptr(), b0_rows,
+                                  nat.ptr(B1), b1_rows, b_cols, groups.data_ptr(), groups.shape[0], M, N, K,
+                                  C.data_ptr(), ldc, c_slot_stride, nat.ptr(C2), ldc2, nat.ptr(aux), ld_aux,
+                                  nat.stream_ptr()),
+              lib, "mb_grouped_gemm")

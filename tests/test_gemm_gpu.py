@@ -1,0 +1,154 @@
+"""K4 tcgen05 grouped GEMM vs a plain PyTorch fp32 reference of the same contraction.
+
+Tolerance: bf16 operands, fp32 accumulation; bf16 outputs are compared at rel 2e-2
+(north_star's documented bf16 tolerance), fp32 wgrad outputs at rel 1e-3 of the max.
+"""
+
+import pytest
+import torch
+
+from paper_2605_08639_b200 import kernels as K
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda"
+
+
+def rel_err(got, ref):
+    return ((got.float() - ref.float()).abs().max() / ref.float().abs().max().clamp_min(1e-6)).item()
+
+
+def _row_groups(rows):
+    a0 = [0]
+    for r in rows[:-1]:
+        a0.append(a0[-1] + r)
+    return a0, sum(rows)
+
+
+@pytest.mark.parametrize("rows", [[128], [256, 0, 384, 128], [128] * 9])
+def test_fwd_store(rows):
+    torch.manual_seed(0)
+    N, Kd = 512, 256
+    a0, R = _row_groups(rows)
+    S = len(rows)
+    slots = list(reversed(range(S)))
+    A = torch.randn(R, Kd, device=DEV).bfloat16()
+    W = (torch.randn(S, N, Kd, device=DEV) * Kd ** -0.5).bfloat16()
+    C = torch.full((R, N), float("nan"), device=DEV).bfloat16()
+    K.grouped_gemm(K.GEMM_FWD_STORE, A, W, K.make_groups(rows, a0, slots), N=N, K=Kd, C=C)
+    torch.cuda.synchronize()
+    for g, r in enumerate(rows):
+        if r == 0:
+            continue
+        ref = A[a0[g]:a0[g] + r].float() @ W[slots[g]].float().T
+        assert rel_err(C[a0[g]:a0[g] + r], ref) < 2e-2
+
+
+def test_fwd_replica_map():
+    torch.manual_seed(1)
+    N, Kd = 256, 128
+    rows = [128, 256, 128]
+    a0, R = _row_groups(rows)
+    A = torch.randn(R, Kd, device=DEV).bfloat16()
+    Wh = torch.randn(2, N, Kd, device=DEV).bfloat16()
+    Wr = torch.randn(3, N, Kd, device=DEV).bfloat16()
+    C = torch.zeros(R, N, device=DEV).bfloat16()
+    groups = K.make_groups(rows, a0, [1, 2, 0], [0, K.FLAG_REPLICA, 0])
+    K.grouped_gemm(K.GEMM_FWD_STORE, A, Wh, groups, N=N, K=Kd, C=C, B1=Wr)
+    torch.cuda.synchronize()
+    refs = [A[0:128].float() @ Wh[1].float().T, A[128:384].float() @ Wr[2].float().T, A[384:].float() @ Wh[0].float().T]
+    assert rel_err(C, torch.cat(refs)) < 2e-2
+
+
+def test_fwd_swiglu():
+    torch.manual_seed(2)
+    hp, Kd = 256, 256        # h' = 256 -> 2h' = 512 = two 256-wide tiles (gate|up blocks of 128)
+    rows = [128, 256]
+    a0, R = _row_groups(rows)
+    A = torch.randn(R, Kd, device=DEV).bfloat16()
+    W = (torch.randn(2, 2 * hp, Kd, device=DEV) * Kd ** -0.5).bfloat16()
+    H = torch.zeros(R, 2 * hp, device=DEV).bfloat16()
+    Act = torch.zeros(R, hp, device=DEV).bfloat16()
+    K.grouped_gemm(K.GEMM_FWD_SWIGLU, A, W, K.make_groups(rows, a0, [0, 1]), N=2 * hp, K=Kd, C=H, C2=Act)
+    torch.cuda.synchronize()
+    for g, r in enumerate(rows):
+        h = A[a0[g]:a0[g] + r].float() @ W[g].float().T
+        assert rel_err(H[a0[g]:a0[g] + r], h) < 2e-2
+        hb = h.view(r, -1, 2, 128)
+        act = (torch.nn.functional.silu(hb[:, :, 0]) * hb[:, :, 1]).reshape(r, hp)
+        assert rel_err(Act[a0[g]:a0[g] + r], act) < 2e-2
+
+
+def test_dgrad_store():
+    torch.manual_seed(3)
+    N, Kd = 512, 384
+    rows = [256, 128]
+    a0, R = _row_groups(rows)
+    A = torch.randn(R, Kd, device=DEV).bfloat16()
+    W = (torch.randn(2, Kd, N, device=DEV) * Kd ** -0.5).bfloat16()   # [slot][K][N], N contiguous
+    C = torch.zeros(R, N, device=DEV).bfloat16()
+    K.grouped_gemm(K.GEMM_DGRAD_STORE, A, W, K.make_groups(rows, a0, [1, 0]), N=N, K=Kd, C=C)
+    torch.cuda.synchronize()
+    ref = torch.cat([A[:256].float() @ W[1].float(), A[256:].float() @ W[0].float()])
+    assert rel_err(C, ref) < 2e-2
+
+
+def test_dgrad_dswiglu():
+    torch.manual_seed(4)
+    hp, hd = 256, 512         # dAct = dY[R,h] . W2[h,h'] ; H/dH [R, 2h'] gate|up blocks of 128
+    rows = [128, 128]
+    a0, R = _row_groups(rows)
+    dY = torch.randn(R, hd, device=DEV).bfloat16()
+    W2 = (torch.randn(2, hd, hp, device=DEV) * hd ** -0.5).bfloat16()
+    H = torch.randn(R, 2 * hp, device=DEV).bfloat16()
+    dH = torch.zeros(R, 2 * hp, device=DEV).bfloat16()
+    K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU, dY, W2, K.make_groups(rows, a0, [0, 1]), N=hp, K=hd, C=dH, aux=H)
+    torch.cuda.synchronize()
+    for g in range(2):
+        sl = slice(a0[g], a0[g] + rows[g])
+        da = dY[sl].float() @ W2[g].float()
+        hb = H[sl].float().view(rows[g], -1, 2, 128)
+        gt, up = hb[:, :, 0].reshape(rows[g], hp), hb[:, :, 1].reshape(rows[g], hp)
+        s = torch.sigmoid(gt)
+        dg = da * up * s * (1 + gt * (1 - s))
+        du = da * gt * s
+        ref = torch.stack([dg.view(rows[g], -1, 128), du.view(rows[g], -1, 128)], dim=2).reshape(rows[g], 2 * hp)
+        assert rel_err(dH[sl], ref) < 2e-2
+
+
+def test_wgrad_accumulate():
+    torch.manual_seed(5)
+    Md, Nd = 256, 512
+    krows = [64, 0, 192, 128]
+    a0, R = _row_groups(krows)
+    slots = [2, 0, 1, 3]
+    flags = [K.FLAG_ACCUMULATE, 0, 0, K.FLAG_ACCUMULATE]
+    A = torch.randn(R, Md, device=DEV).bfloat16()
+    B = torch.randn(R, Nd, device=DEV).bfloat16()
+    C0 = torch.randn(4, Md, Nd, device=DEV)
+    C = C0.clone()
+    K.grouped_gemm(K.GEMM_WGRAD, A, B, K.make_groups(krows, a0, slots, flags), M=Md, N=Nd, C=C,
+                   c_slot_stride=Md * Nd)
+    torch.cuda.synchronize()
+    for g, r in enumerate(krows):
+        s = slots[g]
+        if r == 0:
+            assert torch.equal(C[s], C0[s])
+            continue
+        ref = A[a0[g]:a0[g] + r].float().T @ B[a0[g]:a0[g] + r].float()
+        if flags[g] & K.FLAG_ACCUMULATE:
+            ref = ref + C0[s]
+        assert rel_err(C[s], ref) < 1e-3
+
+
+def test_histogram_matches_bincount():
+    torch.manual_seed(6)
+    E, k = 128, 8
+    idx = torch.stack([torch.randperm(E, device=DEV)[:k] for _ in range(1000)]).int()
+    idx = idx.view(2, 500, k).contiguous()
+    counts, chunks = K.expert_histogram(idx, E, chunk_tokens=32)
+    torch.cuda.synchronize()
+    for b in range(2):
+        ref = torch.bincount(idx[b].flatten().long(), minlength=E)
+        assert torch.equal(counts[b].long(), ref)
+        assert torch.equal(chunks[b].sum(0).long(), ref)
