@@ -33,7 +33,9 @@ int mb_expert_histogram(const int32_t* idx, int64_t nb, int64_t tokens, int32_t 
  * tcgen05/TMEM/TMA persistent grouped GEMM (bf16 in, fp32 accumulate).
  * Replaces: costmodel.comp_time (costmodel.py:161-163), the modelled 6*h*h' FLOP/token expert
  * FFN ("three GEMMs").  groups: device array of
- * struct {int32 rows, a0, slot, flags}.                                                       */
+ * struct {int32 rows, a0, slot, flags, seg_begin, seg_count, pad, pad}; segs (W mode only, may be
+ * NULL): device array of struct {int32 a0, rows} K-segments, so one wgrad launch can contract
+ * over every micro-batch of the step.                                                         */
 enum {
   MB_GEMM_FWD_STORE = 0,     /* C[rows_g,N] = A[rows_g,K] . B_slot[N,K]^T           (Y = Act W2^T) */
   MB_GEMM_FWD_SWIGLU = 1,    /* as above, epilogue C=H, C2=silu(gate)*up             (H = X W1^T)   */
@@ -42,7 +44,8 @@ enum {
   MB_GEMM_WGRAD = 4          /* C_slot[M,N] (+)= A[K_g,M]^T . B[K_g,N]               (dW)           */
 };
 int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t a_cols, const void* B0, int64_t b0_rows,
-                    const void* B1, int64_t b1_rows, int64_t b_cols, const void* groups, int num_groups, int M,
+                    const void* B1, int64_t b1_rows, int64_t b_cols, const void* groups, const void* segs,
+                    int num_groups, int M,
                     int N, int K, void* C, int64_t ldc, int64_t c_slot_stride, void* C2, int64_t ldc2,
                     const void* aux, int64_t ld_aux, void* stream);
 

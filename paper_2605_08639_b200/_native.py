@@ -39,12 +39,47 @@ _KERNEL_SIGS = {
     "mb_expert_histogram": (c_int, [c_vp, c_i64, c_i64, c_i32, c_i32, c_vp, c_vp, c_i32, c_vp]),
     "mb_grouped_gemm": (
         c_int,
-        [c_int, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_int, c_int, c_int, c_int,
+        [c_int, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp, c_int, c_int, c_int, c_int,
          c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp],
     ),
 }
 
-_PLANNER_SIGS: dict = {}
+_KERNEL_SIGS.update({
+    "mb_chunk_scan": (c_int, [c_vp, c_vp, c_i64, c_i32, c_i32, c_vp]),
+    "mb_permute_rank": (c_int, [c_vp, c_i64, c_i32, c_vp, c_i32, c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp]),
+    "mb_scatter_rows": (c_int, [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp]),
+    "mb_combine_rows": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
+    "mb_combine_bwd_expert": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i64, c_i32, c_vp]),
+    "mb_zero_pad_rows": (c_int, [c_vp, c_vp, c_i32, c_i32, c_vp]),
+    "mb_accumulate_f32": (c_int, [c_vp, c_vp, c_i32, c_i64, c_vp]),
+    "mb_ipc_malloc": (c_int, [c_i64, ctypes.POINTER(c_vp), c_vp]),
+    "mb_ipc_handle_size": (c_int, []),
+    "mb_ipc_open": (c_int, [c_vp, ctypes.POINTER(c_vp)]),
+    "mb_ipc_close": (c_int, [c_vp]),
+    "mb_device_free": (c_int, [c_vp]),
+    "mb_memcpy_async": (c_int, [c_vp, c_vp, c_i64, c_vp]),
+    "mb_peer_barrier": (c_int, [c_vp, c_i32, c_i32, c_vp, c_i64, c_vp, c_vp]),
+})
+
+_PLANNER_SIGS: dict = {
+    "mbp_last_error": (c_char_p, []),
+    "mbp_use_numpy_blas": (c_int, [c_char_p, c_char_p]),
+    "mbp_numpy_blas_active": (c_int, []),
+    "mbp_static_plan": (c_int, [c_i32, c_i32, c_vp]),
+    "mbp_lpt_initial": (c_int, [c_vp, c_i32, c_i32, c_vp]),
+    "mbp_anneal_reorder": (c_int, [c_vp, c_i32, c_i32, c_i32, c_i64, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_vp,
+                                   c_i32, c_dbl, c_dbl, c_dbl, c_dbl, c_vp, c_i32, c_i32, c_vp, c_vp]),
+    "mbp_compute_loads": (c_int, [c_vp, c_i32, c_i32, c_i32, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "mbp_greedy_replicate": (c_int, [c_vp, c_i32, c_i32, c_i32, c_vp, c_i64, c_i64, c_dbl, c_dbl, c_dbl, c_dbl,
+                                     c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "mbp_solve_token_split": (c_int, [c_vp, c_i32, c_i32, c_i32, c_vp, c_i64, c_i64, c_dbl, c_dbl, c_dbl, c_dbl,
+                                      c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "mbp_round_split": (c_int, [c_vp, c_i32, c_i32, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "mbp_eplb_replication": (c_int, [c_vp, c_i32, c_i32, c_i32, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
+    "mbp_uniform_matrices": (c_int, [c_vp, c_i64, c_i32, c_vp]),
+    "mbp_dispatch_plan": (c_int, [c_i32, c_i32, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32,
+                                  c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+}
 
 _libs: dict[str, ctypes.CDLL] = {}
 
@@ -74,7 +109,25 @@ def kernels() -> ctypes.CDLL:
 
 
 def planner() -> ctypes.CDLL:
-    return _load("libmb_planner.so", _PLANNER_SIGS)
+    fresh = "libmb_planner.so" not in _libs
+    lib = _load("libmb_planner.so", _PLANNER_SIGS)
+    if fresh and os.environ.get("MB_PLANNER_NUMPY_BLAS", "1") != "0":
+        path = numpy_blas_path()
+        if path:
+            lib.mbp_use_numpy_blas(path.encode(), b"scipy_")
+    return lib
+
+
+def numpy_blas_path() -> str | None:
+    """numpy's bundled ILP64 OpenBLAS (the library numpy's matmul calls), if present."""
+    try:
+        import numpy as np
+        for d in (Path(np.__file__).resolve().parent.parent / "numpy.libs",):
+            for p in sorted(d.glob("libscipy_openblas64_*.so")):
+                return str(p)
+    except Exception:  # pragma: no cover
+        return None
+    return None
 
 
 def register_planner_sigs(sigs: dict) -> None:
@@ -84,13 +137,31 @@ def register_planner_sigs(sigs: dict) -> None:
 def check(status: int, lib: ctypes.CDLL, what: str) -> None:
     if status == 0:
         return
-    msg = lib.mb_last_error() if hasattr(lib, "mb_last_error") else None
+    if hasattr(lib, "mbp_last_error"):
+        msg = lib.mbp_last_error()
+    else:
+        msg = lib.mb_last_error() if hasattr(lib, "mb_last_error") else None
     msg = msg.decode() if isinstance(msg, bytes) else str(msg)
     if status == 1:
         raise ValueError(f"{what}: {msg}")
     if status == 5:
         raise LPError(f"{what}: {msg}")
     raise RuntimeError(f"{what} failed (status {status}): {msg}")
+
+
+def f64(a):
+    import numpy as np
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def i64(a):
+    import numpy as np
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def i32(a):
+    import numpy as np
+    return np.ascontiguousarray(a, dtype=np.int32)
 
 
 def ptr(t) -> int | None:

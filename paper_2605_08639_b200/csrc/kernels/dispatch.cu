@@ -1,0 +1,391 @@
+// K2/K3/K6: token permutation, dispatch and combine over NVLink peer pointers.
+//
+// The reference only MODELS this traffic: costmodel.flow_matrix (costmodel.py:91-108) gives
+// flow[src, serving GPU] from the routing matrix, the placement and the split fractions;
+// replicate.round_split (replicate.py:501-525) turns fractions into whole tokens; combine is
+// the mirror of dispatch (costmodel.py:149-150).  Here the same integers drive real row moves.
+//
+// Canonical permutation P (defined by this build, identical in oracle/moe_ref.py):
+//   on source GPU j enumerate (t, i) row-major; e = idx[t,i]; r = stable rank of (t,i) among the
+//   entries of GPU j routed to e; copy c = min{c : r < cum_end[e][c]} where cum_end are the
+//   prefix sums of the integer split counts of (j, e) over copies [home] + replicas
+//   (ReplicaPlacement.copies, replicate.py:55-56); destination (gpu, row) =
+//   (copies[c], row_base[e][c] + r - cum_end[e][c-1]).
+//   row_base is fixed by the receive layout of the destination GPU: slots (home experts
+//   ascending, then replicated experts ascending) x source GPU ascending x rank, each slot padded
+//   to a multiple of 128 rows (the GEMM M tile).
+#include "capi_common.cuh"
+#include "sm100_ptx.cuh"
+#include "../../../include/mb_kernels.h"
+
+namespace mb {
+
+// ------------------------------------------------------------------ chunk prefix scan
+// chunk_base[b][c][e] = sum_{c' < c} chunk_counts[b][c'][e]   (one warp per expert column)
+__global__ void __launch_bounds__(256) chunk_scan_kernel(const uint32_t* __restrict__ chunk_counts,
+                                                         uint32_t* __restrict__ chunk_base, int chunks, int E) {
+  const int b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warps = blockDim.x >> 5;
+  const uint32_t* cc = chunk_counts + static_cast<int64_t>(b) * chunks * E;
+  uint32_t* cb = chunk_base + static_cast<int64_t>(b) * chunks * E;
+  const int per = (chunks + 31) / 32;
+  for (int e = blockIdx.x * warps + warp; e < E; e += gridDim.x * warps) {
+    const int c0 = lane * per;
+    const int c1 = min(c0 + per, chunks);
+    uint32_t s = 0;
+    for (int c = c0; c < c1; ++c) s += cc[static_cast<int64_t>(c) * E + e];
+    uint32_t incl = s;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += v;
+    }
+    uint32_t run = incl - s;
+    for (int c = c0; c < c1; ++c) {
+      cb[static_cast<int64_t>(c) * E + e] = run;
+      run += cc[static_cast<int64_t>(c) * E + e];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K2 stable-rank permutation
+// One warp per chunk of `chunk_tokens` tokens; ranks are stable in row-major (t, i) order.
+// route_tab: [E][maxc][4] int32 {cum_end, dst_gpu, dst_row_base, 0}; ncopies[E].
+__global__ void __launch_bounds__(128) permute_rank_kernel(
+    const int32_t* __restrict__ idx, int64_t T, int k, const float* __restrict__ gate, int E,
+    const uint32_t* __restrict__ chunk_base, int chunk_tokens, const int4* __restrict__ route_tab,
+    const int32_t* __restrict__ ncopies, int maxc, float* const* __restrict__ dst_gate, int2* __restrict__ perm) {
+  extern __shared__ uint32_t running_all[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int chunk = blockIdx.x * (blockDim.x >> 5) + warp;
+  uint32_t* running = running_all + warp * E;
+  for (int e = lane; e < E; e += 32) running[e] = 0;
+  __syncwarp();
+  const int64_t t0 = static_cast<int64_t>(chunk) * chunk_tokens;
+  if (t0 >= T) return;
+  const int64_t t1 = min(t0 + chunk_tokens, T);
+  const int64_t n0 = t0 * k, n1 = t1 * k;
+  const uint32_t* base = chunk_base + static_cast<int64_t>(chunk) * E;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int64_t s = n0; s < n1; s += 32) {
+    const int64_t n = s + lane;
+    const bool valid = n < n1;
+    const int e = valid ? idx[n] : -1;
+    const bool ok = valid && e >= 0 && e < E;
+    const unsigned peers = __match_any_sync(0xffffffffu, ok ? e : -1);
+    const int leader = __ffs(peers) - 1;
+    uint32_t first = 0;
+    if (ok && lane == leader) {
+      first = base[e] + running[e];
+      running[e] += __popc(peers);
+    }
+    first = __shfl_sync(0xffffffffu, first, leader);
+    __syncwarp();
+    if (!ok) {
+      if (valid) perm[n] = make_int2(-1, -1);
+      continue;
+    }
+    const uint32_t r = first + __popc(peers & lt_mask);
+    const int nc = ncopies[e];
+    const int4* tab = route_tab + static_cast<int64_t>(e) * maxc;
+    int prev = 0, c = 0;
+    int4 ent = tab[0];
+    while (c + 1 < nc && static_cast<int>(r) >= ent.x) {
+      prev = ent.x;
+      ent = tab[++c];
+    }
+    const int row = ent.z + static_cast<int>(r) - prev;
+    perm[n] = make_int2(ent.y, row);
+    if (gate && dst_gate) dst_gate[ent.y][row] = gate[n];
+  }
+}
+
+// ------------------------------------------------------------------ K3 scatter (dispatch A2A)
+// Warp per token: the row is read once (128-bit loads) and stored to every (gpu, row) of its
+// k choices, straight into the (possibly peer, NVLink-mapped) receive buffers.
+template <int VPL>
+__global__ void __launch_bounds__(256) scatter_rows_kernel(const uint4* __restrict__ x, int64_t T, int k, int h,
+                                                           const int2* __restrict__ perm, void* const* __restrict__ dst_rows) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp_global = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int vrow = h >> 3;  // uint4 per row
+  for (int64_t t = warp_global; t < T; t += nwarps) {
+    const uint4* src = x + t * vrow;
+    for (int col0 = 0; col0 < vrow; col0 += 32 * VPL) {
+      uint4 v[VPL];
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) {
+        const int col = col0 + j * 32 + lane;
+        if (col < vrow) v[j] = __ldg(src + col);
+      }
+      for (int i = 0; i < k; ++i) {
+        const int2 pr = perm[t * k + i];
+        if (pr.x < 0) continue;
+        uint4* dst = reinterpret_cast<uint4*>(dst_rows[pr.x]) + static_cast<int64_t>(pr.y) * vrow;
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+          const int col = col0 + j * 32 + lane;
+          if (col < vrow) dst[col] = v[j];
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K6 combine (un-permute)
+// out[t] = sum_i w[t,i] * rows[perm(t,i)]  (fp32, fixed i order), w = gate or 1.
+// Optionally gathers a per-row scalar (dgate) back into [T,k] order.
+template <int VPL>
+__global__ void __launch_bounds__(256) combine_rows_kernel(const void* const* __restrict__ src_rows, const int2* __restrict__ perm,
+                                                           const float* __restrict__ gate, int64_t T, int k, int h,
+                                                           uint4* __restrict__ out, const float* const* __restrict__ src_scalar,
+                                                           float* __restrict__ scalar_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp_global = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int vrow = h >> 3;
+  for (int64_t t = warp_global; t < T; t += nwarps) {
+    if (scalar_out && lane < k) {
+      const int2 pr = perm[t * k + lane];
+      scalar_out[t * k + lane] = (pr.x >= 0) ? src_scalar[pr.x][pr.y] : 0.0f;
+    }
+    for (int col0 = 0; col0 < vrow; col0 += 32 * VPL) {
+      float acc[VPL][8];
+#pragma unroll
+      for (int j = 0; j < VPL; ++j)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[j][q] = 0.0f;
+      for (int i = 0; i < k; ++i) {
+        const int2 pr = perm[t * k + i];
+        if (pr.x < 0) continue;
+        const float w = gate ? gate[t * k + i] : 1.0f;
+        const uint4* src = reinterpret_cast<const uint4*>(src_rows[pr.x]) + static_cast<int64_t>(pr.y) * vrow;
+        uint4 v[VPL];
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+          const int col = col0 + j * 32 + lane;
+          if (col < vrow) v[j] = src[col];
+        }
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+          const uint32_t u[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            acc[j][2 * q] += w * bf16lo(u[q]);
+            acc[j][2 * q + 1] += w * bf16hi(u[q]);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) {
+        const int col = col0 + j * 32 + lane;
+        if (col < vrow)
+          out[t * vrow + col] = make_uint4(pack_bf16x2(acc[j][0], acc[j][1]), pack_bf16x2(acc[j][2], acc[j][3]),
+                                           pack_bf16x2(acc[j][4], acc[j][5]), pack_bf16x2(acc[j][6], acc[j][7]));
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ slot-table helpers
+// slot_tab: [nslots][4] int32 {row_begin, rows_real, rows_pad, expert}; slots tile [0, total) in order.
+__device__ __forceinline__ int find_slot(const int4* __restrict__ slots, int nslots, int64_t row) {
+  int lo = 0, hi = nslots - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (slots[mid].x <= row) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Expert-side combine backward (local to the serving GPU):
+//   dY[row] = gate[row] * dout[row] (in place), dgate[row] = <dout[row], Y[row]>; pad rows -> 0.
+template <int VPL>
+__global__ void __launch_bounds__(256) combine_bwd_expert_kernel(uint4* __restrict__ dout_rows, const uint4* __restrict__ y_rows,
+                                                                 const float* __restrict__ gate_rows, float* __restrict__ dgate_rows,
+                                                                 const int4* __restrict__ slots, int nslots, int64_t total_rows, int h) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp_global = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int vrow = h >> 3;
+  for (int64_t row = warp_global; row < total_rows; row += nwarps) {
+    const int4 sl = slots[find_slot(slots, nslots, row)];
+    const bool real = row < static_cast<int64_t>(sl.x) + sl.y;
+    uint4* d = dout_rows + row * vrow;
+    if (!real) {
+      for (int col = lane; col < vrow; col += 32) d[col] = make_uint4(0, 0, 0, 0);
+      if (lane == 0 && dgate_rows) dgate_rows[row] = 0.0f;
+      continue;
+    }
+    const float g = gate_rows[row];
+    const uint4* y = y_rows + row * vrow;
+    float dot = 0.0f;
+    for (int col0 = 0; col0 < vrow; col0 += 32 * VPL) {
+      uint4 dv[VPL], yv[VPL];
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) {
+        const int col = col0 + j * 32 + lane;
+        if (col < vrow) { dv[j] = d[col]; yv[j] = y[col]; }
+      }
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) {
+        const int col = col0 + j * 32 + lane;
+        if (col >= vrow) continue;
+        const uint32_t du[4] = {dv[j].x, dv[j].y, dv[j].z, dv[j].w};
+        const uint32_t yu[4] = {yv[j].x, yv[j].y, yv[j].z, yv[j].w};
+        uint32_t o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float d0 = bf16lo(du[q]), d1 = bf16hi(du[q]);
+          dot += d0 * bf16lo(yu[q]) + d1 * bf16hi(yu[q]);
+          o[q] = pack_bf16x2(g * d0, g * d1);
+        }
+        d[col] = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
+    if (lane == 0 && dgate_rows) dgate_rows[row] = dot;
+  }
+}
+
+// Zero the pad rows [row_begin + rows_real, row_begin + rows_pad) of every slot.
+__global__ void __launch_bounds__(256) zero_pad_rows_kernel(uint4* __restrict__ rows, const int4* __restrict__ slots, int h) {
+  const int4 sl = slots[blockIdx.x];
+  const int vrow = h >> 3;
+  const int64_t r0 = static_cast<int64_t>(sl.x) + sl.y, r1 = static_cast<int64_t>(sl.x) + sl.z;
+  const int64_t n = (r1 - r0) * vrow;
+  uint4* base = rows + r0 * vrow;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) base[i] = make_uint4(0, 0, 0, 0);
+}
+
+// dst[i] += sum_s srcs[s][i]  (fp32, sources in list order: deterministic replica-grad reduce)
+__global__ void __launch_bounds__(256) accumulate_f32_kernel(float4* __restrict__ dst, const float4* const* __restrict__ srcs,
+                                                             int nsrc, int64_t n4) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float4 a = dst[i];
+    for (int s = 0; s < nsrc; ++s) {
+      const float4 b = srcs[s][i];
+      a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    }
+    dst[i] = a;
+  }
+}
+
+inline int grid_for(int64_t work_items, int per_block) {
+  int64_t g = (work_items + per_block - 1) / per_block;
+  const int64_t cap = static_cast<int64_t>(device_sm_count()) * 8;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+}  // namespace mb
+
+using namespace mb;
+
+extern "C" int mb_chunk_scan(const uint32_t* chunk_counts, uint32_t* chunk_base, int64_t nb, int32_t chunks, int32_t E,
+                             void* stream) {
+  MB_CHECK_ARG(chunk_counts && chunk_base && nb >= 0 && chunks >= 0 && E >= 1, "bad chunk scan args");
+  if (nb == 0 || chunks == 0) return MB_OK;
+  dim3 grid((E + 7) / 8, static_cast<unsigned>(nb));
+  chunk_scan_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(chunk_counts, chunk_base, chunks, E);
+  MB_CUDA_TRY(cudaGetLastError());
+  return MB_OK;
+}
+
+extern "C" int mb_permute_rank(const int32_t* idx, int64_t T, int32_t k, const float* gate, int32_t E,
+                               const uint32_t* chunk_base, int32_t chunk_tokens, const int32_t* route_tab,
+                               const int32_t* ncopies, int32_t maxc, float* const* dst_gate, int32_t* perm,
+                               void* stream) {
+  MB_CHECK_ARG(T >= 0 && k >= 1 && E >= 1 && E <= 2048 && chunk_tokens >= 1 && maxc >= 1, "bad permute args");
+  MB_CHECK_ARG(idx && chunk_base && route_tab && ncopies && perm, "null permute operand");
+  if (T == 0) return MB_OK;
+  const int64_t chunks = (T + chunk_tokens - 1) / chunk_tokens;
+  const int wpb = 4;
+  const int64_t grid = (chunks + wpb - 1) / wpb;
+  permute_rank_kernel<<<static_cast<unsigned>(grid), 32 * wpb, wpb * E * sizeof(uint32_t),
+                        reinterpret_cast<cudaStream_t>(stream)>>>(
+      idx, T, k, gate, E, chunk_base, chunk_tokens, reinterpret_cast<const int4*>(route_tab), ncopies, maxc, dst_gate,
+      reinterpret_cast<int2*>(perm));
+  MB_CUDA_TRY(cudaGetLastError());
+  return MB_OK;
+}
+
+
+extern "C" int mb_scatter_rows(const void* x, int64_t T, int32_t k, int32_t h, const int32_t* perm,
+                               void* const* dst_rows, void* stream) {
+  MB_CHECK_ARG(x && perm && dst_rows && T >= 0 && k >= 1 && h >= 8 && h % 8 == 0, "bad scatter args");
+  if (T == 0) return MB_OK;
+  const int grid = grid_for(T, 8);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int vrow = h / 8;
+  if (vrow <= 64)
+    scatter_rows_kernel<2><<<grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(x), T, k, h, reinterpret_cast<const int2*>(perm), dst_rows);
+  else if (vrow <= 128)
+    scatter_rows_kernel<4><<<grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(x), T, k, h, reinterpret_cast<const int2*>(perm), dst_rows);
+  else
+    scatter_rows_kernel<8><<<grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(x), T, k, h, reinterpret_cast<const int2*>(perm), dst_rows);
+  MB_CUDA_TRY(cudaGetLastError());
+  return MB_OK;
+}
+
+extern "C" int mb_combine_rows(const void* const* src_rows, const int32_t* perm, const float* gate, int64_t T, int32_t k,
+                               int32_t h, void* out, const float* const* src_scalar, float* scalar_out, void* stream) {
+  MB_CHECK_ARG(src_rows && perm && out && T >= 0 && k >= 1 && k <= 32 && h >= 8 && h % 8 == 0, "bad combine args");
+  MB_CHECK_ARG((scalar_out == nullptr) == (src_scalar == nullptr), "src_scalar and scalar_out go together");
+  if (T == 0) return MB_OK;
+  const int grid = grid_for(T, 8);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int vrow = h / 8;
+  const int2* pr = reinterpret_cast<const int2*>(perm);
+  uint4* o = reinterpret_cast<uint4*>(out);
+  if (vrow <= 64)
+    combine_rows_kernel<2><<<grid, 256, 0, s>>>(src_rows, pr, gate, T, k, h, o, src_scalar, scalar_out);
+  else if (vrow <= 128)
+    combine_rows_kernel<4><<<grid, 256, 0, s>>>(src_rows, pr, gate, T, k, h, o, src_scalar, scalar_out);
+  else
+    combine_rows_kernel<8><<<grid, 256, 0, s>>>(src_rows, pr, gate, T, k, h, o, src_scalar, scalar_out);
+  MB_CUDA_TRY(cudaGetLastError());
+  return MB_OK;
+}
+
+extern "C" int mb_combine_bwd_expert(void* dout_rows, const void* y_rows, const float* gate_rows, float* dgate_rows,
+                                     const int32_t* slot_tab, int32_t nslots, int64_t total_rows, int32_t h,
+                                     void* stream) {
+  MB_CHECK_ARG(dout_rows && y_rows && gate_rows && slot_tab && nslots >= 0 && h % 8 == 0, "bad combine_bwd args");
+  if (total_rows == 0 || nslots == 0) return MB_OK;
+  const int grid = grid_for(total_rows, 8);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int vrow = h / 8;
+  const int4* sl = reinterpret_cast<const int4*>(slot_tab);
+  if (vrow <= 64)
+    combine_bwd_expert_kernel<2><<<grid, 256, 0, s>>>(reinterpret_cast<uint4*>(dout_rows), reinterpret_cast<const uint4*>(y_rows), gate_rows, dgate_rows, sl, nslots, total_rows, h);
+  else if (vrow <= 128)
+    combine_bwd_expert_kernel<4><<<grid, 256, 0, s>>>(reinterpret_cast<uint4*>(dout_rows), reinterpret_cast<const uint4*>(y_rows), gate_rows, dgate_rows, sl, nslots, total_rows, h);
+  else
+    combine_bwd_expert_kernel<8><<<grid, 256, 0, s>>>(reinterpret_cast<uint4*>(dout_rows), reinterpret_cast<const uint4*>(y_rows), gate_rows, dgate_rows, sl, nslots, total_rows, h);
+  MB_CUDA_TRY(cudaGetLastError());
+  return MB_OK;
+}
+
+extern "C" int mb_zero_pad_rows(void* rows, const int32_t* slot_tab, int32_t nslots, int32_t h, void* stream) {
+  MB_CHECK_ARG(rows && slot_tab && nslots >= 0 && h % 8 == 0, "bad zero_pad args");
+  if (nslots == 0) return MB_OK;
+  zero_pad_rows_kernel<<<nslots, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<uint4*>(rows), reinterpret_cast<const int4*>(slot_tab), h);
+  MB_CUDA_TRY(cudaGetLastError());
+  return MB_OK;
+}
+
+extern "C" int mb_accumulate_f32(float* dst, const float* const* srcs, int32_t nsrc, int64_t n, void* stream) {
+  MB_CHECK_ARG(dst && (nsrc == 0 || srcs) && n % 4 == 0, "bad accumulate args (n must be a multiple of 4)");
+  if (n == 0 || nsrc == 0) return MB_OK;
+  accumulate_f32_kernel<<<grid_for(n / 4, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<float4*>(dst), reinterpret_cast<const float4* const*>(srcs), nsrc, n / 4);
+  MB_CUDA_TRY(cudaGetLastError());
+  return MB_OK;
+}

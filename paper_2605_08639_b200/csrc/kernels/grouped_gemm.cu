@@ -24,7 +24,7 @@ using namespace mb;
 
 extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t a_cols, const void* B0,
                                int64_t b0_rows, const void* B1, int64_t b1_rows, int64_t b_cols,
-                               const void* groups, int num_groups, int M, int N, int K, void* C, int64_t ldc,
+                               const void* groups, const void* segs, int num_groups, int M, int N, int K, void* C, int64_t ldc,
                                int64_t c_slot_stride, void* C2, int64_t ldc2, const void* aux, int64_t ld_aux,
                                void* stream) {
   MB_CHECK_ARG(num_groups >= 0 && num_groups <= kMaxGroups, "num_groups %d outside [0, %d]", num_groups, kMaxGroups);
@@ -34,6 +34,7 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
   if (!B1) { B1 = B0; b1_rows = b0_rows; }
   GemmParams p{};
   p.groups = reinterpret_cast<const GemmGroup*>(groups);
+  p.segs = reinterpret_cast<const GemmSeg*>(segs);
   p.num_groups = num_groups;
   p.M = M; p.N = N; p.K = K;
   p.C = C; p.ldc = ldc; p.c_slot_stride = c_slot_stride;

@@ -27,12 +27,19 @@ enum GemmEpi : int {
   EPI_ACC_F32 = 3,     // C_slot (+)= acc (fp32)
 };
 
-// Per-group descriptor (device memory, written by the plan-table kernel or host).
+// Per-group descriptor (device memory, written by the dispatch-plan tables).
 struct GemmGroup {
-  int32_t rows;   // F: rows of the group (multiple of 128). W: K rows (multiple of 64).
-  int32_t a0;     // F: first row in A (and C). W: first token row in A and B.
-  int32_t slot;   // F: weight slot index in the selected B tensor. W: output slot.
-  int32_t flags;  // bit0: accumulate into C (W). bit1: B from tensor map 1 (replica slots).
+  int32_t rows;       // F: rows of the group (multiple of 128). W: total K rows (multiple of 64).
+  int32_t a0;         // F: first row in A (and C). W: first token row in A and B (single segment).
+  int32_t slot;       // F: weight slot index in the selected B tensor. W: output slot.
+  int32_t flags;      // bit0: accumulate into C (W). bit1: B from tensor map 1 (replica slots).
+  int32_t seg_begin;  // W: first entry in the segment table (K split over micro-batches)
+  int32_t seg_count;  // W: number of segments; 0 means the single segment (a0, rows)
+  int32_t pad0, pad1;
+};
+// W-mode K segment: `rows` token rows (multiple of 64) starting at token row `a0`.
+struct GemmSeg {
+  int32_t a0, rows;
 };
 
 constexpr int kMaxGroups = 256;
@@ -44,6 +51,7 @@ struct GemmParams {
   CUtensorMap tmB0;
   CUtensorMap tmB1;
   const GemmGroup* groups;
+  const GemmSeg* segs;
   int num_groups;
   int M, N, K;          // F: N, K used; W: M, N used
   void* C;
@@ -61,7 +69,7 @@ struct GemmCfg {
   static constexpr int kABytes = BM * BK * 2;
   static constexpr int kBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kMetaBytes = 8192;  // barriers + group table + tile starts
+  static constexpr int kMetaBytes = 10240;  // barriers + tile starts + group table
   static constexpr int kSmemBytes = kStages * kStageBytes + kMetaBytes + 1024;  // +1024 alignment slack
 };
 
@@ -103,7 +111,7 @@ __global__ void __launch_bounds__(192, 1) grouped_gemm_kernel(const __grid_const
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   int* tile_start = reinterpret_cast<int*>(meta + 256);                      // kMaxGroups+1 ints
-  GemmGroup* sg = reinterpret_cast<GemmGroup*>(meta + 256 + 4 * (kMaxGroups + 4));
+  GemmGroup* sg = reinterpret_cast<GemmGroup*>(meta + 256 + 4 * (kMaxGroups + 8));
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -166,7 +174,19 @@ __global__ void __launch_bounds__(192, 1) grouped_gemm_kernel(const __grid_const
         const TileCoord tc = decode_tile<kW, BN>(t, tile_start, sg, ng, p);
         const GemmGroup gg = sg[tc.g];
         const CUtensorMap* tmB = (gg.flags & 2) ? &p.tmB1 : &p.tmB0;
+        // W mode: walk the K segments (one per micro-batch); F mode: a single implicit segment
+        int seg = 0, seg_row = gg.a0, seg_left = kW ? (gg.seg_count ? 0 : gg.rows / BK) : tc.kblocks;
         for (int kb = 0; kb < tc.kblocks; ++kb) {
+          if (kW) {
+            while (seg_left == 0) {
+              const GemmSeg sgm = p.segs[gg.seg_begin + seg++];
+              seg_row = sgm.a0;
+              seg_left = sgm.rows / BK;
+            }
+            --seg_left;
+          }
+          const int krow = seg_row;  // W: token row of this k-block
+          if (kW) seg_row += BK;
           mbar_wait(&empty_bar[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
           uint8_t* a_dst = sA + stage * Cfg::kABytes;
@@ -178,12 +198,12 @@ __global__ void __launch_bounds__(192, 1) grouped_gemm_kernel(const __grid_const
             // A MN-major (W): inner = M, outer = token rows
 #pragma unroll
             for (int j = 0; j < BM / 64; ++j)
-              tma_load_2d(a_dst + j * 8192, &p.tmA, &full_bar[stage], tc.mb * BM + j * 64, gg.a0 + kb * BK);
+              tma_load_2d(a_dst + j * 8192, &p.tmA, &full_bar[stage], tc.mb * BM + j * 64, krow);
           }
           if (!kBmn) {
             tma_load_2d(b_dst, tmB, &full_bar[stage], kb * BK, gg.slot * p.N + tc.nb * BN);
           } else {
-            const int row0 = kW ? (gg.a0 + kb * BK) : (gg.slot * p.K + kb * BK);
+            const int row0 = kW ? krow : (gg.slot * p.K + kb * BK);
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j)
               tma_load_2d(b_dst + j * 8192, tmB, &full_bar[stage], tc.nb * BN + j * 64, row0);

@@ -17,7 +17,7 @@ GEMM_DGRAD_STORE = 2
 GEMM_DGRAD_DSWIGLU = 3
 GEMM_WGRAD = 4
 
-GROUP_FIELDS = 4  # int32 rows, a0, slot, flags
+GROUP_FIELDS = 8  # int32 rows, a0, slot, flags, seg_begin, seg_count, pad, pad
 FLAG_ACCUMULATE = 1
 FLAG_REPLICA = 2
 
@@ -32,12 +32,17 @@ def _need_cuda(*tensors):
             raise ValueError("data-plane ops take CUDA tensors (there is no CPU path)")
 
 
-def make_groups(rows, a0, slot, flags=None, device="cuda") -> torch.Tensor:
-    """Pack per-group (rows, a0, slot, flags) into the int32 [G, 4] device table."""
+def make_groups(rows, a0, slot, flags=None, seg_begin=None, seg_count=None, device="cuda") -> torch.Tensor:
+    """Pack per-group (rows, a0, slot, flags, seg_begin, seg_count) into the int32 [G, 8] table."""
     n = len(rows)
-    flags = [0] * n if flags is None else flags
-    tab = np.stack([np.asarray(rows), np.asarray(a0), np.asarray(slot), np.asarray(flags)], axis=1).astype(np.int32)
-    return torch.from_numpy(tab.reshape(n, GROUP_FIELDS)).to(device)
+    z = [0] * n
+    flags = z if flags is None else flags
+    seg_begin = z if seg_begin is None else seg_begin
+    seg_count = z if seg_count is None else seg_count
+    tab = np.zeros((n, GROUP_FIELDS), dtype=np.int32)
+    for c, v in enumerate((rows, a0, slot, flags, seg_begin, seg_count)):
+        tab[:, c] = np.asarray(v, dtype=np.int64)
+    return torch.from_numpy(tab).to(device)
 
 
 def expert_histogram(idx: torch.Tensor, num_experts: int, chunk_tokens: int = 32,
@@ -63,7 +68,8 @@ def expert_histogram(idx: torch.Tensor, num_experts: int, chunk_tokens: int = 32
 
 def grouped_gemm(mode: int, A: torch.Tensor, B0: torch.Tensor, groups: torch.Tensor, *, M: int = 0, N: int,
                  K: int = 0, C: torch.Tensor, C2: torch.Tensor | None = None, aux: torch.Tensor | None = None,
-                 B1: torch.Tensor | None = None, c_slot_stride: int = 0) -> None:
+                 B1: torch.Tensor | None = None, c_slot_stride: int = 0,
+                 segs: torch.Tensor | None = None) -> None:
     """K4: tcgen05 grouped GEMM; see include/mb_kernels.h for the five modes."""
     _need_cuda(A, B0, groups, C, C2, aux, B1)
     for t in (A, B0, B1):
@@ -81,7 +87,8 @@ def grouped_gemm(mode: int, A: torch.Tensor, B0: torch.Tensor, groups: torch.Ten
     ld_aux = 0 if aux is None else aux.shape[-1]
     lib = _lib()
     nat.check(lib.mb_grouped_gemm(mode, A.data_ptr(), a_rows, a_cols, B0.data_ptr(), b0_rows,
-                                  nat.ptr(B1), b1_rows, b_cols, groups.data_ptr(), groups.shape[0], M, N, K,
+                                  nat.ptr(B1), b1_rows, b_cols, groups.data_ptr(), nat.ptr(segs), groups.shape[0],
+                                  M, N, K,
                                   C.data_ptr(), ldc, c_slot_stride, nat.ptr(C2), ldc2, nat.ptr(aux), ld_aux,
                                   nat.stream_ptr()),
               lib, "mb_grouped_gemm")

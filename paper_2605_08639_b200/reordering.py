@@ -1,0 +1,133 @@
+"""Inter-batch expert reordering (static blocks, LPT, simulated annealing).
+
+Mirror of the hot-path part of ``moebalance.reorder`` (reorder.py:30-362).  The planners run
+in libmb_planner.so: LPT and static are exact; the annealer reproduces the reference's numpy
+PCG64 stream (SeedSequence(seed) per chain), swap proposals, Metropolis test and numpy's
+summation order, and runs the chains of one layer in parallel threads (results gathered in
+seed order, so the plan does not depend on the thread count).
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from . import _native as nat
+from .cluster import ClusterTopology, HardwareProfile
+
+
+@dataclass
+class ReorderPlan:
+    """Capacity-preserving expert -> GPU assignment of one layer."""
+
+    assignment: np.ndarray
+
+    def experts_on(self, gpu: int) -> np.ndarray:
+        return np.flatnonzero(self.assignment == gpu)
+
+    def copy(self) -> "ReorderPlan":
+        return ReorderPlan(self.assignment.copy())
+
+    def validate(self, topo: ClusterTopology) -> None:
+        g = topo.num_gpus
+        if len(self.assignment) % g:
+            raise ValueError("expert count not divisible by GPU count")
+        counts = np.bincount(self.assignment, minlength=g)
+        per = len(self.assignment) // g
+        if (counts != per).any():
+            raise ValueError(f"plan is not capacity-preserving: counts {counts.tolist()}, expected {per} per GPU")
+
+
+@dataclass(frozen=True)
+class AnnealConfig:
+    """Chain seeds, geometric cooling and LSE sharpness (reorder.py:53-78)."""
+
+    seeds: tuple = tuple(range(16))
+    cooling_rate: float = 0.9995
+    termination_eps: float | None = None
+    eps_frac: float = 1e-3
+    beta: float = 20.0
+
+    def __post_init__(self) -> None:
+        if len(self.seeds) < 1:
+            raise ValueError("need at least one annealing seed")
+        if not 0 < self.cooling_rate < 1:
+            raise ValueError(f"cooling_rate must be in (0, 1), got {self.cooling_rate}")
+        if self.termination_eps is not None and not self.termination_eps > 0:
+            raise ValueError("termination_eps must be > 0")
+        if not self.eps_frac > 0:
+            raise ValueError("eps_frac must be > 0")
+        if not self.beta > 0:
+            raise ValueError("beta must be > 0")
+
+    def eps_for(self, theta0: float) -> float:
+        return self.termination_eps if self.termination_eps is not None else self.eps_frac * theta0
+
+
+@dataclass
+class SamplePlacement:
+    source_gpu: np.ndarray
+
+
+def static_plan(num_experts: int, topo: ClusterTopology) -> ReorderPlan:
+    """No-balancing baseline: experts [g*M, (g+1)*M) on GPU g (reorder.py:291-296)."""
+    g = topo.num_gpus
+    if num_experts % g:
+        raise ValueError(f"{num_experts} experts not divisible by {g} GPUs")
+    out = np.zeros(num_experts, dtype=np.int64)
+    lib = nat.planner()
+    nat.check(lib.mbp_static_plan(num_experts, g, nat.ptr(out)), lib, "static_plan")
+    return ReorderPlan(out)
+
+
+def lpt_initial(x_batch, topo: ClusterTopology) -> ReorderPlan:
+    """Heaviest expert to the least-loaded open GPU, ties to the lower index (reorder.py:265-288)."""
+    x = nat.f64(x_batch)
+    g = topo.num_gpus
+    if x.shape[1] % g:
+        raise ValueError(f"{x.shape[1]} experts not divisible by {g} GPUs")
+    out = np.zeros(x.shape[1], dtype=np.int64)
+    lib = nat.planner()
+    nat.check(lib.mbp_lpt_initial(nat.ptr(x), g, x.shape[1], nat.ptr(out)), lib, "lpt_initial")
+    return ReorderPlan(out)
+
+
+def anneal_reorder(x_batch, topo: ClusterTopology, model, hw: HardwareProfile, cfg: AnnealConfig,
+                   extra_initial_plans: Sequence[ReorderPlan] = (), threads: int | None = None) -> ReorderPlan:
+    """Swap SA from LPT; best exact T_MoE over [LPT, extra plans, chains in seed order]
+    (reorder.py:329-362).  `threads` (extension): chain parallelism, default all cores."""
+    x = nat.f64(x_batch)
+    num_experts = x.shape[1]
+    if num_experts % topo.num_gpus:
+        raise ValueError(f"{num_experts} experts not divisible by {topo.num_gpus} GPUs")
+    for plan in extra_initial_plans:
+        plan.validate(topo)
+    extra = nat.i64(np.stack([np.asarray(p.assignment) for p in extra_initial_plans])
+                    if extra_initial_plans else np.zeros((0, num_experts)))
+    seeds = np.ascontiguousarray([int(s) for s in cfg.seeds], dtype=np.uint64)
+    out = np.zeros(num_experts, dtype=np.int64)
+    iters = np.zeros(1, dtype=np.int64)
+    nthreads = threads if threads is not None else (os.cpu_count() or 1)
+    lib = nat.planner()
+    nat.check(lib.mbp_anneal_reorder(
+        nat.ptr(x), topo.num_nodes, topo.gpus_per_node, num_experts, model.hidden_size, model.intermediate_size,
+        hw.flops_per_gpu, hw.bw_nvlink, hw.bw_rdma, hw.bytes_per_token, nat.ptr(seeds), len(seeds),
+        cfg.cooling_rate, cfg.eps_frac, cfg.termination_eps if cfg.termination_eps is not None else -1.0,
+        cfg.beta, nat.ptr(extra), len(extra_initial_plans), nthreads, nat.ptr(out), nat.ptr(iters)),
+        lib, "anneal_reorder")
+    return ReorderPlan(out)
+
+
+def apply_plan(x, plan: ReorderPlan, placement: SamplePlacement | None = None, trace=None,
+               micro_batch: int | None = None, layer: int | None = None) -> np.ndarray:
+    """Expert relocation never changes matrix values (reorder.py:575-607); sample relocation
+    (data-locality placement) is out of scope for this build."""
+    x = np.asarray(x, dtype=np.float64)
+    if x.shape[1] != len(plan.assignment):
+        raise ValueError(f"matrix has {x.shape[1]} experts, plan covers {len(plan.assignment)}")
+    if placement is not None:
+        raise NotImplementedError("sample relocation (reorder.py:365-627) is outside the data-plane scope")
+    return x.copy()

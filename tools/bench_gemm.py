@@ -1,0 +1,70 @@
+"""Micro-benchmark of the K4 grouped GEMM modes at MoE-layer shapes (CUDA events).
+
+usage: python tools/bench_gemm.py [--rows-per-group 512] [--groups 128] [--h 2048] [--hp 768]
+"""
+
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2605_08639_b200 import kernels as K  # noqa: E402
+
+
+def timeit(fn, iters=20, warmup=3):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--rows-per-group", type=int, default=512)
+    ap.add_argument("--groups", type=int, default=128)
+    ap.add_argument("--h", type=int, default=2048)
+    ap.add_argument("--hp", type=int, default=768)
+    a = ap.parse_args()
+    G, r, h, hp = a.groups, a.rows_per_group, a.h, a.hp
+    R = G * r
+    dev = "cuda"
+    rows = [r] * G
+    a0 = [i * r for i in range(G)]
+    groups = K.make_groups(rows, a0, list(range(G)))
+    wg = K.make_groups(rows, a0, list(range(G)), [K.FLAG_ACCUMULATE] * G)
+    X = torch.randn(R, h, device=dev).bfloat16()
+    W1 = (torch.randn(G, 2 * hp, h, device=dev) * 0.02).bfloat16()
+    W2 = (torch.randn(G, h, hp, device=dev) * 0.02).bfloat16()
+    H = torch.empty(R, 2 * hp, device=dev).bfloat16()
+    Act = torch.empty(R, hp, device=dev).bfloat16()
+    Y = torch.empty(R, h, device=dev).bfloat16()
+    dY = torch.randn(R, h, device=dev).bfloat16()
+    dH = torch.empty(R, 2 * hp, device=dev).bfloat16()
+    dX = torch.empty(R, h, device=dev).bfloat16()
+    gW1 = torch.zeros(G, 2 * hp, h, device=dev)
+    gW2 = torch.zeros(G, h, hp, device=dev)
+    flop = 2.0 * R * h * hp
+    res = {}
+    res["fwd1_swiglu"] = (timeit(lambda: K.grouped_gemm(K.GEMM_FWD_SWIGLU, X, W1, groups, N=2 * hp, K=h, C=H, C2=Act)), 2 * flop)
+    res["fwd2_store"] = (timeit(lambda: K.grouped_gemm(K.GEMM_FWD_STORE, Act, W2, groups, N=h, K=hp, C=Y)), flop)
+    res["dgrad_dswiglu"] = (timeit(lambda: K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU, dY, W2, groups, N=hp, K=h, C=dH, aux=H)), flop)
+    res["dgrad_dx"] = (timeit(lambda: K.grouped_gemm(K.GEMM_DGRAD_STORE, dH, W1, groups, N=h, K=2 * hp, C=dX)), 2 * flop)
+    res["wgrad_w2"] = (timeit(lambda: K.grouped_gemm(K.GEMM_WGRAD, dY, Act, wg, M=h, N=hp, C=gW2, c_slot_stride=h * hp)), flop)
+    res["wgrad_w1"] = (timeit(lambda: K.grouped_gemm(K.GEMM_WGRAD, dH, X, wg, M=2 * hp, N=h, C=gW1, c_slot_stride=2 * hp * h)), 2 * flop)
+    out = {k: {"ms": round(v[0], 4), "tflops": round(v[1] / v[0] / 1e9, 1)} for k, v in res.items()}
+    tot_ms = sum(v[0] for v in res.values())
+    out["total"] = {"ms": round(tot_ms, 4), "tflops": round(9 * flop / tot_ms / 1e9, 1)}
+    print(json.dumps({"shape": {"groups": G, "rows": r, "h": h, "hp": hp}, "gemm": out}))
+
+
+if __name__ == "__main__":
+    main()
