@@ -1,0 +1,459 @@
+"""The MoE-layer training step under replayed routing, on B200.
+
+This is the data plane the reference only models (sim.evaluate_bundle, sim.py:89-110:
+flow_matrix -> comp = flow.sum(0) -> dispatch/combine link loads -> T = max comp + max comm).
+Per micro-batch, on every rank (one process per GPU):
+
+  K1  expert histogram of the local top-k indices (+ chunk scan)           histogram.cu
+  K5  replica weight push into the layer-shared replica slots (owners)      copy engine, peer
+  K2  stable-rank permutation -> (dst GPU, dst row) per (token, choice)    dispatch.cu
+  K3  row scatter straight into peer receive buffers (dispatch A2A)         dispatch.cu
+  K4  tcgen05 grouped GEMM: H = X W1^T (+SwiGLU), Y = Act W2^T              grouped_gemm.cu
+  K6  combine: out[t] = sum_i gate[t,i] * Y[perm(t,i)] over peer loads      dispatch.cu
+  bwd K3 (dout scatter) -> expert-side dY = gate*dout, dgate = <dout,Y> -> K4 dAct(+dSwiGLU),
+      dX -> K6 un-permute sum + dgate gather
+and once per step K4 wgrad for every local slot with K split over all micro-batches (the
+fp32 weight-gradient accumulation window), then K5^T: owners pull replica gradients.
+
+Routing is replayed, so every count, row offset and replica is known before the step: the
+host planners run once per step (StepPlan) and the kernels never exchange sizes.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from . import kernels as K
+from . import policies as pol
+from . import reordering as ro
+from . import replication as rep
+from . import traces as rt
+from .cluster import ClusterTopology, HardwareProfile
+from .comm import Comm, SymmetricArena
+
+PAD = 128       # receive-slot row padding = GEMM M tile
+CHUNK = 32      # tokens per permutation chunk
+GATE_BLOCK = 128  # gate|up interleave block of W1 rows (= half the 256-wide SwiGLU tile)
+
+
+@dataclass(frozen=True)
+class LayerShape:
+    num_experts: int
+    top_k: int
+    hidden: int
+    ffn: int
+
+    def check(self) -> None:
+        if self.hidden % 256 or self.ffn % 128:
+            raise ValueError("kernels need hidden % 256 == 0 and ffn % 128 == 0")
+
+
+@dataclass
+class MicroBatchPlan:
+    placement: rep.ReplicaPlacement
+    counts: dict                    # expert -> (G, copies) int64 (round_split)
+    route_tab: np.ndarray           # [G][E][maxc][4]
+    ncopies: np.ndarray             # [E]
+    slot_tab: np.ndarray            # [G][max_slots][4] {row_begin, rows_real, rows_pad, expert}
+    slot_w: np.ndarray              # [G][max_slots][2] {weight slot, replica}
+    nslots: np.ndarray              # [G]
+    total_rows: np.ndarray          # [G]
+    flow: np.ndarray                # [G][G] rows src -> dst
+
+
+@dataclass
+class StepPlan:
+    """Everything the step needs, identical on every rank (built from the gathered routing)."""
+
+    policy: str
+    shape: LayerShape
+    world: int
+    home: np.ndarray                # (E,) ReorderPlan.assignment
+    mbs: list = field(default_factory=list)
+    maxc: int = 1
+    max_slots: int = 1
+    rows_cap: int = PAD
+    rep_experts: list = field(default_factory=list)   # per GPU: sorted experts replicated onto it this step
+    slots: int = 0
+
+    @property
+    def home_local(self) -> list:
+        return [np.flatnonzero(self.home == g) for g in range(self.world)]
+
+    def executed_loads(self) -> np.ndarray:
+        """(MB, G) GEMM rows per GPU actually executed (= costmodel comp with integer splits)."""
+        return np.stack([mb.flow.sum(axis=0) for mb in self.mbs])
+
+    def skew(self) -> float:
+        loads = self.executed_loads()
+        return float(np.mean([rt.skewness(l) for l in loads]))
+
+
+def build_step_plan(policy: str, mats: np.ndarray, topo: ClusterTopology, model: rt.ModelProfile,
+                    hw: HardwareProfile, cfgs: pol.SimConfigs, shape: LayerShape) -> StepPlan:
+    """Plan one step (one batch of MB micro-batches, one layer) from the gathered (MB, G, E)
+    routing matrices, with the reference policies (sim.build_policy_bundle, sim.py:214-280).
+    'balanced_oracle' is planned like 'static': its token routing must already be uniform."""
+    mbs_n, g, e = mats.shape
+    trace = rt.build_trace(model, topo, mats[:, None], tokens_per_gpu=0)
+    pol_name = "static" if policy == "balanced_oracle" else policy
+    bundle, _ = pol.build_policy_bundle(trace, pol_name, topo, model, hw, cfgs)
+    home = np.asarray(bundle.reorder[0].assignment, dtype=np.int64)
+    plan = StepPlan(policy=policy, shape=shape, world=g, home=home, slots=cfgs.replica.slots_per_gpu)
+    entries = []
+    for mb in range(mbs_n):
+        x = mats[mb].astype(np.float64)
+        entry = bundle.replication.entries.get((mb, 0))
+        if entry is None:
+            placement, split = rep.ReplicaPlacement(home=home.copy()), rep.SplitPlan()
+        else:
+            placement, split = entry.placement, entry.split
+        counts = rep.round_split(split, placement, x)
+        entries.append((placement, counts))
+    plan.maxc = max([1] + [1 + len(p.replicas.get(ex, [])) for p, _ in entries for ex in p.replicas])
+    plan.max_slots = e // g + max(1, cfgs.replica.slots_per_gpu)
+    lib = nat.planner()
+    for mb, (placement, counts) in enumerate(entries):
+        x = np.ascontiguousarray(mats[mb], dtype=np.int64)
+        order = list(placement.replicas.keys())
+        rep_e = nat.i32(order)
+        ptrs, gpus, cnts = [0], [], []
+        for ex in order:
+            gpus.extend(placement.replicas[ex])
+            ptrs.append(len(gpus))
+            cnts.append(np.ascontiguousarray(counts[ex], dtype=np.int64).ravel())
+        rep_p, rep_g = nat.i32(ptrs), nat.i32(gpus)
+        cnt = nat.i64(np.concatenate(cnts) if cnts else np.zeros(0))
+        route = np.zeros((g, e, plan.maxc, 4), dtype=np.int32)
+        ncop = np.zeros(e, dtype=np.int32)
+        slot_tab = np.zeros((g, plan.max_slots, 4), dtype=np.int32)
+        slot_w = np.zeros((g, plan.max_slots, 2), dtype=np.int32)
+        nslots = np.zeros(g, dtype=np.int32)
+        total = np.zeros(g, dtype=np.int64)
+        flow = np.zeros((g, g), dtype=np.int64)
+        nat.check(lib.mbp_dispatch_plan(g, e, nat.ptr(x), nat.ptr(home), len(order), nat.ptr(rep_e), nat.ptr(rep_p),
+                                        nat.ptr(rep_g), nat.ptr(cnt), PAD, plan.maxc, plan.max_slots, nat.ptr(route),
+                                        nat.ptr(ncop), nat.ptr(slot_tab), nat.ptr(slot_w), nat.ptr(nslots),
+                                        nat.ptr(total), nat.ptr(flow)), lib, "dispatch_plan")
+        plan.mbs.append(MicroBatchPlan(placement, counts, route, ncop, slot_tab, slot_w, nslots, total, flow))
+    plan.rows_cap = int(max(int(m.total_rows.max()) for m in plan.mbs))
+    plan.rows_cap = max(PAD, (plan.rows_cap + PAD - 1) // PAD * PAD)
+    plan.rep_experts = [sorted({int(ex) for m in plan.mbs for ex, gs in m.placement.replicas.items() if d in gs})
+                        for d in range(g)]
+    return plan
+
+
+# ----------------------------------------------------------------------------- weights
+
+
+def interleave_w1(w_gate: torch.Tensor, w_up: torch.Tensor) -> torch.Tensor:
+    """[.., h', h] gate/up -> [.., 2h', h] with alternating 128-row gate/up blocks (the layout
+    the SwiGLU epilogue consumes: one 256-wide N tile = 128 gate + 128 matching up columns)."""
+    *lead, hp, h = w_gate.shape
+    nb = hp // GATE_BLOCK
+    g = w_gate.reshape(*lead, nb, GATE_BLOCK, h)
+    u = w_up.reshape(*lead, nb, GATE_BLOCK, h)
+    return torch.stack([g, u], dim=-3).reshape(*lead, 2 * hp, h)
+
+
+def deinterleave_w1(w1: torch.Tensor) -> tuple:
+    *lead, hp2, h = w1.shape
+    nb = hp2 // (2 * GATE_BLOCK)
+    v = w1.reshape(*lead, nb, 2, GATE_BLOCK, h)
+    return v[..., 0, :, :].reshape(*lead, hp2 // 2, h), v[..., 1, :, :].reshape(*lead, hp2 // 2, h)
+
+
+# ----------------------------------------------------------------------------- data plane
+
+
+class MoEDataPlane:
+    """Per-rank device state for one MoE layer: home experts, the layer-shared replica slots,
+    fp32 gradients, per-micro-batch receive/activation buffers and the step tables."""
+
+    def __init__(self, comm: Comm, shape: LayerShape, tokens: int, micro_batches: int, plan: StepPlan,
+                 device: torch.device | None = None):
+        shape.check()
+        self.comm, self.shape, self.T, self.MB = comm, shape, tokens, micro_batches
+        self.rank, self.world = comm.rank, comm.world
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        E, h, hp = shape.num_experts, shape.hidden, shape.ffn
+        if E % self.world:
+            raise ValueError(f"{E} experts not divisible by {self.world} GPUs")
+        self.M = E // self.world
+        self.R = plan.rows_cap
+        self.slots = max(plan.slots, 1)
+        self.rep_cap = max(1, self.slots * micro_batches)
+        bf, f4 = 2, 4
+        R, MB = self.R, micro_batches
+        S = self.M + self.rep_cap
+        # ---- symmetric arena (peer-visible buffers; identical layout on every rank)
+        sizes = {
+            "xr": MB * R * h * bf, "y": MB * R * h * bf, "dyr": MB * R * h * bf, "dxp": MB * R * h * bf,
+            "gate_r": MB * R * f4, "dgate_r": MB * R * f4,
+            "w1r": self.slots * 2 * hp * h * bf, "w2r": self.slots * h * hp * bf,
+            "w1": self.M * 2 * hp * h * bf, "w2": self.M * h * hp * bf,
+            "gw1": S * 2 * hp * h * f4, "gw2": S * h * hp * f4,
+        }
+        total = sum((v + 1023) // 1024 * 1024 for v in sizes.values()) + 1024 * len(sizes)
+        self.arena = SymmetricArena(comm, total, self.device)
+        self.off = {k: self.arena.alloc(v) for k, v in sizes.items()}
+        A = self.arena
+        self.Xr = A.local(self.off["xr"], (MB, R, h), torch.bfloat16)
+        self.Y = A.local(self.off["y"], (MB, R, h), torch.bfloat16)
+        self.dYr = A.local(self.off["dyr"], (MB, R, h), torch.bfloat16)
+        self.dXp = A.local(self.off["dxp"], (MB, R, h), torch.bfloat16)
+        self.gate_r = A.local(self.off["gate_r"], (MB, R), torch.float32)
+        self.dgate_r = A.local(self.off["dgate_r"], (MB, R), torch.float32)
+        self.W1r = A.local(self.off["w1r"], (self.slots, 2 * hp, h), torch.bfloat16)
+        self.W2r = A.local(self.off["w2r"], (self.slots, h, hp), torch.bfloat16)
+        self.W1 = A.local(self.off["w1"], (self.M, 2 * hp, h), torch.bfloat16)
+        self.W2 = A.local(self.off["w2"], (self.M, h, hp), torch.bfloat16)
+        self.gW1 = A.local(self.off["gw1"], (S, 2 * hp, h), torch.float32)
+        self.gW2 = A.local(self.off["gw2"], (S, h, hp), torch.float32)
+        # ---- local activations
+        self.H = torch.empty((MB, R, 2 * hp), dtype=torch.bfloat16, device=self.device)
+        self.Act = torch.empty((MB, R, hp), dtype=torch.bfloat16, device=self.device)
+        self.dH = torch.empty((MB, R, 2 * hp), dtype=torch.bfloat16, device=self.device)
+        # ---- per-micro-batch token-side buffers
+        T, k = tokens, shape.top_k
+        self.perm = torch.empty((MB, T, k, 2), dtype=torch.int32, device=self.device)
+        chunks = (T + CHUNK - 1) // CHUNK
+        self.counts = torch.empty((MB, E), dtype=torch.int32, device=self.device)
+        self.chunk_counts = torch.empty((MB, chunks, E), dtype=torch.int32, device=self.device)
+        self.chunk_base = torch.empty((MB, chunks, E), dtype=torch.int32, device=self.device)
+        # peer pointer tables [MB][world]
+        self.ptr_xr = A.peer_table(self.off["xr"], R * h * bf, MB)
+        self.ptr_y = A.peer_table(self.off["y"], R * h * bf, MB)
+        self.ptr_dyr = A.peer_table(self.off["dyr"], R * h * bf, MB)
+        self.ptr_dxp = A.peer_table(self.off["dxp"], R * h * bf, MB)
+        self.ptr_gate = A.peer_table(self.off["gate_r"], R * f4, MB)
+        self.ptr_dgate = A.peer_table(self.off["dgate_r"], R * f4, MB)
+        self.side = torch.cuda.Stream(device=self.device)
+        self.launches = 0
+        self.load_plan(plan)
+
+    # ------------------------------------------------------------------ plan upload
+    def load_plan(self, plan: StepPlan) -> None:
+        if plan.rows_cap > self.R:
+            raise ValueError(f"plan needs {plan.rows_cap} receive rows per micro-batch, buffers hold {self.R}")
+        if max((len(r) for r in plan.rep_experts), default=0) > self.rep_cap:
+            raise ValueError("plan replicates more experts than the replica gradient buffer holds")
+        self.plan = plan
+        d, MB, dev = self.rank, self.MB, self.device
+        E = self.shape.num_experts
+        home = plan.home
+        self.home_experts = np.flatnonzero(home == d)
+        local_of = {int(ex): int(np.flatnonzero(np.flatnonzero(home == home[ex]) == ex)[0]) for ex in range(E)}
+        self.local_of = local_of
+        route, ncop, groups, slots, nsl, pushes = [], [], [], [], [], []
+        max_slots = plan.max_slots
+        for m, mbp in enumerate(plan.mbs):
+            route.append(mbp.route_tab[d])
+            ncop.append(mbp.ncopies)
+            st = mbp.slot_tab[d]
+            sw = mbp.slot_w[d]
+            n = int(mbp.nslots[d])
+            g = np.zeros((max_slots, K.GROUP_FIELDS), dtype=np.int32)
+            g[:n, 0] = st[:n, 2]
+            g[:n, 1] = st[:n, 0]
+            g[:n, 2] = sw[:n, 0]
+            g[:n, 3] = np.where(sw[:n, 1] > 0, K.FLAG_REPLICA, 0)
+            groups.append(g)
+            slots.append(st)
+            nsl.append(n)
+            # replica pushes this rank performs as the owner: (dst gpu, dst slot, local expert)
+            pl = []
+            for dst in range(self.world):
+                stt, sww = mbp.slot_tab[dst], mbp.slot_w[dst]
+                for s in range(int(mbp.nslots[dst])):
+                    if sww[s, 1] and home[stt[s, 3]] == d:
+                        pl.append((dst, int(sww[s, 0]), local_of[int(stt[s, 3])]))
+            pushes.append(pl)
+        self.route_tab = torch.from_numpy(np.stack(route)).to(dev)
+        self.ncopies = torch.from_numpy(np.stack(ncop)).to(dev)
+        self.groups = torch.from_numpy(np.stack(groups)).to(dev)
+        self.slot_tab = torch.from_numpy(np.stack(slots)).to(dev)
+        self.nslots = nsl
+        self.pushes = pushes
+        # ---- wgrad groups: home experts (accumulate) then experts replicated onto this rank
+        wg, segs = [], []
+        R = self.R
+        for loc, ex in enumerate(self.home_experts):
+            s0 = len(segs)
+            tot = 0
+            for m, mbp in enumerate(plan.mbs):
+                st = mbp.slot_tab[d]
+                for s in range(int(mbp.nslots[d])):
+                    if st[s, 3] == ex and mbp.slot_w[d][s, 1] == 0 and st[s, 2] > 0:
+                        segs.append((m * R + int(st[s, 0]), int(st[s, 2])))
+                        tot += int(st[s, 2])
+            wg.append((tot, 0, loc, K.FLAG_ACCUMULATE, s0, len(segs) - s0))
+        for q, ex in enumerate(plan.rep_experts[d]):
+            s0 = len(segs)
+            tot = 0
+            for m, mbp in enumerate(plan.mbs):
+                st, sw = mbp.slot_tab[d], mbp.slot_w[d]
+                for s in range(int(mbp.nslots[d])):
+                    if st[s, 3] == ex and sw[s, 1] == 1 and st[s, 2] > 0:
+                        segs.append((m * R + int(st[s, 0]), int(st[s, 2])))
+                        tot += int(st[s, 2])
+            wg.append((tot, 0, self.M + q, 0, s0, len(segs) - s0))
+        wtab = np.zeros((len(wg), K.GROUP_FIELDS), dtype=np.int32)
+        for i, row in enumerate(wg):
+            wtab[i, :6] = row
+        self.wgroups = torch.from_numpy(wtab).to(dev)
+        self.wsegs = torch.from_numpy(np.asarray(segs if segs else [(0, 0)], dtype=np.int32).reshape(-1, 2)).to(dev)
+        # replicas of zero-row experts must still be overwritten: zero the replica grads per step
+        self.n_rep_here = len(plan.rep_experts[d])
+        # ---- replica gradient reduce lists (this rank as owner): (local expert, [(src rank, q)])
+        reduce = []
+        mn1 = 2 * self.shape.ffn * self.shape.hidden
+        rep_rows = {}
+        for mbp in plan.mbs:
+            for p in range(self.world):
+                stt, sww = mbp.slot_tab[p], mbp.slot_w[p]
+                for s in range(int(mbp.nslots[p])):
+                    if sww[s, 1]:
+                        rep_rows[(p, int(stt[s, 3]))] = rep_rows.get((p, int(stt[s, 3])), 0) + int(stt[s, 2])
+        for loc, ex in enumerate(self.home_experts):
+            srcs = [(p, plan.rep_experts[p].index(int(ex))) for p in range(self.world)
+                    if p != d and int(ex) in plan.rep_experts[p] and rep_rows.get((p, int(ex)), 0) > 0]
+            if srcs:
+                reduce.append((loc, srcs))
+        self.reduce = []
+        for loc, srcs in reduce:
+            p1 = [self.arena.peer_ptr(p, self.off["gw1"]) + (self.M + q) * mn1 * 4 for p, q in srcs]
+            p2 = [self.arena.peer_ptr(p, self.off["gw2"]) + (self.M + q) * mn1 // 2 * 4 for p, q in srcs]
+            self.reduce.append((loc, torch.tensor(p1, dtype=torch.int64, device=dev),
+                                torch.tensor(p2, dtype=torch.int64, device=dev), len(srcs)))
+
+    # ------------------------------------------------------------------ weights
+    def set_weights(self, w_gate: torch.Tensor, w_up: torch.Tensor, w_down: torch.Tensor) -> None:
+        """Home expert weights of this rank (ascending expert id): gate/up [M,h',h], down [M,h,h']."""
+        self.W1.copy_(interleave_w1(w_gate, w_up))
+        self.W2.copy_(w_down)
+
+    def zero_grads(self) -> None:
+        self.gW1.zero_()
+        self.gW2.zero_()
+
+    # ------------------------------------------------------------------ kernels
+    def _lib(self):
+        return nat.kernels()
+
+    def _k(self, name, *args):
+        lib = self._lib()
+        nat.check(getattr(lib, name)(*args), lib, name)
+        self.launches += 1
+
+    def _stream(self):
+        return nat.stream_ptr()
+
+    def forward_backward(self, x: torch.Tensor, idx: torch.Tensor, gates: torch.Tensor, dout: torch.Tensor,
+                         out: torch.Tensor, dx: torch.Tensor, dgate: torch.Tensor) -> None:
+        """One training step of the layer over MB micro-batches (inputs [MB, T, ...] on device).
+        Writes out / dx / dgate and accumulates fp32 expert gradients; asynchronous."""
+        E, k, h, hp = self.shape.num_experts, self.shape.top_k, self.shape.hidden, self.shape.ffn
+        T, R, MB = self.T, self.R, self.MB
+        st = self._stream()
+        A = self.arena
+        A.barrier()  # previous step's readers of our receive buffers are done
+        for m in range(MB):
+            self._forward_mb(m, x[m], idx[m], gates[m], out[m], st)
+            self._backward_mb(m, dout[m], dx[m], dgate[m], st)
+        self._wgrad(st)
+
+    def _replica_push(self, m: int) -> None:
+        if not self.pushes[m]:
+            return
+        h, hp = self.shape.hidden, self.shape.ffn
+        cur = torch.cuda.current_stream()
+        self.side.wait_stream(cur)
+        lib = self._lib()
+        n1, n2 = 2 * hp * h * 2, h * hp * 2
+        for dst, slot, loc in self.pushes[m]:
+            d1 = self.arena.peer_ptr(dst, self.off["w1r"]) + slot * n1
+            d2 = self.arena.peer_ptr(dst, self.off["w2r"]) + slot * n2
+            nat.check(lib.mb_memcpy_async(d1, self.W1[loc].data_ptr(), n1, self.side.cuda_stream), lib, "push w1")
+            nat.check(lib.mb_memcpy_async(d2, self.W2[loc].data_ptr(), n2, self.side.cuda_stream), lib, "push w2")
+        cur.wait_stream(self.side)
+
+    def _forward_mb(self, m, x, idx, gates, out, st):
+        E, k, h, hp = self.shape.num_experts, self.shape.top_k, self.shape.hidden, self.shape.ffn
+        T, R = self.T, self.R
+        chunks = (T + CHUNK - 1) // CHUNK
+        A = self.arena
+        # K5: owners push this micro-batch's replica weights (copy engine, overlaps K1/K2)
+        self._replica_push(m)
+        # K1 + chunk scan + K2
+        self._k("mb_expert_histogram", idx.data_ptr(), 1, T, k, E, self.counts[m].data_ptr(),
+                self.chunk_counts[m].data_ptr(), CHUNK, st)
+        self._k("mb_chunk_scan", self.chunk_counts[m].data_ptr(), self.chunk_base[m].data_ptr(), 1, chunks, E, st)
+        self._k("mb_zero_pad_rows", self.Xr[m].data_ptr(), self.slot_tab[m].data_ptr(), self.nslots[m], h, st)
+        A.barrier()  # every receiver has cleared its pad rows and finished the previous readers
+        self._k("mb_permute_rank", idx.data_ptr(), T, k, gates.data_ptr(), E, self.chunk_base[m].data_ptr(), CHUNK,
+                self.route_tab[m].data_ptr(), self.ncopies[m].data_ptr(), self.plan.maxc,
+                self.ptr_gate[m].data_ptr(), self.perm[m].data_ptr(), st)
+        # K3: dispatch (peer stores)
+        self._k("mb_scatter_rows", x.data_ptr(), T, k, h, self.perm[m].data_ptr(), self.ptr_xr[m].data_ptr(), st)
+        A.barrier()  # all rows (and replica weights) have landed
+        ng = self.nslots[m]
+        if ng:
+            g = self.groups[m]
+            K.grouped_gemm(K.GEMM_FWD_SWIGLU, self.Xr[m], self.W1, g[:ng], N=2 * hp, K=h, C=self.H[m], C2=self.Act[m],
+                           B1=self.W1r)
+            K.grouped_gemm(K.GEMM_FWD_STORE, self.Act[m], self.W2, g[:ng], N=h, K=hp, C=self.Y[m], B1=self.W2r)
+            self.launches += 2
+        A.barrier()  # every expert output is ready
+        # K6: combine over peer loads
+        self._k("mb_combine_rows", self.ptr_y[m].data_ptr(), self.perm[m].data_ptr(), gates.data_ptr(),
+                T, k, h, out.data_ptr(), None, None, st)
+
+    def _backward_mb(self, m, dout, dx, dgate, st):
+        E, k, h, hp = self.shape.num_experts, self.shape.top_k, self.shape.hidden, self.shape.ffn
+        T, R = self.T, self.R
+        A = self.arena
+        # dout rows to the serving GPUs (same permutation as the forward dispatch)
+        self._k("mb_scatter_rows", dout.data_ptr(), T, k, h, self.perm[m].data_ptr(), self.ptr_dyr[m].data_ptr(), st)
+        A.barrier()
+        total = int(self.plan.mbs[m].total_rows[self.rank])
+        self._k("mb_combine_bwd_expert", self.dYr[m].data_ptr(), self.Y[m].data_ptr(), self.gate_r[m].data_ptr(),
+                self.dgate_r[m].data_ptr(), self.slot_tab[m].data_ptr(), self.nslots[m], total, h, st)
+        ng = self.nslots[m]
+        if ng:
+            g = self.groups[m]
+            K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU, self.dYr[m], self.W2, g[:ng], N=hp, K=h, C=self.dH[m], aux=self.H[m],
+                           B1=self.W2r)
+            K.grouped_gemm(K.GEMM_DGRAD_STORE, self.dH[m], self.W1, g[:ng], N=h, K=2 * hp, C=self.dXp[m], B1=self.W1r)
+            self.launches += 2
+        A.barrier()
+        self._k("mb_combine_rows", self.ptr_dxp[m].data_ptr(), self.perm[m].data_ptr(), None, T, k, h, dx.data_ptr(),
+                self.ptr_dgate[m].data_ptr(), dgate.data_ptr(), st)
+
+    def _wgrad(self, st):
+        h, hp = self.shape.hidden, self.shape.ffn
+        R, MB = self.R, self.MB
+        ng = self.wgroups.shape[0]
+        if ng:
+            dyr = self.dYr.view(MB * R, h)
+            K.grouped_gemm(K.GEMM_WGRAD, dyr, self.Act.view(MB * R, hp), self.wgroups, M=h, N=hp, C=self.gW2,
+                           c_slot_stride=h * hp, segs=self.wsegs)
+            K.grouped_gemm(K.GEMM_WGRAD, self.dH.view(MB * R, 2 * hp), self.Xr.view(MB * R, h), self.wgroups,
+                           M=2 * hp, N=h, C=self.gW1, c_slot_stride=2 * hp * h, segs=self.wsegs)
+            self.launches += 2
+        if self.world > 1:
+            self.arena.barrier()  # replica gradients complete on every rank
+            mn1, mn2 = 2 * hp * h, h * hp
+            for loc, p1, p2, n in self.reduce:
+                self._k("mb_accumulate_f32", self.gW1[loc].data_ptr(), p1.data_ptr(), n, mn1, st)
+                self._k("mb_accumulate_f32", self.gW2[loc].data_ptr(), p2.data_ptr(), n, mn2, st)
+
+    step = forward_backward
+
+    def close(self) -> None:
+        self.arena.close()

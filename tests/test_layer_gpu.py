@@ -1,0 +1,79 @@
+"""End-to-end MoE-layer step on one B200 (world = 1) against the CPU oracle.
+
+Integer outputs (device histogram, canonical permutation) must be bit-exact; layer outputs
+and gradients must be within the documented bf16 tolerance rel 2e-2 of the fp32 oracle.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import moe_ref
+from paper_2605_08639_b200 import ModelProfile, SimConfigs, ReplicaConfig, build_topology
+from paper_2605_08639_b200.cluster import b200_profile
+from paper_2605_08639_b200.comm import Comm
+from paper_2605_08639_b200.moe_layer import MoEDataPlane, build_step_plan, deinterleave_w1
+from paper_2605_08639_b200.workload import SHAPES, make_activations, make_routing, make_weights
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-2
+
+
+def _run(name, T, MB, zipf_s=1.0, balanced=False):
+    cfg = SHAPES[name]
+    shape = cfg["shape"]
+    routing = make_routing(shape, T, MB, 1, 0, zipf_s=zipf_s, shift=cfg["shift"], balanced=balanced)
+    topo = build_topology(1, 1, b200_profile(shape.hidden))
+    model = ModelProfile(1, shape.num_experts, shape.top_k, shape.hidden, shape.ffn)
+    plan = build_step_plan("static", routing.mats, topo, model, topo.profile, SimConfigs(replica=ReplicaConfig(0)),
+                           shape)
+    dp = MoEDataPlane(Comm(), shape, T, MB, plan)
+    wg, wu, wd = make_weights(shape)
+    dp.set_weights(wg.cuda(), wu.cuda(), wd.cuda())
+    dp.zero_grads()
+    x, dout = make_activations(shape, T, MB, 0)
+    x, dout = x.cuda(), dout.cuda()
+    idx = torch.from_numpy(routing.idx).cuda()
+    gates = torch.from_numpy(routing.gates).cuda()
+    out = torch.empty_like(x)
+    dx = torch.empty_like(x)
+    dgate = torch.empty(MB, T, shape.top_k, dtype=torch.float32, device="cuda")
+    dp.step(x, idx, gates, dout, out, dx, dgate)
+    torch.cuda.synchronize()
+    return shape, routing, plan, dp, (wg, wu, wd), (x, dout, idx, gates), (out, dx, dgate)
+
+
+@pytest.mark.parametrize("name,T,MB", [("tiny", 256, 2), ("qwen3-30b-a3b", 512, 2)])
+def test_layer_step_matches_oracle(name, T, MB):
+    shape, routing, plan, dp, (wg, wu, wd), (x, dout, idx, gates), (out, dx, dgate) = _run(name, T, MB)
+    E = shape.num_experts
+    home = plan.home
+    gwg = torch.zeros(E, shape.ffn, shape.hidden, device="cuda")
+    gwu = torch.zeros_like(gwg)
+    gwd = torch.zeros(E, shape.hidden, shape.ffn, device="cuda")
+    for m in range(MB):
+        # K1: device histogram == np.bincount (bit-exact)
+        assert np.array_equal(dp.counts[m].cpu().numpy(), moe_ref.histogram(routing.idx[m], E))
+        # K2: device permutation == canonical permutation (bit-exact)
+        _, row_base = moe_ref.receive_layout(routing.mats[m], home, {}, {}, pad=128)
+        ref_perm = moe_ref.canonical_permutation_fast(routing.idx[m], 0, routing.mats[m], home, {}, {}, row_base)
+        assert np.array_equal(dp.perm[m].cpu().numpy(), ref_perm)
+        ref = moe_ref.moe_layer_fp32(x[m], idx[m], gates[m], wg.cuda(), wu.cuda(), wd.cuda(), dout[m])
+        assert moe_ref.rel_err(out[m], ref["out"]) < TOL
+        assert moe_ref.rel_err(dx[m], ref["dx"]) < TOL
+        assert moe_ref.rel_err(dgate[m], ref["dgate"]) < TOL
+        gwg += ref["dWg"]
+        gwu += ref["dWu"]
+        gwd += ref["dWd"]
+    g_gate, g_up = deinterleave_w1(dp.gW1[:dp.M])
+    assert moe_ref.rel_err(g_gate, gwg) < TOL
+    assert moe_ref.rel_err(g_up, gwu) < TOL
+    assert moe_ref.rel_err(dp.gW2[:dp.M], gwd) < TOL
+    dp.close()
+
+
+def test_balanced_routing_is_uniform():
+    shape, routing, plan, dp, *_ = _run("tiny", 256, 1, balanced=True)
+    counts = dp.counts[0].cpu().numpy()
+    assert counts.max() - counts.min() <= 1
+    dp.close()
