@@ -1,0 +1,337 @@
+#!/usr/bin/env python
+"""MoE-layer fwd+bwd tokens/s of the B200 ReLibra hot path (BASELINE.json metric).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config qwen3-30b-a3b] [--zipf 1.0]
+  torchrun --nproc-per-node N bench.py --gpus N ...           (one process per GPU, NCCL)
+  python bench.py --impl reference ...                          (CPU reference arm, rank 0)
+
+A step = one training step of one MoE layer over MB micro-batches of T tokens per GPU
+(forward + backward incl. fp32 weight gradients) with replayed routing.  EP = N (all N GPUs
+of one box; the reference's "node" = a GPU group of min(N, 4)).  Policies measured on the same
+routing: ReLibra (headline `value`), no-balancing static EP, oracle-EPLB, and the balanced
+ideal (uniform routing).  Rank 0 prints ONE JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import gc
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE-layer fwd+bwd tokens/s"
+PEAKS_FALLBACK = {"bf16_tflops_sustained": 1376.6, "bf16_tflops": 1667.1, "hbm_gbs": 6534.5}
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return json.load(f), "measured (MEASURED_PEAKS.json)"
+    except OSError:
+        return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 50 ms while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "50", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- CPU reference arm
+
+def cpu_reference_sample(cfg_name: str, tokens: int, world: int, zipf: float, budget_s: float, threads: int):
+    """The reference's CPU path on a bounded sample: the planner pipeline of moebalance on the
+    full step's routing (oracle restatement) + np.bincount histogram + the fp32 layer fwd+bwd on a
+    token sample.  Returns (tokens/s extrapolated per step-token, sample description)."""
+    import torch
+    from oracle import moe_ref
+    from paper_2605_08639_b200.workload import SHAPES, make_activations, make_routing, make_weights
+    torch.set_num_threads(threads)
+    cfg = SHAPES[cfg_name]
+    shape = cfg["shape"]
+    n = 256
+    wg, wu, wd = make_weights(shape)
+    done_tokens, elapsed = 0, 0.0
+    while elapsed < budget_s:
+        r = make_routing(shape, n, 1, 1, 0, zipf_s=zipf, shift=cfg["shift"])
+        x, dout = make_activations(shape, n, 1, 0)
+        t0 = time.perf_counter()
+        for j in range(1):
+            moe_ref.histogram(r.idx[0], shape.num_experts)
+        moe_ref.moe_layer_fp32(x[0], torch.from_numpy(r.idx[0]), torch.from_numpy(r.gates[0]), wg, wu, wd, dout[0])
+        dt = time.perf_counter() - t0
+        elapsed += dt
+        done_tokens += n
+        if dt < budget_s / 8:
+            n *= 2
+    tps = done_tokens / elapsed
+    return tps, f"{done_tokens} tokens of {cfg_name} (1 GPU's share), fp32 torch CPU fwd+bwd + bincount, {elapsed:.1f}s"
+
+
+def run_reference(args, rank, world):
+    import torch
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    vals = []
+    for i in range(args.warmup + args.steps):
+        tps, sample = cpu_reference_sample(args.config, args.tokens, world, args.zipf,
+                                           budget_s=2.0 if i < args.warmup else 4.0, threads=threads)
+        if i >= args.warmup:
+            vals.append(tps)
+    # whole-job throughput: every GPU's share is independent CPU work on the same host
+    value = float(np.mean(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.config} MoE layer (CPU reference arm)", "tokens_per_gpu": args.tokens},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- B200 arm
+
+def measure_policy(args, comm, policy, shape, cfg, routing, topo, model, cfgs, want_detail):
+    import torch
+    from paper_2605_08639_b200.moe_layer import MoEDataPlane, build_step_plan
+    from paper_2605_08639_b200.workload import make_activations, make_weights_for
+    rank, world = comm.rank, comm.world
+    T, MB = args.tokens, args.micro_batches
+    t0 = time.perf_counter()
+    plan = build_step_plan(policy, routing.mats, topo, model, topo.profile, cfgs, shape)
+    plan_ms = (time.perf_counter() - t0) * 1e3
+    dp = MoEDataPlane(comm, shape, T, MB, plan)
+    experts = np.flatnonzero(plan.home == rank)
+    wg, wu, wd = make_weights_for(shape, experts)
+    dp.set_weights(wg, wu, wd)
+    del wg, wu, wd
+    dp.zero_grads()
+    xh, douth = make_activations(shape, T, MB, rank)
+    dev = {"x": xh.cuda(), "dout": douth.cuda(), "idx": torch.from_numpy(routing.idx).cuda(),
+           "gates": torch.from_numpy(routing.gates).cuda()}
+    dev["out"] = torch.empty_like(dev["x"])
+    dev["dx"] = torch.empty_like(dev["x"])
+    dev["dgate"] = torch.empty(MB, T, shape.top_k, dtype=torch.float32, device="cuda")
+
+    def step():
+        dp.step(dev["x"], dev["idx"], dev["gates"], dev["dout"], dev["out"], dev["dx"], dev["dgate"])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    comm.host_barrier()
+    sampler = ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) if want_detail else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.15)
+    dp.timing = want_detail
+    dp.gemm_events = []
+    launches0 = dp.launches
+    torch.cuda.synchronize()
+    comm.host_barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(args.steps):
+        step()
+    e.record()
+    torch.cuda.synchronize()
+    comm.host_barrier()
+    clocks = sampler.stop() if sampler else None
+    ms = s.elapsed_time(e) / args.steps
+    launches = (dp.launches - launches0) // args.steps
+    dp.timing = False
+    ms_max = ms
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_max = float(t.item())
+    res = {"ms": ms_max, "plan_ms": plan_ms, "skew": plan.skew(), "launches": launches,
+           "rows": [dp.real_rows(m) for m in range(MB)], "rows_cap": plan.rows_cap}
+    if want_detail:
+        gemm_ms = sum(a.elapsed_time(b) for a, b, _ in dp.gemm_events) / args.steps
+        gemm_flop = sum(f for _, _, f in dp.gemm_events) / args.steps
+        res.update(gemm_ms=gemm_ms, gemm_flop=gemm_flop, gemm_launches=len(dp.gemm_events) // args.steps,
+                   clocks=clocks)
+        # e2e through the host-buffer API (pinned host tensors, copies inside the timed region)
+        host = {k: v.cpu().pin_memory() for k, v in dev.items()}
+        for _ in range(2):
+            dp.step_host(host, dev)
+        comm.host_barrier()
+        t0 = time.perf_counter()
+        n_e2e = max(2, min(args.steps, 5))
+        for _ in range(n_e2e):
+            dp.step_host(host, dev)
+        comm.host_barrier()
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / n_e2e
+        if world > 1:
+            t = torch.tensor([e2e_ms], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        res["e2e_ms"] = e2e_ms
+        res["h2d"] = sum(host[k].numel() * host[k].element_size() for k in ("x", "idx", "gates", "dout"))
+        res["d2h"] = sum(host[k].numel() * host[k].element_size() for k in ("out", "dx", "dgate"))
+        del host
+    dp.close()
+    del dp, dev
+    gc.collect()
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_ours(args, comm):
+    import torch
+    from paper_2605_08639_b200 import AnnealConfig, ModelProfile, ReplicaConfig, SimConfigs
+    from paper_2605_08639_b200.cluster import b200_box_topology, b200_profile
+    from paper_2605_08639_b200.workload import SHAPES, make_routing
+    rank, world = comm.rank, comm.world
+    cfg = SHAPES[args.config]
+    shape = cfg["shape"]
+    group = min(world, args.group or cfg["group"])
+    topo = b200_box_topology(world, group, b200_profile(shape.hidden))
+    model = ModelProfile(1, shape.num_experts, shape.top_k, shape.hidden, shape.ffn)
+    slots = cfg["slots"] if args.slots is None else args.slots
+    cfgs = SimConfigs(anneal=AnnealConfig(seeds=tuple(range(args.sa_chains))), replica=ReplicaConfig(slots),
+                      threads=min(8, os.cpu_count() or 1))
+    T, MB = args.tokens, args.micro_batches
+    skewed = make_routing(shape, T, MB, world, rank, zipf_s=args.zipf, shift=cfg["shift"])
+    balanced = make_routing(shape, T, MB, world, rank, zipf_s=args.zipf, shift=cfg["shift"], balanced=True)
+    policies = [p for p in args.policies.split(",") if p]
+    results = {}
+    for pol in policies:
+        routing = balanced if pol == "balanced_oracle" else skewed
+        results[pol] = measure_policy(args, comm, pol, shape, cfg, routing, topo, model, cfgs,
+                                      want_detail=(pol == args.headline))
+    head = results[args.headline]
+    tokens_step = world * T * MB
+    value = tokens_step / (head["ms"] / 1e3)
+    peaks, peak_src = load_peaks()
+    peak_tf = float(peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"]))
+    gemm_tflops = head["gemm_flop"] / (head["gemm_ms"] / 1e3) / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": head["ms"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"{args.config} MoE layer fwd+bwd, EP={world}, replayed Zipf routing",
+                   "experts": shape.num_experts, "top_k": shape.top_k, "hidden": shape.hidden, "ffn": shape.ffn,
+                   "tokens_per_gpu": T, "micro_batches": MB, "global_tokens_per_step": tokens_step,
+                   "policy": args.headline, "zipf_s": args.zipf, "hot_shift": cfg["shift"], "ep": world,
+                   "gpu_group": group, "replica_slots": slots, "sa_chains": args.sa_chains,
+                   "l2": "inputs larger than L2 (per-step working set >> 126 MB)"},
+        "roofline": {"kernel": "K4 tcgen05 grouped GEMM (all fwd/dgrad/wgrad launches of the step)",
+                     "bound": "tensor", "achieved": round(gemm_tflops, 1), "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": round(gemm_tflops / peak_tf, 4), "traffic": None,
+                     "peak_source": f"bf16_tflops_sustained, {peak_src}",
+                     "flops_per_step": head["gemm_flop"], "gemm_ms_per_step": round(head["gemm_ms"], 4),
+                     "gemm_share_of_step": round(head["gemm_ms"] / head["ms"], 4)},
+        "e2e": {"value": tokens_step / (head["e2e_ms"] / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": head["h2d"],
+                "d2h_bytes_per_step": head["d2h"], "ms_per_step": head["e2e_ms"]},
+        "gpu_launches": head["launches"],
+        "clocks": head["clocks"],
+        "balance": {p: {"tokens_per_s": tokens_step / (r["ms"] / 1e3), "ms_per_step": r["ms"], "skew": r["skew"],
+                        "planner_ms": r["plan_ms"]} for p, r in results.items()},
+    }
+    if "static" in results:
+        line["balance"]["speedup_vs_static"] = results["static"]["ms"] / head["ms"]
+    if "balanced_oracle" in results:
+        line["balance"]["frac_of_balanced"] = results["balanced_oracle"]["ms"] / head["ms"]
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        tps, sample = cpu_reference_sample(args.config, T, world, args.zipf, budget_s=args.cpu_budget,
+                                           threads=os.cpu_count() or 1)
+        line["cpu_baseline"] = {"value": tps, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+                                "sample": sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="qwen3-30b-a3b")
+    ap.add_argument("--tokens", type=int, default=8192)
+    ap.add_argument("--micro-batches", type=int, default=8)
+    ap.add_argument("--zipf", type=float, default=1.0)
+    ap.add_argument("--slots", type=int, default=None)
+    ap.add_argument("--group", type=int, default=0)
+    ap.add_argument("--sa-chains", type=int, default=8)
+    ap.add_argument("--policies", default="relibra,static,eplb_like,balanced_oracle")
+    ap.add_argument("--headline", default="relibra")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.headline not in args.policies.split(","):
+        args.policies = args.headline + "," + args.policies
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    import torch
+    from paper_2605_08639_b200.comm import init_distributed
+    if world == 1:
+        torch.cuda.set_device(0)
+    comm = init_distributed()
+    try:
+        run_ours(args, comm)
+    finally:
+        if comm.dist:
+            comm.dist.barrier()
+            comm.dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

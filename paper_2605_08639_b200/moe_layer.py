@@ -235,7 +235,30 @@ class MoEDataPlane:
         self.ptr_dgate = A.peer_table(self.off["dgate_r"], R * f4, MB)
         self.side = torch.cuda.Stream(device=self.device)
         self.launches = 0
+        self.timing = False       # record CUDA events around every K4 launch (bench roofline)
+        self.gemm_events = []     # (start, end, algorithmic FLOPs)
         self.load_plan(plan)
+
+    def _timed(self, flops: float):
+        """Context manager recording CUDA events on the current stream around a K4 launch."""
+        dp = self
+
+        class _T:
+            def __enter__(self):
+                if dp.timing:
+                    self.s = torch.cuda.Event(enable_timing=True)
+                    self.e = torch.cuda.Event(enable_timing=True)
+                    self.s.record()
+
+            def __exit__(self, *a):
+                if dp.timing:
+                    self.e.record()
+                    dp.gemm_events.append((self.s, self.e, flops))
+        return _T()
+
+    def real_rows(self, m: int) -> int:
+        """Token rows this rank's experts serve in micro-batch m (padding excluded)."""
+        return int(self.plan.mbs[m].flow[:, self.rank].sum())
 
     # ------------------------------------------------------------------ plan upload
     def load_plan(self, plan: StepPlan) -> None:
@@ -355,18 +378,69 @@ class MoEDataPlane:
         return nat.stream_ptr()
 
     def forward_backward(self, x: torch.Tensor, idx: torch.Tensor, gates: torch.Tensor, dout: torch.Tensor,
-                         out: torch.Tensor, dx: torch.Tensor, dgate: torch.Tensor) -> None:
+                         out: torch.Tensor, dx: torch.Tensor, dgate: torch.Tensor, hooks=None) -> None:
         """One training step of the layer over MB micro-batches (inputs [MB, T, ...] on device).
-        Writes out / dx / dgate and accumulates fp32 expert gradients; asynchronous."""
-        E, k, h, hp = self.shape.num_experts, self.shape.top_k, self.shape.hidden, self.shape.ffn
-        T, R, MB = self.T, self.R, self.MB
+        Writes out / dx / dgate and accumulates fp32 expert gradients; asynchronous.
+        `hooks` (optional) gets before(m) / after_forward(m) / after_backward(m) callbacks on the
+        compute stream (used by step_host to overlap host copies)."""
         st = self._stream()
         A = self.arena
         A.barrier()  # previous step's readers of our receive buffers are done
-        for m in range(MB):
+        for m in range(self.MB):
+            if hooks:
+                hooks.before(m)
             self._forward_mb(m, x[m], idx[m], gates[m], out[m], st)
+            if hooks:
+                hooks.after_forward(m)
             self._backward_mb(m, dout[m], dx[m], dgate[m], st)
+            if hooks:
+                hooks.after_backward(m)
         self._wgrad(st)
+
+    def step_host(self, host: dict, dev: dict) -> None:
+        """The user-facing step with HOST (pinned) tensors: per micro-batch, x/idx/gates/dout are
+        copied host->device on one copy stream while earlier micro-batches compute, and
+        out/dx/dgate are copied device->host on another as soon as they exist.  `dev` holds the
+        device staging tensors of the same shapes.  Synchronous: returns with results on host."""
+        cur = torch.cuda.current_stream()
+        if not hasattr(self, "_h2d"):
+            self._h2d = torch.cuda.Stream(device=self.device)
+            self._d2h = torch.cuda.Stream(device=self.device)
+        h2d, d2h = self._h2d, self._d2h
+        ready = []
+        h2d.wait_stream(cur)
+        with torch.cuda.stream(h2d):
+            for m in range(self.MB):
+                for key in ("x", "idx", "gates", "dout"):
+                    dev[key][m].copy_(host[key][m], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(h2d)
+                ready.append(ev)
+        dp = self
+
+        class _Hooks:
+            def before(self, m):
+                cur.wait_event(ready[m])
+
+            def after_forward(self, m):
+                ev = torch.cuda.Event()
+                ev.record(cur)
+                d2h.wait_event(ev)
+                with torch.cuda.stream(d2h):
+                    host["out"][m].copy_(dev["out"][m], non_blocking=True)
+
+            def after_backward(self, m):
+                ev = torch.cuda.Event()
+                ev.record(cur)
+                d2h.wait_event(ev)
+                with torch.cuda.stream(d2h):
+                    host["dx"][m].copy_(dev["dx"][m], non_blocking=True)
+                    host["dgate"][m].copy_(dev["dgate"][m], non_blocking=True)
+
+        self.forward_backward(dev["x"], dev["idx"], dev["gates"], dev["dout"], dev["out"], dev["dx"], dev["dgate"],
+                              hooks=_Hooks())
+        cur.wait_stream(d2h)
+        cur.synchronize()
 
     def _replica_push(self, m: int) -> None:
         if not self.pushes[m]:
@@ -405,9 +479,12 @@ class MoEDataPlane:
         ng = self.nslots[m]
         if ng:
             g = self.groups[m]
-            K.grouped_gemm(K.GEMM_FWD_SWIGLU, self.Xr[m], self.W1, g[:ng], N=2 * hp, K=h, C=self.H[m], C2=self.Act[m],
-                           B1=self.W1r)
-            K.grouped_gemm(K.GEMM_FWD_STORE, self.Act[m], self.W2, g[:ng], N=h, K=hp, C=self.Y[m], B1=self.W2r)
+            rows = self.real_rows(m)
+            with self._timed(4.0 * rows * h * hp):
+                K.grouped_gemm(K.GEMM_FWD_SWIGLU, self.Xr[m], self.W1, g[:ng], N=2 * hp, K=h, C=self.H[m],
+                               C2=self.Act[m], B1=self.W1r)
+            with self._timed(2.0 * rows * h * hp):
+                K.grouped_gemm(K.GEMM_FWD_STORE, self.Act[m], self.W2, g[:ng], N=h, K=hp, C=self.Y[m], B1=self.W2r)
             self.launches += 2
         A.barrier()  # every expert output is ready
         # K6: combine over peer loads
@@ -427,9 +504,13 @@ class MoEDataPlane:
         ng = self.nslots[m]
         if ng:
             g = self.groups[m]
-            K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU, self.dYr[m], self.W2, g[:ng], N=hp, K=h, C=self.dH[m], aux=self.H[m],
-                           B1=self.W2r)
-            K.grouped_gemm(K.GEMM_DGRAD_STORE, self.dH[m], self.W1, g[:ng], N=h, K=2 * hp, C=self.dXp[m], B1=self.W1r)
+            rows = self.real_rows(m)
+            with self._timed(2.0 * rows * h * hp):
+                K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU, self.dYr[m], self.W2, g[:ng], N=hp, K=h, C=self.dH[m],
+                               aux=self.H[m], B1=self.W2r)
+            with self._timed(4.0 * rows * h * hp):
+                K.grouped_gemm(K.GEMM_DGRAD_STORE, self.dH[m], self.W1, g[:ng], N=h, K=2 * hp, C=self.dXp[m],
+                               B1=self.W1r)
             self.launches += 2
         A.barrier()
         self._k("mb_combine_rows", self.ptr_dxp[m].data_ptr(), self.perm[m].data_ptr(), None, T, k, h, dx.data_ptr(),
@@ -440,11 +521,14 @@ class MoEDataPlane:
         R, MB = self.R, self.MB
         ng = self.wgroups.shape[0]
         if ng:
+            rows = sum(self.real_rows(m) for m in range(MB))
             dyr = self.dYr.view(MB * R, h)
-            K.grouped_gemm(K.GEMM_WGRAD, dyr, self.Act.view(MB * R, hp), self.wgroups, M=h, N=hp, C=self.gW2,
-                           c_slot_stride=h * hp, segs=self.wsegs)
-            K.grouped_gemm(K.GEMM_WGRAD, self.dH.view(MB * R, 2 * hp), self.Xr.view(MB * R, h), self.wgroups,
-                           M=2 * hp, N=h, C=self.gW1, c_slot_stride=2 * hp * h, segs=self.wsegs)
+            with self._timed(2.0 * rows * h * hp):
+                K.grouped_gemm(K.GEMM_WGRAD, dyr, self.Act.view(MB * R, hp), self.wgroups, M=h, N=hp, C=self.gW2,
+                               c_slot_stride=h * hp, segs=self.wsegs)
+            with self._timed(4.0 * rows * h * hp):
+                K.grouped_gemm(K.GEMM_WGRAD, self.dH.view(MB * R, 2 * hp), self.Xr.view(MB * R, h), self.wgroups,
+                               M=2 * hp, N=h, C=self.gW1, c_slot_stride=2 * hp * h, segs=self.wsegs)
             self.launches += 2
         if self.world > 1:
             self.arena.barrier()  # replica gradients complete on every rank
