@@ -1,5 +1,8 @@
-// Host launcher + C-ABI for the K4 tcgen05 grouped GEMM (see grouped_gemm.cuh).
-#include "grouped_gemm.cuh"
+// Host launcher + C-ABI for the K4 tcgen05 grouped GEMM (grouped_gemm.cuh: 1-CTA 128xBN
+// tiles; grouped_gemm_pair.cuh: CTA-pair 256x256 tiles, the default when the shape allows).
+#include <cstdlib>
+
+#include "grouped_gemm_pair.cuh"
 #include "capi_common.cuh"
 #include "../../../include/mb_kernels.h"
 
@@ -18,15 +21,40 @@ static int launch_gemm(const GemmParams& p, cudaStream_t stream) {
   return MB_OK;
 }
 
+template <bool kW, bool kAmn, bool kBmn, int kEpi>
+static int launch_pair(const GemmParams& p, cudaStream_t stream) {
+  auto kern = grouped_gemm_pair_kernel<kW, kAmn, kBmn, kEpi>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    MB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg::kSmemBytes));
+    attr_set = true;
+  }
+  const int grid = device_sm_count() & ~1;
+  kern<<<grid, 320, PairCfg::kSmemBytes, stream>>>(p);
+  MB_CUDA_TRY(cudaGetLastError());
+  return MB_OK;
+}
+
+static bool pair_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("MB_GEMM_PAIR");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 }  // namespace mb
 
 using namespace mb;
 
 extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t a_cols, const void* B0,
                                int64_t b0_rows, const void* B1, int64_t b1_rows, int64_t b_cols,
-                               const void* groups, const void* segs, int num_groups, int M, int N, int K, void* C, int64_t ldc,
-                               int64_t c_slot_stride, void* C2, int64_t ldc2, const void* aux, int64_t ld_aux,
-                               void* stream) {
+                               const void* groups, const void* segs, int num_groups, int M, int N, int K, void* C,
+                               int64_t ldc, int64_t c_slot_stride, void* C2, int64_t ldc2, const void* aux,
+                               int64_t ld_aux, void* stream) {
+  const bool force_single = (mode & 0x100) != 0 || !pair_enabled();
+  mode &= 0xff;
   MB_CHECK_ARG(num_groups >= 0 && num_groups <= kMaxGroups, "num_groups %d outside [0, %d]", num_groups, kMaxGroups);
   MB_CHECK_ARG(A && B0 && C && groups, "null operand pointer");
   MB_CHECK_ARG(a_cols % 64 == 0 && b_cols % 64 == 0, "operand widths must be multiples of 64");
@@ -40,17 +68,22 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
   p.C = C; p.ldc = ldc; p.c_slot_stride = c_slot_stride;
   p.C2 = C2; p.ldc2 = ldc2; p.aux = aux; p.ld_aux = ld_aux;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const bool pair = !force_single && N % 256 == 0 && (mode != MB_GEMM_WGRAD || M % 256 == 0);
   int rc;
   switch (mode) {
     case MB_GEMM_FWD_STORE:
     case MB_GEMM_FWD_SWIGLU: {
       MB_CHECK_ARG(N % 256 == 0 && K % 64 == 0 && a_cols == K && b_cols == K, "fwd GEMM shape N=%d K=%d", N, K);
+      const uint32_t bbox = pair ? 128 : 256;
       if ((rc = make_tmap_bf16_2d(&p.tmA, A, a_cols, a_rows, a_cols * 2, 64, 128))) return rc;
-      if ((rc = make_tmap_bf16_2d(&p.tmB0, B0, b_cols, b0_rows, b_cols * 2, 64, 256))) return rc;
-      if ((rc = make_tmap_bf16_2d(&p.tmB1, B1, b_cols, b1_rows, b_cols * 2, 64, 256))) return rc;
-      if (mode == MB_GEMM_FWD_STORE) return launch_gemm<false, false, false, 256, EPI_STORE_BF16>(p, s);
+      if ((rc = make_tmap_bf16_2d(&p.tmB0, B0, b_cols, b0_rows, b_cols * 2, 64, bbox))) return rc;
+      if ((rc = make_tmap_bf16_2d(&p.tmB1, B1, b_cols, b1_rows, b_cols * 2, 64, bbox))) return rc;
+      if (mode == MB_GEMM_FWD_STORE)
+        return pair ? launch_pair<false, false, false, EPI_STORE_BF16>(p, s)
+                    : launch_gemm<false, false, false, 256, EPI_STORE_BF16>(p, s);
       MB_CHECK_ARG(C2 != nullptr, "SwiGLU epilogue needs the activation output");
-      return launch_gemm<false, false, false, 256, EPI_SWIGLU>(p, s);
+      return pair ? launch_pair<false, false, false, EPI_SWIGLU>(p, s)
+                  : launch_gemm<false, false, false, 256, EPI_SWIGLU>(p, s);
     }
     case MB_GEMM_DGRAD_STORE:
     case MB_GEMM_DGRAD_DSWIGLU: {
@@ -60,17 +93,20 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
       if ((rc = make_tmap_bf16_2d(&p.tmB1, B1, b_cols, b1_rows, b_cols * 2, 64, 64))) return rc;
       if (mode == MB_GEMM_DGRAD_STORE) {
         MB_CHECK_ARG(N % 256 == 0, "dgrad N=%d must be a multiple of 256", N);
-        return launch_gemm<false, false, true, 256, EPI_STORE_BF16>(p, s);
+        return pair ? launch_pair<false, false, true, EPI_STORE_BF16>(p, s)
+                    : launch_gemm<false, false, true, 256, EPI_STORE_BF16>(p, s);
       }
       MB_CHECK_ARG(N % 128 == 0 && aux != nullptr, "dSwiGLU epilogue needs N%%128==0 and H");
-      return launch_gemm<false, false, true, 128, EPI_DSWIGLU>(p, s);
+      return pair ? launch_pair<false, false, true, EPI_DSWIGLU>(p, s)
+                  : launch_gemm<false, false, true, 128, EPI_DSWIGLU>(p, s);
     }
     case MB_GEMM_WGRAD: {
       MB_CHECK_ARG(M % 128 == 0 && N % 256 == 0 && a_cols == M && b_cols == N, "wgrad GEMM shape M=%d N=%d", M, N);
       if ((rc = make_tmap_bf16_2d(&p.tmA, A, a_cols, a_rows, a_cols * 2, 64, 64))) return rc;
       if ((rc = make_tmap_bf16_2d(&p.tmB0, B0, b_cols, b0_rows, b_cols * 2, 64, 64))) return rc;
       p.tmB1 = p.tmB0;
-      return launch_gemm<true, true, true, 256, EPI_ACC_F32>(p, s);
+      return pair ? launch_pair<true, true, true, EPI_ACC_F32>(p, s)
+                  : launch_gemm<true, true, true, 256, EPI_ACC_F32>(p, s);
     }
     default:
       return set_error(MB_EINVAL, "unknown grouped GEMM mode %d", mode);

@@ -33,6 +33,9 @@ def main():
     ap.add_argument("--groups", type=int, default=128)
     ap.add_argument("--h", type=int, default=2048)
     ap.add_argument("--hp", type=int, default=768)
+    ap.add_argument("--only", default="")
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
     a = ap.parse_args()
     G, r, h, hp = a.groups, a.rows_per_group, a.h, a.hp
     R = G * r
@@ -53,16 +56,21 @@ def main():
     gW1 = torch.zeros(G, 2 * hp, h, device=dev)
     gW2 = torch.zeros(G, h, hp, device=dev)
     flop = 2.0 * R * h * hp
+    global timeit
+    _t = timeit
+    timeit = lambda fn: _t(fn, iters=a.iters, warmup=a.warmup)
+    only = set(a.only.split(",")) if a.only else None
     res = {}
-    res["fwd1_swiglu"] = (timeit(lambda: K.grouped_gemm(K.GEMM_FWD_SWIGLU, X, W1, groups, N=2 * hp, K=h, C=H, C2=Act)), 2 * flop)
-    res["fwd2_store"] = (timeit(lambda: K.grouped_gemm(K.GEMM_FWD_STORE, Act, W2, groups, N=h, K=hp, C=Y)), flop)
-    res["dgrad_dswiglu"] = (timeit(lambda: K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU, dY, W2, groups, N=hp, K=h, C=dH, aux=H)), flop)
-    res["dgrad_dx"] = (timeit(lambda: K.grouped_gemm(K.GEMM_DGRAD_STORE, dH, W1, groups, N=h, K=2 * hp, C=dX)), 2 * flop)
-    res["wgrad_w2"] = (timeit(lambda: K.grouped_gemm(K.GEMM_WGRAD, dY, Act, wg, M=h, N=hp, C=gW2, c_slot_stride=h * hp)), flop)
-    res["wgrad_w1"] = (timeit(lambda: K.grouped_gemm(K.GEMM_WGRAD, dH, X, wg, M=2 * hp, N=h, C=gW1, c_slot_stride=2 * hp * h)), 2 * flop)
+    if not only or "fwd1_swiglu" in only: res["fwd1_swiglu"] = (timeit(lambda: K.grouped_gemm(K.GEMM_FWD_SWIGLU, X, W1, groups, N=2 * hp, K=h, C=H, C2=Act)), 2 * flop)
+    if not only or "fwd2_store" in only: res["fwd2_store"] = (timeit(lambda: K.grouped_gemm(K.GEMM_FWD_STORE, Act, W2, groups, N=h, K=hp, C=Y)), flop)
+    if not only or "dgrad_dswiglu" in only: res["dgrad_dswiglu"] = (timeit(lambda: K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU, dY, W2, groups, N=hp, K=h, C=dH, aux=H)), flop)
+    if not only or "dgrad_dx" in only: res["dgrad_dx"] = (timeit(lambda: K.grouped_gemm(K.GEMM_DGRAD_STORE, dH, W1, groups, N=h, K=2 * hp, C=dX)), 2 * flop)
+    if not only or "wgrad_w2" in only: res["wgrad_w2"] = (timeit(lambda: K.grouped_gemm(K.GEMM_WGRAD, dY, Act, wg, M=h, N=hp, C=gW2, c_slot_stride=h * hp)), flop)
+    if not only or "wgrad_w1" in only: res["wgrad_w1"] = (timeit(lambda: K.grouped_gemm(K.GEMM_WGRAD, dH, X, wg, M=2 * hp, N=h, C=gW1, c_slot_stride=2 * hp * h)), 2 * flop)
     out = {k: {"ms": round(v[0], 4), "tflops": round(v[1] / v[0] / 1e9, 1)} for k, v in res.items()}
     tot_ms = sum(v[0] for v in res.values())
-    out["total"] = {"ms": round(tot_ms, 4), "tflops": round(9 * flop / tot_ms / 1e9, 1)}
+    if not only:
+        out["total"] = {"ms": round(tot_ms, 4), "tflops": round(9 * flop / tot_ms / 1e9, 1)}
     print(json.dumps({"shape": {"groups": G, "rows": r, "h": h, "hp": hp}, "gemm": out}))
 
 
