@@ -41,13 +41,73 @@ enum {
   MB_GEMM_FWD_SWIGLU = 1,    /* as above, epilogue C=H, C2=silu(gate)*up             (H = X W1^T)   */
   MB_GEMM_DGRAD_STORE = 2,   /* C[rows_g,N] = A[rows_g,K] . B_slot[K,N]              (dX = dH W1)   */
   MB_GEMM_DGRAD_DSWIGLU = 3, /* as above, epilogue SwiGLU backward with aux=H -> C=dH (dAct = dY W2) */
-  MB_GEMM_WGRAD = 4          /* C_slot[M,N] (+)= A[K_g,M]^T . B[K_g,N]               (dW)           */
+  MB_GEMM_WGRAD = 4,         /* C_slot[M,N] (+)= A[K_g,M]^T . B[K_g,N]               (dW)           */
+  MB_GEMM_DGRAD_DSWIGLU_GATED = 5 /* A = raw dout rows; epilogue applies row_scale (gate): C = dH,
+                                     C2 = gate*act, row_partial[row][N/128] = partial <dout.W2, act>
+                                     whose sum is dgate = <dout, Y> (replaces the combine backward) */
 };
+/* mode | 0x100 forces the 1-CTA kernel (default: CTA-pair 256x256 tiles when the shape allows). */
 int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t a_cols, const void* B0, int64_t b0_rows,
                     const void* B1, int64_t b1_rows, int64_t b_cols, const void* groups, const void* segs,
                     int num_groups, int M,
                     int N, int K, void* C, int64_t ldc, int64_t c_slot_stride, void* C2, int64_t ldc2,
-                    const void* aux, int64_t ld_aux, void* stream);
+                    const void* aux, int64_t ld_aux, const float* row_scale, float* row_partial, void* stream);
+
+/* ---------------------------------------------------------------- K2 permutation
+ * chunk_base[b][c][e] = exclusive prefix over chunks of chunk_counts (from mb_expert_histogram). */
+int mb_chunk_scan(const uint32_t* chunk_counts, uint32_t* chunk_base, int64_t nb, int32_t chunks, int32_t E,
+                  void* stream);
+/* Canonical permutation of one source GPU: perm[t][i] = {dst_gpu, dst_row} with the stable rank
+ * of (t,i) among the source's entries of expert e split over its copies by the integer counts in
+ * route_tab[E][maxc][4] {cum_end, dst_gpu, dst_row_base, 0} (round_split, replicate.py:501-525;
+ * copy order ReplicaPlacement.copies, replicate.py:55-56).  gate values are stored at
+ * dst_gate[dst_gpu][dst_row] (peer pointers) when both are non-NULL.
+ * Replaces: the dispatch leg of costmodel.flow_matrix (costmodel.py:91-108), which only counts. */
+int mb_permute_rank(const int32_t* idx, int64_t T, int32_t k, const float* gate, int32_t E, const uint32_t* chunk_base,
+                    int32_t chunk_tokens, const int32_t* route_tab, const int32_t* ncopies, int32_t maxc,
+                    float* const* dst_gate, int32_t* perm, void* stream);
+
+/* ---------------------------------------------------------------- K3 dispatch all-to-all
+ * Row scatter: row t of x ([T,h] bf16) is stored at dst_rows[perm.gpu] + perm.row*h for every
+ * choice i (device array of per-GPU base pointers, peers mapped over NVLink; 128-bit stores).
+ * Replaces: the dispatch link loads of costmodel._accumulate_direction (costmodel.py:64-88, 148). */
+int mb_scatter_rows(const void* x, int64_t T, int32_t k, int32_t h, const int32_t* perm, void* const* dst_rows,
+                    void* stream);
+
+/* ---------------------------------------------------------------- K6 combine
+ * out[t] = sum_i w[t,i] * src_rows[perm.gpu][perm.row] in fp32 (w = gate, or 1 when gate == NULL),
+ * rows read from peers; optionally scalar_out[t,i] = sum of the npart per-row partials at
+ * src_scalar[perm.gpu][perm.row*npart ...] (the dgate gather).
+ * Replaces: the mirrored combine leg of compute_loads (costmodel.py:149-150). */
+int mb_combine_rows(const void* const* src_rows, const int32_t* perm, const float* gate, int64_t T, int32_t k,
+                    int32_t h, void* out, const float* const* src_scalar, float* scalar_out, int32_t npart,
+                    void* stream);
+/* Expert-side combine backward (unfused reference variant of the gated dSwiGLU epilogue):
+ * dY = gate*dout in place, dgate = <dout, Y>, pad rows zeroed. */
+int mb_combine_bwd_expert(void* dout_rows, const void* y_rows, const float* gate_rows, float* dgate_rows,
+                          const int32_t* slot_tab, int32_t nslots, int64_t total_rows, int32_t h, void* stream);
+/* Zero the padding rows of every receive slot (slot_tab [nslots][4] {row_begin, rows_real, rows_pad, expert}). */
+int mb_zero_pad_rows(void* rows, const int32_t* slot_tab, int32_t nslots, int32_t h, void* stream);
+
+/* ---------------------------------------------------------------- K5 replicas
+ * dst[i] += sum_s srcs[s][i] (fp32, sources in list order): replica-gradient reduce into the owner,
+ * sources read from peers (replica_memory replicate.py:528-534). */
+int mb_accumulate_f32(float* dst, const float* const* srcs, int32_t nsrc, int64_t n, void* stream);
+/* Copy-engine copy (replica weight push into a peer's layer-shared replica slot). */
+int mb_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
+
+/* ---------------------------------------------------------------- peer memory / barrier
+ * CUDA-IPC symmetric buffers for the one-process-per-GPU box; the reference models links only
+ * (HardwareProfile.bw_nvlink/bw_rdma, topology.py:29-47). */
+int mb_ipc_handle_size(void);
+int mb_ipc_malloc(int64_t bytes, void** ptr, void* handle_out);
+int mb_ipc_open(const void* handle, void** ptr);
+int mb_ipc_close(void* ptr);
+int mb_device_free(void* ptr);
+/* Device-side barrier over per-rank flag arrays (flags[p] = rank p's array of world u32); traps
+ * after timeout_ns instead of hanging. */
+int mb_peer_barrier(uint32_t* const* flags, int32_t rank, int32_t world, uint32_t* epoch, int64_t timeout_ns,
+                    int32_t* error_flag, void* stream);
 
 #ifdef __cplusplus
 }

@@ -141,15 +141,21 @@ template <int VPL>
 __global__ void __launch_bounds__(256) combine_rows_kernel(const void* const* __restrict__ src_rows, const int2* __restrict__ perm,
                                                            const float* __restrict__ gate, int64_t T, int k, int h,
                                                            uint4* __restrict__ out, const float* const* __restrict__ src_scalar,
-                                                           float* __restrict__ scalar_out) {
+                                                           float* __restrict__ scalar_out, int npart) {
   const int lane = threadIdx.x & 31;
   const int64_t warp_global = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const int vrow = h >> 3;
   for (int64_t t = warp_global; t < T; t += nwarps) {
     if (scalar_out && lane < k) {
+      // per-row scalar = sum of its npart partials (fixed order: deterministic)
       const int2 pr = perm[t * k + lane];
-      scalar_out[t * k + lane] = (pr.x >= 0) ? src_scalar[pr.x][pr.y] : 0.0f;
+      float s = 0.0f;
+      if (pr.x >= 0) {
+        const float* src = src_scalar[pr.x] + static_cast<int64_t>(pr.y) * npart;
+        for (int q = 0; q < npart; ++q) s += src[q];
+      }
+      scalar_out[t * k + lane] = s;
     }
     for (int col0 = 0; col0 < vrow; col0 += 32 * VPL) {
       float acc[VPL][8];
@@ -334,9 +340,11 @@ extern "C" int mb_scatter_rows(const void* x, int64_t T, int32_t k, int32_t h, c
 }
 
 extern "C" int mb_combine_rows(const void* const* src_rows, const int32_t* perm, const float* gate, int64_t T, int32_t k,
-                               int32_t h, void* out, const float* const* src_scalar, float* scalar_out, void* stream) {
+                               int32_t h, void* out, const float* const* src_scalar, float* scalar_out,
+                               int32_t npart, void* stream) {
   MB_CHECK_ARG(src_rows && perm && out && T >= 0 && k >= 1 && k <= 32 && h >= 8 && h % 8 == 0, "bad combine args");
   MB_CHECK_ARG((scalar_out == nullptr) == (src_scalar == nullptr), "src_scalar and scalar_out go together");
+  MB_CHECK_ARG(npart >= 1, "npart must be >= 1");
   if (T == 0) return MB_OK;
   const int grid = grid_for(T, 8);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -344,11 +352,11 @@ extern "C" int mb_combine_rows(const void* const* src_rows, const int32_t* perm,
   const int2* pr = reinterpret_cast<const int2*>(perm);
   uint4* o = reinterpret_cast<uint4*>(out);
   if (vrow <= 64)
-    combine_rows_kernel<2><<<grid, 256, 0, s>>>(src_rows, pr, gate, T, k, h, o, src_scalar, scalar_out);
+    combine_rows_kernel<2><<<grid, 256, 0, s>>>(src_rows, pr, gate, T, k, h, o, src_scalar, scalar_out, npart);
   else if (vrow <= 128)
-    combine_rows_kernel<4><<<grid, 256, 0, s>>>(src_rows, pr, gate, T, k, h, o, src_scalar, scalar_out);
+    combine_rows_kernel<4><<<grid, 256, 0, s>>>(src_rows, pr, gate, T, k, h, o, src_scalar, scalar_out, npart);
   else
-    combine_rows_kernel<8><<<grid, 256, 0, s>>>(src_rows, pr, gate, T, k, h, o, src_scalar, scalar_out);
+    combine_rows_kernel<8><<<grid, 256, 0, s>>>(src_rows, pr, gate, T, k, h, o, src_scalar, scalar_out, npart);
   MB_CUDA_TRY(cudaGetLastError());
   return MB_OK;
 }

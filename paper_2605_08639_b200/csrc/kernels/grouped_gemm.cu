@@ -52,7 +52,7 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
                                int64_t b0_rows, const void* B1, int64_t b1_rows, int64_t b_cols,
                                const void* groups, const void* segs, int num_groups, int M, int N, int K, void* C,
                                int64_t ldc, int64_t c_slot_stride, void* C2, int64_t ldc2, const void* aux,
-                               int64_t ld_aux, void* stream) {
+                               int64_t ld_aux, const float* row_scale, float* row_partial, void* stream) {
   const bool force_single = (mode & 0x100) != 0 || !pair_enabled();
   mode &= 0xff;
   MB_CHECK_ARG(num_groups >= 0 && num_groups <= kMaxGroups, "num_groups %d outside [0, %d]", num_groups, kMaxGroups);
@@ -67,6 +67,7 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
   p.M = M; p.N = N; p.K = K;
   p.C = C; p.ldc = ldc; p.c_slot_stride = c_slot_stride;
   p.C2 = C2; p.ldc2 = ldc2; p.aux = aux; p.ld_aux = ld_aux;
+  p.rscale = row_scale; p.rpart = row_partial;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const bool pair = !force_single && N % 256 == 0 && (mode != MB_GEMM_WGRAD || M % 256 == 0);
   int rc;
@@ -84,6 +85,15 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
       MB_CHECK_ARG(C2 != nullptr, "SwiGLU epilogue needs the activation output");
       return pair ? launch_pair<false, false, false, EPI_SWIGLU>(p, s)
                   : launch_gemm<false, false, false, 256, EPI_SWIGLU>(p, s);
+    }
+    case MB_GEMM_DGRAD_DSWIGLU_GATED: {
+      MB_CHECK_ARG(!force_single && N % 256 == 0 && K % 64 == 0 && a_cols == K && b_cols == N,
+                   "gated dSwiGLU GEMM needs the CTA-pair kernel and N %% 256 == 0 (N=%d K=%d)", N, K);
+      MB_CHECK_ARG(aux && C2 && row_scale && row_partial, "gated dSwiGLU needs H, Act out, gate and partials");
+      if ((rc = make_tmap_bf16_2d(&p.tmA, A, a_cols, a_rows, a_cols * 2, 64, 128))) return rc;
+      if ((rc = make_tmap_bf16_2d(&p.tmB0, B0, b_cols, b0_rows, b_cols * 2, 64, 64))) return rc;
+      if ((rc = make_tmap_bf16_2d(&p.tmB1, B1, b_cols, b1_rows, b_cols * 2, 64, 64))) return rc;
+      return launch_pair<false, false, true, EPI_DSWIGLU_GATED>(p, s);
     }
     case MB_GEMM_DGRAD_STORE:
     case MB_GEMM_DGRAD_DSWIGLU: {

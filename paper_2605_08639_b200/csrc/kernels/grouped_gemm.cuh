@@ -25,6 +25,9 @@ enum GemmEpi : int {
   EPI_SWIGLU = 1,      // C = bf16(acc) (H, gate|up blocks of BN/2), C2 = bf16(silu(g)*u)
   EPI_DSWIGLU = 2,     // acc = dAct; aux = H; C = dH (gate|up blocks of 2*BN)
   EPI_ACC_F32 = 3,     // C_slot (+)= acc (fp32)
+  EPI_DSWIGLU_GATED = 4,  // acc = dout.W2 (unscaled); aux = H; rscale = gate per row:
+                          //   C = dH of gate*acc, C2 = gate*act (in place of Act, feeds dW2),
+                          //   rpart[row][N/128] = partial <acc, act> (dgate = <dout, Y>)
 };
 
 // Per-group descriptor (device memory, written by the dispatch-plan tables).
@@ -35,7 +38,8 @@ struct GemmGroup {
   int32_t flags;      // bit0: accumulate into C (W). bit1: B from tensor map 1 (replica slots).
   int32_t seg_begin;  // W: first entry in the segment table (K split over micro-batches)
   int32_t seg_count;  // W: number of segments; 0 means the single segment (a0, rows)
-  int32_t pad0, pad1;
+  int32_t rows_real;  // F: rows holding tokens (the rest of `rows` is padding); used by gated epilogues
+  int32_t pad1;
 };
 // W-mode K segment: `rows` token rows (multiple of 64) starting at token row `a0`.
 struct GemmSeg {
@@ -61,6 +65,8 @@ struct GemmParams {
   int64_t ldc2;
   const void* aux;
   int64_t ld_aux;
+  const float* rscale;  // per-row scale (gate) for EPI_DSWIGLU_GATED
+  float* rpart;         // per-row partial sums [rows][N/128] for EPI_DSWIGLU_GATED
 };
 
 template <int BN>

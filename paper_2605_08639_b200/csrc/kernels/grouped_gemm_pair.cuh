@@ -322,6 +322,79 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
             for (int v = 0; v < 4; ++v) { hgv[v] = ngv[v]; huv[v] = nuv[v]; }
           }
         }
+      } else if constexpr (kEpi == EPI_DSWIGLU_GATED) {
+        // acc = dout.W2 (the dout rows arrive unscaled); block b = 2*nb + ch2 of H / dH / Act
+        const int64_t row = gg.a0 + tile_row;
+        const bool real = valid && tile_row < gg.rows_real;
+        const int blk = tc.nb * 2 + ch2;
+        const int64_t hcol = static_cast<int64_t>(blk) * 256;
+        const __nv_bfloat16* hrow = reinterpret_cast<const __nv_bfloat16*>(p.aux) + row * p.ld_aux + hcol;
+        __nv_bfloat16* drow = reinterpret_cast<__nv_bfloat16*>(p.C) + row * p.ldc + hcol;
+        __nv_bfloat16* arow = reinterpret_cast<__nv_bfloat16*>(p.C2) + row * p.ldc2 + static_cast<int64_t>(blk) * 128;
+        const float gate = real ? p.rscale[row] : 0.0f;
+        float part = 0.0f;
+        uint4 hgv[4], huv[4], ngv[4], nuv[4];
+        if (real) {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            hgv[v] = reinterpret_cast<const uint4*>(hrow)[v];
+            huv[v] = reinterpret_cast<const uint4*>(hrow + 128)[v];
+          }
+        }
+#pragma unroll 1
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t d[32];
+          tmem_ld_32x32b_x32(t_acc + ch2 * 128 + ch * 32, d);
+          if (real && ch + 1 < 4) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              ngv[v] = reinterpret_cast<const uint4*>(hrow + (ch + 1) * 32)[v];
+              nuv[v] = reinterpret_cast<const uint4*>(hrow + 128 + (ch + 1) * 32)[v];
+            }
+          }
+          tmem_ld_wait();
+          if (!valid) continue;
+          uint4* og = reinterpret_cast<uint4*>(drow + ch * 32);
+          uint4* ou = reinterpret_cast<uint4*>(drow + 128 + ch * 32);
+          uint4* oa = reinterpret_cast<uint4*>(arow + ch * 32);
+          if (!real) {  // padding rows: zero dH and gate*act so the wgrad sees exact zeros
+#pragma unroll
+            for (int v = 0; v < 4; ++v) og[v] = ou[v] = oa[v] = make_uint4(0, 0, 0, 0);
+            continue;
+          }
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const uint32_t gw[4] = {hgv[v].x, hgv[v].y, hgv[v].z, hgv[v].w};
+            const uint32_t uw[4] = {huv[v].x, huv[v].y, huv[v].z, huv[v].w};
+            uint32_t rg[4], ru[4], ra[4];
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+              float dg2[2], du2[2], ag2[2];
+#pragma unroll
+              for (int h2 = 0; h2 < 2; ++h2) {
+                const float gv = h2 ? bf16hi(gw[w]) : bf16lo(gw[w]);
+                const float uv = h2 ? bf16hi(uw[w]) : bf16lo(uw[w]);
+                const float raw = __uint_as_float(d[8 * v + 2 * w + h2]);
+                const float s = __fdividef(1.0f, 1.0f + __expf(-gv));
+                const float act = gv * s * uv;
+                part += raw * act;
+                const float dav = gate * raw;
+                du2[h2] = dav * gv * s;
+                dg2[h2] = dav * uv * s * (1.0f + gv * (1.0f - s));
+                ag2[h2] = gate * act;
+              }
+              rg[w] = pack_bf16x2(dg2[0], dg2[1]);
+              ru[w] = pack_bf16x2(du2[0], du2[1]);
+              ra[w] = pack_bf16x2(ag2[0], ag2[1]);
+            }
+            og[v] = make_uint4(rg[0], rg[1], rg[2], rg[3]);
+            ou[v] = make_uint4(ru[0], ru[1], ru[2], ru[3]);
+            oa[v] = make_uint4(ra[0], ra[1], ra[2], ra[3]);
+          }
+#pragma unroll
+          for (int v = 0; v < 4; ++v) { hgv[v] = ngv[v]; huv[v] = nuv[v]; }
+        }
+        if (real) p.rpart[row * (p.N / 128) + blk] = part;
       } else {  // EPI_ACC_F32
         const bool accumulate = (gg.flags & 1) != 0;
         float* crow = reinterpret_cast<float*>(p.C) + gg.slot * p.c_slot_stride +

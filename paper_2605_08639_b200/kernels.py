@@ -16,6 +16,7 @@ GEMM_FWD_SWIGLU = 1
 GEMM_DGRAD_STORE = 2
 GEMM_DGRAD_DSWIGLU = 3
 GEMM_WGRAD = 4
+GEMM_DGRAD_DSWIGLU_GATED = 5
 
 GROUP_FIELDS = 8  # int32 rows, a0, slot, flags, seg_begin, seg_count, pad, pad
 FLAG_ACCUMULATE = 1
@@ -32,15 +33,17 @@ def _need_cuda(*tensors):
             raise ValueError("data-plane ops take CUDA tensors (there is no CPU path)")
 
 
-def make_groups(rows, a0, slot, flags=None, seg_begin=None, seg_count=None, device="cuda") -> torch.Tensor:
-    """Pack per-group (rows, a0, slot, flags, seg_begin, seg_count) into the int32 [G, 8] table."""
+def make_groups(rows, a0, slot, flags=None, seg_begin=None, seg_count=None, rows_real=None,
+                device="cuda") -> torch.Tensor:
+    """Pack per-group (rows, a0, slot, flags, seg_begin, seg_count, rows_real) into the int32 [G, 8] table."""
     n = len(rows)
     z = [0] * n
     flags = z if flags is None else flags
     seg_begin = z if seg_begin is None else seg_begin
     seg_count = z if seg_count is None else seg_count
+    rows_real = rows if rows_real is None else rows_real
     tab = np.zeros((n, GROUP_FIELDS), dtype=np.int32)
-    for c, v in enumerate((rows, a0, slot, flags, seg_begin, seg_count)):
+    for c, v in enumerate((rows, a0, slot, flags, seg_begin, seg_count, rows_real)):
         tab[:, c] = np.asarray(v, dtype=np.int64)
     return torch.from_numpy(tab).to(device)
 
@@ -69,7 +72,8 @@ def expert_histogram(idx: torch.Tensor, num_experts: int, chunk_tokens: int = 32
 def grouped_gemm(mode: int, A: torch.Tensor, B0: torch.Tensor, groups: torch.Tensor, *, M: int = 0, N: int,
                  K: int = 0, C: torch.Tensor, C2: torch.Tensor | None = None, aux: torch.Tensor | None = None,
                  B1: torch.Tensor | None = None, c_slot_stride: int = 0,
-                 segs: torch.Tensor | None = None) -> None:
+                 segs: torch.Tensor | None = None, row_scale: torch.Tensor | None = None,
+                 row_partial: torch.Tensor | None = None, single_cta: bool = False) -> None:
     """K4: tcgen05 grouped GEMM; see include/mb_kernels.h for the five modes."""
     _need_cuda(A, B0, groups, C, C2, aux, B1)
     for t in (A, B0, B1):
@@ -86,9 +90,9 @@ def grouped_gemm(mode: int, A: torch.Tensor, B0: torch.Tensor, groups: torch.Ten
     ldc2 = 0 if C2 is None else C2.shape[-1]
     ld_aux = 0 if aux is None else aux.shape[-1]
     lib = _lib()
-    nat.check(lib.mb_grouped_gemm(mode, A.data_ptr(), a_rows, a_cols, B0.data_ptr(), b0_rows,
-                                  nat.ptr(B1), b1_rows, b_cols, groups.data_ptr(), nat.ptr(segs), groups.shape[0],
-                                  M, N, K,
+    nat.check(lib.mb_grouped_gemm(mode | (0x100 if single_cta else 0), A.data_ptr(), a_rows, a_cols,
+                                  B0.data_ptr(), b0_rows, nat.ptr(B1), b1_rows, b_cols, groups.data_ptr(),
+                                  nat.ptr(segs), groups.shape[0], M, N, K,
                                   C.data_ptr(), ldc, c_slot_stride, nat.ptr(C2), ldc2, nat.ptr(aux), ld_aux,
-                                  nat.stream_ptr()),
+                                  nat.ptr(row_scale), nat.ptr(row_partial), nat.stream_ptr()),
               lib, "mb_grouped_gemm")

@@ -189,12 +189,13 @@ class MoEDataPlane:
         self.slots = max(plan.slots, 1)
         self.rep_cap = max(1, self.slots * micro_batches)
         bf, f4 = 2, 4
+        self.npart = hp // 128   # dgate partials per row (one per 128-column block of h')
         R, MB = self.R, micro_batches
         S = self.M + self.rep_cap
         # ---- symmetric arena (peer-visible buffers; identical layout on every rank)
         sizes = {
             "xr": MB * R * h * bf, "y": MB * R * h * bf, "dyr": MB * R * h * bf, "dxp": MB * R * h * bf,
-            "gate_r": MB * R * f4, "dgate_r": MB * R * f4,
+            "gate_r": MB * R * f4, "dgate_r": MB * R * self.npart * f4,
             "w1r": self.slots * 2 * hp * h * bf, "w2r": self.slots * h * hp * bf,
             "w1": self.M * 2 * hp * h * bf, "w2": self.M * h * hp * bf,
             "gw1": S * 2 * hp * h * f4, "gw2": S * h * hp * f4,
@@ -208,7 +209,7 @@ class MoEDataPlane:
         self.dYr = A.local(self.off["dyr"], (MB, R, h), torch.bfloat16)
         self.dXp = A.local(self.off["dxp"], (MB, R, h), torch.bfloat16)
         self.gate_r = A.local(self.off["gate_r"], (MB, R), torch.float32)
-        self.dgate_r = A.local(self.off["dgate_r"], (MB, R), torch.float32)
+        self.dgate_r = A.local(self.off["dgate_r"], (MB, R, self.npart), torch.float32)
         self.W1r = A.local(self.off["w1r"], (self.slots, 2 * hp, h), torch.bfloat16)
         self.W2r = A.local(self.off["w2r"], (self.slots, h, hp), torch.bfloat16)
         self.W1 = A.local(self.off["w1"], (self.M, 2 * hp, h), torch.bfloat16)
@@ -232,7 +233,7 @@ class MoEDataPlane:
         self.ptr_dyr = A.peer_table(self.off["dyr"], R * h * bf, MB)
         self.ptr_dxp = A.peer_table(self.off["dxp"], R * h * bf, MB)
         self.ptr_gate = A.peer_table(self.off["gate_r"], R * f4, MB)
-        self.ptr_dgate = A.peer_table(self.off["dgate_r"], R * f4, MB)
+        self.ptr_dgate = A.peer_table(self.off["dgate_r"], R * self.npart * f4, MB)
         self.side = torch.cuda.Stream(device=self.device)
         self.launches = 0
         self.timing = False       # record CUDA events around every K4 launch (bench roofline)
@@ -286,6 +287,7 @@ class MoEDataPlane:
             g[:n, 1] = st[:n, 0]
             g[:n, 2] = sw[:n, 0]
             g[:n, 3] = np.where(sw[:n, 1] > 0, K.FLAG_REPLICA, 0)
+            g[:n, 6] = st[:n, 1]
             groups.append(g)
             slots.append(st)
             nsl.append(n)
@@ -489,32 +491,32 @@ class MoEDataPlane:
         A.barrier()  # every expert output is ready
         # K6: combine over peer loads
         self._k("mb_combine_rows", self.ptr_y[m].data_ptr(), self.perm[m].data_ptr(), gates.data_ptr(),
-                T, k, h, out.data_ptr(), None, None, st)
+                T, k, h, out.data_ptr(), None, None, 1, st)
 
     def _backward_mb(self, m, dout, dx, dgate, st):
         E, k, h, hp = self.shape.num_experts, self.shape.top_k, self.shape.hidden, self.shape.ffn
         T, R = self.T, self.R
         A = self.arena
-        # dout rows to the serving GPUs (same permutation as the forward dispatch)
+        # dout rows (unscaled) to the serving GPUs, same permutation as the forward dispatch
         self._k("mb_scatter_rows", dout.data_ptr(), T, k, h, self.perm[m].data_ptr(), self.ptr_dyr[m].data_ptr(), st)
         A.barrier()
-        total = int(self.plan.mbs[m].total_rows[self.rank])
-        self._k("mb_combine_bwd_expert", self.dYr[m].data_ptr(), self.Y[m].data_ptr(), self.gate_r[m].data_ptr(),
-                self.dgate_r[m].data_ptr(), self.slot_tab[m].data_ptr(), self.nslots[m], total, h, st)
         ng = self.nslots[m]
         if ng:
             g = self.groups[m]
             rows = self.real_rows(m)
+            # dAct = dout.W2 with the combine backward fused in the epilogue: gate applied per row,
+            # dgate partials <dout.W2, act> = <dout, Y>, gate*act written over Act for dW2
             with self._timed(2.0 * rows * h * hp):
-                K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU, self.dYr[m], self.W2, g[:ng], N=hp, K=h, C=self.dH[m],
-                               aux=self.H[m], B1=self.W2r)
+                K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU_GATED, self.dYr[m], self.W2, g[:ng], N=hp, K=h, C=self.dH[m],
+                               C2=self.Act[m], aux=self.H[m], B1=self.W2r, row_scale=self.gate_r[m],
+                               row_partial=self.dgate_r[m])
             with self._timed(4.0 * rows * h * hp):
                 K.grouped_gemm(K.GEMM_DGRAD_STORE, self.dH[m], self.W1, g[:ng], N=h, K=2 * hp, C=self.dXp[m],
                                B1=self.W1r)
             self.launches += 2
         A.barrier()
         self._k("mb_combine_rows", self.ptr_dxp[m].data_ptr(), self.perm[m].data_ptr(), None, T, k, h, dx.data_ptr(),
-                self.ptr_dgate[m].data_ptr(), dgate.data_ptr(), st)
+                self.ptr_dgate[m].data_ptr(), dgate.data_ptr(), self.npart, st)
 
     def _wgrad(self, st):
         h, hp = self.shape.hidden, self.shape.ffn

@@ -116,6 +116,56 @@ def test_dgrad_dswiglu():
         assert rel_err(dH[sl], ref) < 2e-2
 
 
+def test_dgrad_dswiglu_gated():
+    """Fused combine-backward: raw dout rows in, gate per row, dgate partials, gate*act out."""
+    torch.manual_seed(7)
+    hp, hd = 512, 256
+    rows, real = [256, 128], [200, 128]
+    a0, R = _row_groups(rows)
+    dout = torch.randn(R, hd, device=DEV).bfloat16()
+    W2 = (torch.randn(2, hd, hp, device=DEV) * hd ** -0.5).bfloat16()
+    H = torch.randn(R, 2 * hp, device=DEV).bfloat16()
+    gate = torch.rand(R, device=DEV)
+    dH = torch.full((R, 2 * hp), float("nan"), device=DEV).bfloat16()
+    actg = torch.full((R, hp), float("nan"), device=DEV).bfloat16()
+    part = torch.zeros(R, hp // 128, device=DEV)
+    K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU_GATED, dout, W2, K.make_groups(rows, a0, [0, 1], rows_real=real), N=hp, K=hd,
+                   C=dH, C2=actg, aux=H, row_scale=gate, row_partial=part)
+    torch.cuda.synchronize()
+    for g in range(2):
+        sl = slice(a0[g], a0[g] + real[g])
+        raw = dout[sl].float() @ W2[g].float()
+        hb = H[sl].float().view(real[g], -1, 2, 128)
+        gt, up = hb[:, :, 0].reshape(real[g], hp), hb[:, :, 1].reshape(real[g], hp)
+        s = torch.sigmoid(gt)
+        act = gt * s * up
+        da = gate[sl, None] * raw
+        dg = da * up * s * (1 + gt * (1 - s))
+        du = da * gt * s
+        ref = torch.stack([dg.view(real[g], -1, 128), du.view(real[g], -1, 128)], dim=2).reshape(real[g], 2 * hp)
+        assert rel_err(dH[sl], ref) < 2e-2
+        assert rel_err(actg[sl], gate[sl, None] * act) < 2e-2
+        assert rel_err(part[sl].sum(1), (raw * act).sum(1)) < 2e-2
+        pad = slice(a0[g] + real[g], a0[g] + rows[g])
+        assert torch.all(dH[pad] == 0) and torch.all(actg[pad] == 0)
+
+
+def test_single_cta_path_matches_pair():
+    torch.manual_seed(8)
+    N, Kd = 512, 256
+    rows = [384, 128]
+    a0, R = _row_groups(rows)
+    A = torch.randn(R, Kd, device=DEV).bfloat16()
+    W = (torch.randn(2, N, Kd, device=DEV) * Kd ** -0.5).bfloat16()
+    C1 = torch.zeros(R, N, device=DEV).bfloat16()
+    C2 = torch.zeros(R, N, device=DEV).bfloat16()
+    g = K.make_groups(rows, a0, [1, 0])
+    K.grouped_gemm(K.GEMM_FWD_STORE, A, W, g, N=N, K=Kd, C=C1)
+    K.grouped_gemm(K.GEMM_FWD_STORE, A, W, g, N=N, K=Kd, C=C2, single_cta=True)
+    torch.cuda.synchronize()
+    assert rel_err(C1, C2) < 1e-2
+
+
 def test_wgrad_accumulate():
     torch.manual_seed(5)
     Md, Nd = 256, 512
