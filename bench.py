@@ -318,6 +318,7 @@ def main():
         args.policies = args.headline + "," + args.policies
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    os.environ["NCCL_DEBUG"] = "WARN"  # keep NCCL's version banner off stdout: one JSON line only
     if args.impl == "reference":
         return run_reference(args, rank, world)
     import torch

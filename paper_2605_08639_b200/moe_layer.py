@@ -2,26 +2,28 @@
 
 This is the data plane the reference only models (sim.evaluate_bundle, sim.py:89-110:
 flow_matrix -> comp = flow.sum(0) -> dispatch/combine link loads -> T = max comp + max comm).
-Per micro-batch, on every rank (one process per GPU):
+One process per GPU; every rank runs, per step of MB micro-batches:
 
   K1  expert histogram of the local top-k indices (+ chunk scan)           histogram.cu
-  K5  replica weight push into the layer-shared replica slots (owners)      copy engine, peer
+  K5  replica weight push into the replica slots of this step (owners)      copy engine, peer
   K2  stable-rank permutation -> (dst GPU, dst row) per (token, choice)    dispatch.cu
   K3  row scatter straight into peer receive buffers (dispatch A2A)         dispatch.cu
-  K4  tcgen05 grouped GEMM: H = X W1^T (+SwiGLU), Y = Act W2^T              grouped_gemm.cu
+  K4  tcgen05 grouped GEMM: H = X W1^T (+SwiGLU), Y = Act W2^T              grouped_gemm*.cu
   K6  combine: out[t] = sum_i gate[t,i] * Y[perm(t,i)] over peer loads      dispatch.cu
-  bwd K3 (dout scatter) -> expert-side dY = gate*dout, dgate = <dout,Y> -> K4 dAct(+dSwiGLU),
-      dX -> K6 un-permute sum + dgate gather
-and once per step K4 wgrad for every local slot with K split over all micro-batches (the
-fp32 weight-gradient accumulation window), then K5^T: owners pull replica gradients.
+  bwd K3 (raw dout scatter) -> K4 dAct with the combine backward fused in its epilogue
+      (gate scaling, dgate partials, gate*act) -> K4 dX -> K6 un-permute sum + dgate gather
+  once per step: K4 wgrad of every local slot, K contracted over all micro-batches (the fp32
+      gradient-accumulation window), then K5^T: owners pull replica gradients from peers.
 
-Routing is replayed, so every count, row offset and replica is known before the step: the
-host planners run once per step (StepPlan) and the kernels never exchange sizes.
+Two streams: the compute stream runs the GEMMs, the comm stream runs dispatch / combine and
+every device barrier (totally ordered per rank), linked by per-micro-batch events, so the
+NVLink all-to-all of one micro-batch overlaps the tensor-core work of another.  Routing is
+replayed, so every count, row offset and replica is known before the step: the host planners
+run once per step (StepPlan) and the kernels never exchange sizes.
 """
 
 from __future__ import annotations
 
-import math
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -30,7 +32,6 @@ import torch
 from . import _native as nat
 from . import kernels as K
 from . import policies as pol
-from . import reordering as ro
 from . import replication as rep
 from . import traces as rt
 from .cluster import ClusterTopology, HardwareProfile
@@ -49,8 +50,8 @@ class LayerShape:
     ffn: int
 
     def check(self) -> None:
-        if self.hidden % 256 or self.ffn % 128:
-            raise ValueError("kernels need hidden % 256 == 0 and ffn % 128 == 0")
+        if self.hidden % 256 or self.ffn % 256:
+            raise ValueError("kernels need hidden % 256 == 0 and ffn % 256 == 0")
 
 
 @dataclass
@@ -81,17 +82,17 @@ class StepPlan:
     rep_experts: list = field(default_factory=list)   # per GPU: sorted experts replicated onto it this step
     slots: int = 0
 
-    @property
-    def home_local(self) -> list:
-        return [np.flatnonzero(self.home == g) for g in range(self.world)]
-
     def executed_loads(self) -> np.ndarray:
         """(MB, G) GEMM rows per GPU actually executed (= costmodel comp with integer splits)."""
         return np.stack([mb.flow.sum(axis=0) for mb in self.mbs])
 
     def skew(self) -> float:
-        loads = self.executed_loads()
-        return float(np.mean([rt.skewness(l) for l in loads]))
+        """Mean over micro-batches of max/mean executed GPU load (routing.skewness, routing.py:483-493)."""
+        return float(np.mean([rt.skewness(l) for l in self.executed_loads()]))
+
+    def nvlink_rows(self) -> np.ndarray:
+        """(MB, G) rows each GPU sends to other GPUs per A2A phase (off-diagonal flow)."""
+        return np.stack([mb.flow.sum(axis=1) - np.diag(mb.flow) for mb in self.mbs])
 
 
 def build_step_plan(policy: str, mats: np.ndarray, topo: ClusterTopology, model: rt.ModelProfile,
@@ -172,7 +173,7 @@ def deinterleave_w1(w1: torch.Tensor) -> tuple:
 
 
 class MoEDataPlane:
-    """Per-rank device state for one MoE layer: home experts, the layer-shared replica slots,
+    """Per-rank device state for one MoE layer: home experts, per-micro-batch replica slots,
     fp32 gradients, per-micro-batch receive/activation buffers and the step tables."""
 
     def __init__(self, comm: Comm, shape: LayerShape, tokens: int, micro_batches: int, plan: StepPlan,
@@ -192,17 +193,18 @@ class MoEDataPlane:
         self.npart = hp // 128   # dgate partials per row (one per 128-column block of h')
         R, MB = self.R, micro_batches
         S = self.M + self.rep_cap
+        self.w1_bytes, self.w2_bytes = 2 * hp * h * bf, h * hp * bf
         # ---- symmetric arena (peer-visible buffers; identical layout on every rank)
         sizes = {
             "xr": MB * R * h * bf, "y": MB * R * h * bf, "dyr": MB * R * h * bf, "dxp": MB * R * h * bf,
             "gate_r": MB * R * f4, "dgate_r": MB * R * self.npart * f4,
-            "w1r": self.slots * 2 * hp * h * bf, "w2r": self.slots * h * hp * bf,
-            "w1": self.M * 2 * hp * h * bf, "w2": self.M * h * hp * bf,
+            "w1r": MB * self.slots * self.w1_bytes, "w2r": MB * self.slots * self.w2_bytes,
+            "w1": self.M * self.w1_bytes, "w2": self.M * self.w2_bytes,
             "gw1": S * 2 * hp * h * f4, "gw2": S * h * hp * f4,
         }
         total = sum((v + 1023) // 1024 * 1024 for v in sizes.values()) + 1024 * len(sizes)
         self.arena = SymmetricArena(comm, total, self.device)
-        self.off = {k: self.arena.alloc(v) for k, v in sizes.items()}
+        self.off = {key: self.arena.alloc(v) for key, v in sizes.items()}
         A = self.arena
         self.Xr = A.local(self.off["xr"], (MB, R, h), torch.bfloat16)
         self.Y = A.local(self.off["y"], (MB, R, h), torch.bfloat16)
@@ -210,8 +212,8 @@ class MoEDataPlane:
         self.dXp = A.local(self.off["dxp"], (MB, R, h), torch.bfloat16)
         self.gate_r = A.local(self.off["gate_r"], (MB, R), torch.float32)
         self.dgate_r = A.local(self.off["dgate_r"], (MB, R, self.npart), torch.float32)
-        self.W1r = A.local(self.off["w1r"], (self.slots, 2 * hp, h), torch.bfloat16)
-        self.W2r = A.local(self.off["w2r"], (self.slots, h, hp), torch.bfloat16)
+        self.W1r = A.local(self.off["w1r"], (MB, self.slots, 2 * hp, h), torch.bfloat16)
+        self.W2r = A.local(self.off["w2r"], (MB, self.slots, h, hp), torch.bfloat16)
         self.W1 = A.local(self.off["w1"], (self.M, 2 * hp, h), torch.bfloat16)
         self.W2 = A.local(self.off["w2"], (self.M, h, hp), torch.bfloat16)
         self.gW1 = A.local(self.off["gw1"], (S, 2 * hp, h), torch.float32)
@@ -234,12 +236,14 @@ class MoEDataPlane:
         self.ptr_dxp = A.peer_table(self.off["dxp"], R * h * bf, MB)
         self.ptr_gate = A.peer_table(self.off["gate_r"], R * f4, MB)
         self.ptr_dgate = A.peer_table(self.off["dgate_r"], R * self.npart * f4, MB)
-        self.side = torch.cuda.Stream(device=self.device)
+        self.xs = torch.cuda.Stream(device=self.device)      # comm stream: dispatch / combine / barriers
+        self.cps = torch.cuda.Stream(device=self.device)     # copy-engine stream: replica pushes
         self.launches = 0
         self.timing = False       # record CUDA events around every K4 launch (bench roofline)
         self.gemm_events = []     # (start, end, algorithmic FLOPs)
         self.load_plan(plan)
 
+    # ------------------------------------------------------------------ helpers
     def _timed(self, flops: float):
         """Context manager recording CUDA events on the current stream around a K4 launch."""
         dp = self
@@ -268,12 +272,11 @@ class MoEDataPlane:
         if max((len(r) for r in plan.rep_experts), default=0) > self.rep_cap:
             raise ValueError("plan replicates more experts than the replica gradient buffer holds")
         self.plan = plan
-        d, MB, dev = self.rank, self.MB, self.device
+        d, dev = self.rank, self.device
         E = self.shape.num_experts
         home = plan.home
         self.home_experts = np.flatnonzero(home == d)
         local_of = {int(ex): int(np.flatnonzero(np.flatnonzero(home == home[ex]) == ex)[0]) for ex in range(E)}
-        self.local_of = local_of
         route, ncop, groups, slots, nsl, pushes = [], [], [], [], [], []
         max_slots = plan.max_slots
         for m, mbp in enumerate(plan.mbs):
@@ -282,6 +285,8 @@ class MoEDataPlane:
             st = mbp.slot_tab[d]
             sw = mbp.slot_w[d]
             n = int(mbp.nslots[d])
+            if int(sw[:n, 0][sw[:n, 1] > 0].max(initial=-1)) >= self.slots:
+                raise ValueError("plan uses more replica slots than allocated")
             g = np.zeros((max_slots, K.GROUP_FIELDS), dtype=np.int32)
             g[:n, 0] = st[:n, 2]
             g[:n, 1] = st[:n, 0]
@@ -291,14 +296,12 @@ class MoEDataPlane:
             groups.append(g)
             slots.append(st)
             nsl.append(n)
-            # replica pushes this rank performs as the owner: (dst gpu, dst slot, local expert)
-            pl = []
+            # replica pushes this rank performs as the owner: (dst gpu, micro-batch, dst slot, local expert)
             for dst in range(self.world):
                 stt, sww = mbp.slot_tab[dst], mbp.slot_w[dst]
                 for s in range(int(mbp.nslots[dst])):
                     if sww[s, 1] and home[stt[s, 3]] == d:
-                        pl.append((dst, int(sww[s, 0]), local_of[int(stt[s, 3])]))
-            pushes.append(pl)
+                        pushes.append((dst, m, int(sww[s, 0]), local_of[int(stt[s, 3])]))
         self.route_tab = torch.from_numpy(np.stack(route)).to(dev)
         self.ncopies = torch.from_numpy(np.stack(ncop)).to(dev)
         self.groups = torch.from_numpy(np.stack(groups)).to(dev)
@@ -309,8 +312,7 @@ class MoEDataPlane:
         wg, segs = [], []
         R = self.R
         for loc, ex in enumerate(self.home_experts):
-            s0 = len(segs)
-            tot = 0
+            s0, tot = len(segs), 0
             for m, mbp in enumerate(plan.mbs):
                 st = mbp.slot_tab[d]
                 for s in range(int(mbp.nslots[d])):
@@ -319,8 +321,7 @@ class MoEDataPlane:
                         tot += int(st[s, 2])
             wg.append((tot, 0, loc, K.FLAG_ACCUMULATE, s0, len(segs) - s0))
         for q, ex in enumerate(plan.rep_experts[d]):
-            s0 = len(segs)
-            tot = 0
+            s0, tot = len(segs), 0
             for m, mbp in enumerate(plan.mbs):
                 st, sw = mbp.slot_tab[d], mbp.slot_w[d]
                 for s in range(int(mbp.nslots[d])):
@@ -333,29 +334,25 @@ class MoEDataPlane:
             wtab[i, :6] = row
         self.wgroups = torch.from_numpy(wtab).to(dev)
         self.wsegs = torch.from_numpy(np.asarray(segs if segs else [(0, 0)], dtype=np.int32).reshape(-1, 2)).to(dev)
-        # replicas of zero-row experts must still be overwritten: zero the replica grads per step
-        self.n_rep_here = len(plan.rep_experts[d])
-        # ---- replica gradient reduce lists (this rank as owner): (local expert, [(src rank, q)])
-        reduce = []
-        mn1 = 2 * self.shape.ffn * self.shape.hidden
+        # ---- replica gradient reduce lists (this rank as owner): only replicas that served rows
         rep_rows = {}
         for mbp in plan.mbs:
             for p in range(self.world):
                 stt, sww = mbp.slot_tab[p], mbp.slot_w[p]
                 for s in range(int(mbp.nslots[p])):
                     if sww[s, 1]:
-                        rep_rows[(p, int(stt[s, 3]))] = rep_rows.get((p, int(stt[s, 3])), 0) + int(stt[s, 2])
+                        key = (p, int(stt[s, 3]))
+                        rep_rows[key] = rep_rows.get(key, 0) + int(stt[s, 2])
+        mn1 = 2 * self.shape.ffn * self.shape.hidden
+        self.reduce = []
         for loc, ex in enumerate(self.home_experts):
             srcs = [(p, plan.rep_experts[p].index(int(ex))) for p in range(self.world)
                     if p != d and int(ex) in plan.rep_experts[p] and rep_rows.get((p, int(ex)), 0) > 0]
             if srcs:
-                reduce.append((loc, srcs))
-        self.reduce = []
-        for loc, srcs in reduce:
-            p1 = [self.arena.peer_ptr(p, self.off["gw1"]) + (self.M + q) * mn1 * 4 for p, q in srcs]
-            p2 = [self.arena.peer_ptr(p, self.off["gw2"]) + (self.M + q) * mn1 // 2 * 4 for p, q in srcs]
-            self.reduce.append((loc, torch.tensor(p1, dtype=torch.int64, device=dev),
-                                torch.tensor(p2, dtype=torch.int64, device=dev), len(srcs)))
+                p1 = [self.arena.peer_ptr(p, self.off["gw1"]) + (self.M + q) * mn1 * 4 for p, q in srcs]
+                p2 = [self.arena.peer_ptr(p, self.off["gw2"]) + (self.M + q) * (mn1 // 2) * 4 for p, q in srcs]
+                self.reduce.append((loc, torch.tensor(p1, dtype=torch.int64, device=dev),
+                                    torch.tensor(p2, dtype=torch.int64, device=dev), len(srcs)))
 
     # ------------------------------------------------------------------ weights
     def set_weights(self, w_gate: torch.Tensor, w_up: torch.Tensor, w_down: torch.Tensor) -> None:
@@ -367,43 +364,155 @@ class MoEDataPlane:
         self.gW1.zero_()
         self.gW2.zero_()
 
-    # ------------------------------------------------------------------ kernels
-    def _lib(self):
-        return nat.kernels()
-
+    # ------------------------------------------------------------------ step
     def _k(self, name, *args):
-        lib = self._lib()
+        lib = nat.kernels()
         nat.check(getattr(lib, name)(*args), lib, name)
         self.launches += 1
-
-    def _stream(self):
-        return nat.stream_ptr()
 
     def forward_backward(self, x: torch.Tensor, idx: torch.Tensor, gates: torch.Tensor, dout: torch.Tensor,
                          out: torch.Tensor, dx: torch.Tensor, dgate: torch.Tensor, hooks=None) -> None:
         """One training step of the layer over MB micro-batches (inputs [MB, T, ...] on device).
-        Writes out / dx / dgate and accumulates fp32 expert gradients; asynchronous.
-        `hooks` (optional) gets before(m) / after_forward(m) / after_backward(m) callbacks on the
-        compute stream (used by step_host to overlap host copies)."""
-        st = self._stream()
-        A = self.arena
-        A.barrier()  # previous step's readers of our receive buffers are done
-        for m in range(self.MB):
+        Writes out / dx / dgate and accumulates fp32 expert gradients.  Asynchronous with respect
+        to the host; the current stream is ordered after all of it on return.  `hooks` (optional)
+        gets inputs_ready(m, stream), after_forward(m, stream), after_backward(m, stream)."""
+        MB = self.MB
+        h, hp, k, T = self.shape.hidden, self.shape.ffn, self.shape.top_k, self.T
+        E = self.shape.num_experts
+        cs, xs, A = torch.cuda.current_stream(), self.xs, self.arena
+        st_x = xs.cuda_stream
+        chunks = (T + CHUNK - 1) // CHUNK
+        xs.wait_stream(cs)
+        # K5: replica weights of every micro-batch into the peers' slots (copy engine)
+        if self.pushes:
+            self.cps.wait_stream(cs)
+            lib = nat.kernels()
+            for dst, m, slot, loc in self.pushes:
+                d1 = A.peer_ptr(dst, self.off["w1r"]) + (m * self.slots + slot) * self.w1_bytes
+                d2 = A.peer_ptr(dst, self.off["w2r"]) + (m * self.slots + slot) * self.w2_bytes
+                nat.check(lib.mb_memcpy_async(d1, self.W1[loc].data_ptr(), self.w1_bytes, self.cps.cuda_stream),
+                          lib, "replica push")
+                nat.check(lib.mb_memcpy_async(d2, self.W2[loc].data_ptr(), self.w2_bytes, self.cps.cuda_stream),
+                          lib, "replica push")
+            xs.wait_stream(self.cps)
+        # ---- dispatch of every micro-batch (comm stream)
+        ev_disp = []
+        for m in range(MB):
             if hooks:
-                hooks.before(m)
-            self._forward_mb(m, x[m], idx[m], gates[m], out[m], st)
+                hooks.inputs_ready(m, xs)
+            self._k("mb_expert_histogram", idx[m].data_ptr(), 1, T, k, E, self.counts[m].data_ptr(),
+                    self.chunk_counts[m].data_ptr(), CHUNK, st_x)
+            self._k("mb_chunk_scan", self.chunk_counts[m].data_ptr(), self.chunk_base[m].data_ptr(), 1, chunks, E,
+                    st_x)
+            self._k("mb_zero_pad_rows", self.Xr[m].data_ptr(), self.slot_tab[m].data_ptr(), self.nslots[m], h, st_x)
+            if m == 0:
+                A.barrier(xs)  # all ranks: previous step drained, replica pushes landed
+            self._k("mb_permute_rank", idx[m].data_ptr(), T, k, gates[m].data_ptr(), E,
+                    self.chunk_base[m].data_ptr(), CHUNK, self.route_tab[m].data_ptr(), self.ncopies[m].data_ptr(),
+                    self.plan.maxc, self.ptr_gate[m].data_ptr(), self.perm[m].data_ptr(), st_x)
+            self._k("mb_scatter_rows", x[m].data_ptr(), T, k, h, self.perm[m].data_ptr(), self.ptr_xr[m].data_ptr(),
+                    st_x)
+            A.barrier(xs)  # rows of micro-batch m have landed everywhere
+            ev = torch.cuda.Event()
+            ev.record(xs)
+            ev_disp.append(ev)
+        # ---- forward GEMMs (compute stream)
+        ev_fwd = []
+        for m in range(MB):
+            cs.wait_event(ev_disp[m])
+            ng = self.nslots[m]
+            if ng:
+                g = self.groups[m][:ng]
+                rows = self.real_rows(m)
+                with self._timed(4.0 * rows * h * hp):
+                    K.grouped_gemm(K.GEMM_FWD_SWIGLU, self.Xr[m], self.W1, g, N=2 * hp, K=h, C=self.H[m],
+                                   C2=self.Act[m], B1=self.W1r[m])
+                with self._timed(2.0 * rows * h * hp):
+                    K.grouped_gemm(K.GEMM_FWD_STORE, self.Act[m], self.W2, g, N=h, K=hp, C=self.Y[m],
+                                   B1=self.W2r[m])
+                self.launches += 2
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            ev_fwd.append(ev)
+        # ---- combine + raw-dout dispatch (comm stream)
+        ev_dout = []
+        for m in range(MB):
+            xs.wait_event(ev_fwd[m])
+            A.barrier(xs)  # Y of micro-batch m complete on every rank
+            self._k("mb_combine_rows", self.ptr_y[m].data_ptr(), self.perm[m].data_ptr(), gates[m].data_ptr(),
+                    T, k, h, out[m].data_ptr(), None, None, 1, st_x)
             if hooks:
-                hooks.after_forward(m)
-            self._backward_mb(m, dout[m], dx[m], dgate[m], st)
+                hooks.after_forward(m, xs)
+            self._k("mb_scatter_rows", dout[m].data_ptr(), T, k, h, self.perm[m].data_ptr(),
+                    self.ptr_dyr[m].data_ptr(), st_x)
+            A.barrier(xs)  # dout rows of micro-batch m have landed everywhere
+            ev = torch.cuda.Event()
+            ev.record(xs)
+            ev_dout.append(ev)
+        # ---- backward GEMMs (compute stream)
+        ev_bwd = []
+        for m in range(MB):
+            cs.wait_event(ev_dout[m])
+            ng = self.nslots[m]
+            if ng:
+                g = self.groups[m][:ng]
+                rows = self.real_rows(m)
+                # dAct = dout.W2 with the combine backward fused in the epilogue: gate applied per row,
+                # dgate partials <dout.W2, act> = <dout, Y>, gate*act written over Act for dW2
+                with self._timed(2.0 * rows * h * hp):
+                    K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU_GATED, self.dYr[m], self.W2, g, N=hp, K=h, C=self.dH[m],
+                                   C2=self.Act[m], aux=self.H[m], B1=self.W2r[m], row_scale=self.gate_r[m],
+                                   row_partial=self.dgate_r[m])
+                with self._timed(4.0 * rows * h * hp):
+                    K.grouped_gemm(K.GEMM_DGRAD_STORE, self.dH[m], self.W1, g, N=h, K=2 * hp, C=self.dXp[m],
+                                   B1=self.W1r[m])
+                self.launches += 2
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            ev_bwd.append(ev)
+        # ---- dX un-permute + dgate gather (comm stream), overlapping the weight gradients
+        for m in range(MB):
+            xs.wait_event(ev_bwd[m])
+            A.barrier(xs)  # dX rows / dgate partials of micro-batch m complete everywhere
+            self._k("mb_combine_rows", self.ptr_dxp[m].data_ptr(), self.perm[m].data_ptr(), None, T, k, h,
+                    dx[m].data_ptr(), self.ptr_dgate[m].data_ptr(), dgate[m].data_ptr(), self.npart, st_x)
             if hooks:
-                hooks.after_backward(m)
-        self._wgrad(st)
+                hooks.after_backward(m, xs)
+        # ---- weight gradients (compute stream), K over every micro-batch of the step
+        self._wgrad()
+        ev = torch.cuda.Event()
+        ev.record(cs)
+        xs.wait_event(ev)
+        if self.world > 1:
+            A.barrier(xs)  # every rank's replica gradients are complete
+            mn1, mn2 = 2 * hp * h, h * hp
+            for loc, p1, p2, n in self.reduce:
+                self._k("mb_accumulate_f32", self.gW1[loc].data_ptr(), p1.data_ptr(), n, mn1, st_x)
+                self._k("mb_accumulate_f32", self.gW2[loc].data_ptr(), p2.data_ptr(), n, mn2, st_x)
+            A.barrier(xs)  # peers finished reading our replica gradients (next step may overwrite)
+        cs.wait_stream(xs)
+
+    def _wgrad(self):
+        h, hp = self.shape.hidden, self.shape.ffn
+        R, MB = self.R, self.MB
+        if not self.wgroups.shape[0]:
+            return
+        rows = sum(self.real_rows(m) for m in range(MB))
+        with self._timed(2.0 * rows * h * hp):
+            K.grouped_gemm(K.GEMM_WGRAD, self.dYr.view(MB * R, h), self.Act.view(MB * R, hp), self.wgroups, M=h, N=hp,
+                           C=self.gW2, c_slot_stride=h * hp, segs=self.wsegs)
+        with self._timed(4.0 * rows * h * hp):
+            K.grouped_gemm(K.GEMM_WGRAD, self.dH.view(MB * R, 2 * hp), self.Xr.view(MB * R, h), self.wgroups,
+                           M=2 * hp, N=h, C=self.gW1, c_slot_stride=2 * hp * h, segs=self.wsegs)
+        self.launches += 2
+
+    step = forward_backward
 
     def step_host(self, host: dict, dev: dict) -> None:
-        """The user-facing step with HOST (pinned) tensors: per micro-batch, x/idx/gates/dout are
-        copied host->device on one copy stream while earlier micro-batches compute, and
-        out/dx/dgate are copied device->host on another as soon as they exist.  `dev` holds the
-        device staging tensors of the same shapes.  Synchronous: returns with results on host."""
+        """The user-facing step with HOST (pinned) tensors: micro-batch inputs are copied
+        host->device on a copy stream while earlier micro-batches run, and out/dx/dgate are copied
+        device->host as soon as they exist.  `dev` holds device staging tensors of the same
+        shapes.  Synchronous: returns with the results on the host."""
         cur = torch.cuda.current_stream()
         if not hasattr(self, "_h2d"):
             self._h2d = torch.cuda.Stream(device=self.device)
@@ -418,128 +527,28 @@ class MoEDataPlane:
                 ev = torch.cuda.Event()
                 ev.record(h2d)
                 ready.append(ev)
-        dp = self
 
         class _Hooks:
-            def before(self, m):
-                cur.wait_event(ready[m])
+            def inputs_ready(self, m, stream):
+                stream.wait_event(ready[m])
 
-            def after_forward(self, m):
-                ev = torch.cuda.Event()
-                ev.record(cur)
-                d2h.wait_event(ev)
+            def after_forward(self, m, stream):
+                d2h.wait_stream(stream)
                 with torch.cuda.stream(d2h):
                     host["out"][m].copy_(dev["out"][m], non_blocking=True)
 
-            def after_backward(self, m):
-                ev = torch.cuda.Event()
-                ev.record(cur)
-                d2h.wait_event(ev)
+            def after_backward(self, m, stream):
+                d2h.wait_stream(stream)
                 with torch.cuda.stream(d2h):
                     host["dx"][m].copy_(dev["dx"][m], non_blocking=True)
                     host["dgate"][m].copy_(dev["dgate"][m], non_blocking=True)
 
+        # the compute stream reads the dispatched rows only, so only the comm stream waits on inputs
         self.forward_backward(dev["x"], dev["idx"], dev["gates"], dev["dout"], dev["out"], dev["dx"], dev["dgate"],
                               hooks=_Hooks())
         cur.wait_stream(d2h)
         cur.synchronize()
 
-    def _replica_push(self, m: int) -> None:
-        if not self.pushes[m]:
-            return
-        h, hp = self.shape.hidden, self.shape.ffn
-        cur = torch.cuda.current_stream()
-        self.side.wait_stream(cur)
-        lib = self._lib()
-        n1, n2 = 2 * hp * h * 2, h * hp * 2
-        for dst, slot, loc in self.pushes[m]:
-            d1 = self.arena.peer_ptr(dst, self.off["w1r"]) + slot * n1
-            d2 = self.arena.peer_ptr(dst, self.off["w2r"]) + slot * n2
-            nat.check(lib.mb_memcpy_async(d1, self.W1[loc].data_ptr(), n1, self.side.cuda_stream), lib, "push w1")
-            nat.check(lib.mb_memcpy_async(d2, self.W2[loc].data_ptr(), n2, self.side.cuda_stream), lib, "push w2")
-        cur.wait_stream(self.side)
-
-    def _forward_mb(self, m, x, idx, gates, out, st):
-        E, k, h, hp = self.shape.num_experts, self.shape.top_k, self.shape.hidden, self.shape.ffn
-        T, R = self.T, self.R
-        chunks = (T + CHUNK - 1) // CHUNK
-        A = self.arena
-        # K5: owners push this micro-batch's replica weights (copy engine, overlaps K1/K2)
-        self._replica_push(m)
-        # K1 + chunk scan + K2
-        self._k("mb_expert_histogram", idx.data_ptr(), 1, T, k, E, self.counts[m].data_ptr(),
-                self.chunk_counts[m].data_ptr(), CHUNK, st)
-        self._k("mb_chunk_scan", self.chunk_counts[m].data_ptr(), self.chunk_base[m].data_ptr(), 1, chunks, E, st)
-        self._k("mb_zero_pad_rows", self.Xr[m].data_ptr(), self.slot_tab[m].data_ptr(), self.nslots[m], h, st)
-        A.barrier()  # every receiver has cleared its pad rows and finished the previous readers
-        self._k("mb_permute_rank", idx.data_ptr(), T, k, gates.data_ptr(), E, self.chunk_base[m].data_ptr(), CHUNK,
-                self.route_tab[m].data_ptr(), self.ncopies[m].data_ptr(), self.plan.maxc,
-                self.ptr_gate[m].data_ptr(), self.perm[m].data_ptr(), st)
-        # K3: dispatch (peer stores)
-        self._k("mb_scatter_rows", x.data_ptr(), T, k, h, self.perm[m].data_ptr(), self.ptr_xr[m].data_ptr(), st)
-        A.barrier()  # all rows (and replica weights) have landed
-        ng = self.nslots[m]
-        if ng:
-            g = self.groups[m]
-            rows = self.real_rows(m)
-            with self._timed(4.0 * rows * h * hp):
-                K.grouped_gemm(K.GEMM_FWD_SWIGLU, self.Xr[m], self.W1, g[:ng], N=2 * hp, K=h, C=self.H[m],
-                               C2=self.Act[m], B1=self.W1r)
-            with self._timed(2.0 * rows * h * hp):
-                K.grouped_gemm(K.GEMM_FWD_STORE, self.Act[m], self.W2, g[:ng], N=h, K=hp, C=self.Y[m], B1=self.W2r)
-            self.launches += 2
-        A.barrier()  # every expert output is ready
-        # K6: combine over peer loads
-        self._k("mb_combine_rows", self.ptr_y[m].data_ptr(), self.perm[m].data_ptr(), gates.data_ptr(),
-                T, k, h, out.data_ptr(), None, None, 1, st)
-
-    def _backward_mb(self, m, dout, dx, dgate, st):
-        E, k, h, hp = self.shape.num_experts, self.shape.top_k, self.shape.hidden, self.shape.ffn
-        T, R = self.T, self.R
-        A = self.arena
-        # dout rows (unscaled) to the serving GPUs, same permutation as the forward dispatch
-        self._k("mb_scatter_rows", dout.data_ptr(), T, k, h, self.perm[m].data_ptr(), self.ptr_dyr[m].data_ptr(), st)
-        A.barrier()
-        ng = self.nslots[m]
-        if ng:
-            g = self.groups[m]
-            rows = self.real_rows(m)
-            # dAct = dout.W2 with the combine backward fused in the epilogue: gate applied per row,
-            # dgate partials <dout.W2, act> = <dout, Y>, gate*act written over Act for dW2
-            with self._timed(2.0 * rows * h * hp):
-                K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU_GATED, self.dYr[m], self.W2, g[:ng], N=hp, K=h, C=self.dH[m],
-                               C2=self.Act[m], aux=self.H[m], B1=self.W2r, row_scale=self.gate_r[m],
-                               row_partial=self.dgate_r[m])
-            with self._timed(4.0 * rows * h * hp):
-                K.grouped_gemm(K.GEMM_DGRAD_STORE, self.dH[m], self.W1, g[:ng], N=h, K=2 * hp, C=self.dXp[m],
-                               B1=self.W1r)
-            self.launches += 2
-        A.barrier()
-        self._k("mb_combine_rows", self.ptr_dxp[m].data_ptr(), self.perm[m].data_ptr(), None, T, k, h, dx.data_ptr(),
-                self.ptr_dgate[m].data_ptr(), dgate.data_ptr(), self.npart, st)
-
-    def _wgrad(self, st):
-        h, hp = self.shape.hidden, self.shape.ffn
-        R, MB = self.R, self.MB
-        ng = self.wgroups.shape[0]
-        if ng:
-            rows = sum(self.real_rows(m) for m in range(MB))
-            dyr = self.dYr.view(MB * R, h)
-            with self._timed(2.0 * rows * h * hp):
-                K.grouped_gemm(K.GEMM_WGRAD, dyr, self.Act.view(MB * R, hp), self.wgroups, M=h, N=hp, C=self.gW2,
-                               c_slot_stride=h * hp, segs=self.wsegs)
-            with self._timed(4.0 * rows * h * hp):
-                K.grouped_gemm(K.GEMM_WGRAD, self.dH.view(MB * R, 2 * hp), self.Xr.view(MB * R, h), self.wgroups,
-                               M=2 * hp, N=h, C=self.gW1, c_slot_stride=2 * hp * h, segs=self.wsegs)
-            self.launches += 2
-        if self.world > 1:
-            self.arena.barrier()  # replica gradients complete on every rank
-            mn1, mn2 = 2 * hp * h, h * hp
-            for loc, p1, p2, n in self.reduce:
-                self._k("mb_accumulate_f32", self.gW1[loc].data_ptr(), p1.data_ptr(), n, mn1, st)
-                self._k("mb_accumulate_f32", self.gW2[loc].data_ptr(), p2.data_ptr(), n, mn2, st)
-
-    step = forward_backward
-
     def close(self) -> None:
+        torch.cuda.synchronize(self.device)
         self.arena.close()
