@@ -146,13 +146,16 @@ def run_reference(args, rank, world):
 
 def measure_policy(args, comm, policy, shape, cfg, routing, topo, model, cfgs, want_detail):
     import torch
-    from paper_2605_08639_b200.moe_layer import MoEDataPlane, build_step_plan
+    from paper_2605_08639_b200.moe_layer import MoEDataPlane, build_step_plan, plan_digest
     from paper_2605_08639_b200.workload import make_activations, make_weights_for
     rank, world = comm.rank, comm.world
     T, MB = args.tokens, args.micro_batches
     t0 = time.perf_counter()
     plan = build_step_plan(policy, routing.mats, topo, model, topo.profile, cfgs, shape)
     plan_ms = (time.perf_counter() - t0) * 1e3
+    digests = comm.all_gather_object(plan_digest(plan))
+    if len(set(digests)) != 1:
+        raise RuntimeError(f"ranks disagree on the step plan: {digests}")
     dp = MoEDataPlane(comm, shape, T, MB, plan)
     experts = np.flatnonzero(plan.home == rank)
     wg, wu, wd = make_weights_for(shape, experts)
@@ -235,6 +238,8 @@ def run_ours(args, comm):
     import torch
     from paper_2605_08639_b200 import AnnealConfig, ModelProfile, ReplicaConfig, SimConfigs
     from paper_2605_08639_b200.cluster import b200_box_topology, b200_profile
+    from paper_2605_08639_b200.kernels import expert_histogram
+    from paper_2605_08639_b200.moe_layer import gather_routing
     from paper_2605_08639_b200.workload import SHAPES, make_routing
     rank, world = comm.rank, comm.world
     cfg = SHAPES[args.config]
@@ -246,8 +251,18 @@ def run_ours(args, comm):
     cfgs = SimConfigs(anneal=AnnealConfig(seeds=tuple(range(args.sa_chains))), replica=ReplicaConfig(slots),
                       threads=min(8, os.cpu_count() or 1))
     T, MB = args.tokens, args.micro_batches
-    skewed = make_routing(shape, T, MB, world, rank, zipf_s=args.zipf, shift=cfg["shift"])
-    balanced = make_routing(shape, T, MB, world, rank, zipf_s=args.zipf, shift=cfg["shift"], balanced=True)
+
+    def routing_for(balanced):
+        # each rank draws its own replayed routing, histograms it on the GPU (K1) and all-gathers
+        # the counts into the (MB, G, E) trace every planner sees
+        r = make_routing(shape, T, MB, world, rank, zipf_s=args.zipf, shift=cfg["shift"], balanced=balanced,
+                         all_ranks=False)
+        counts, _ = expert_histogram(torch.from_numpy(r.idx).cuda(), shape.num_experts)
+        r.mats = gather_routing(comm, counts.cpu().numpy().astype(np.int64))
+        return r
+
+    skewed = routing_for(False)
+    balanced = routing_for(True)
     policies = [p for p in args.policies.split(",") if p]
     results = {}
     for pol in policies:

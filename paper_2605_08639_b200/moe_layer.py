@@ -149,6 +149,24 @@ def build_step_plan(policy: str, mats: np.ndarray, topo: ClusterTopology, model:
     return plan
 
 
+def gather_routing(comm: Comm, local_counts: np.ndarray) -> np.ndarray:
+    """(MB, E) expert counts of this rank (the K1 histogram rows) -> (MB, G, E) of every rank,
+    i.e. RoutingTrace.matrices[:, layer] (routing.py:151-168) assembled across processes."""
+    rows = comm.all_gather_object(np.ascontiguousarray(local_counts, dtype=np.int64))
+    return np.stack(rows, axis=1)
+
+
+def plan_digest(plan: StepPlan) -> str:
+    """sha256 of every table of a step plan: ranks must agree bit for bit before the step."""
+    import hashlib
+    h = hashlib.sha256(np.ascontiguousarray(plan.home).tobytes())
+    for m in plan.mbs:
+        for a in (m.route_tab, m.ncopies, m.slot_tab, m.slot_w, m.nslots, m.total_rows, m.flow):
+            h.update(np.ascontiguousarray(a).tobytes())
+        h.update(repr(list(m.placement.replicas.items())).encode())
+    return h.hexdigest()[:16]
+
+
 # ----------------------------------------------------------------------------- weights
 
 

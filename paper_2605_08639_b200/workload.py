@@ -34,15 +34,17 @@ class Routing:
 
 
 def make_routing(shape: LayerShape, tokens: int, micro_batches: int, world: int, rank: int, zipf_s: float = 1.0,
-                 shift: int = 7, seed: int = 20261018, balanced: bool = False) -> Routing:
-    """Replayed routing of every rank (counts) and this rank's token-level indices/gates."""
+                 shift: int = 7, seed: int = 20261018, balanced: bool = False, all_ranks: bool = True) -> Routing:
+    """This rank's token-level indices/gates and (all_ranks) every rank's counts via np.bincount.
+    With all_ranks=False only this rank's row of `mats` is filled (the caller histograms on the
+    device and all-gathers, see moe_layer.gather_routing)."""
     gen = ZipfRouting(shape.num_experts, shape.top_k, tokens, zipf_s=zipf_s, shift=shift, seed=seed,
                       balanced=balanced)
     mats = np.zeros((micro_batches, world, shape.num_experts), dtype=np.int64)
     idx = np.zeros((micro_batches, tokens, shape.top_k), dtype=np.int32)
     gates = np.zeros((micro_batches, tokens, shape.top_k), dtype=np.float32)
     for m in range(micro_batches):
-        for j in range(world):
+        for j in range(world) if all_ranks else (rank,):
             i_j, g_j = gen.sample(m, 0, j)
             mats[m, j] = np.bincount(i_j.ravel(), minlength=shape.num_experts)
             if j == rank:
