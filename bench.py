@@ -204,8 +204,14 @@ def measure_policy(args, comm, policy, shape, cfg, routing, topo, model, cfgs, w
     res = {"ms": ms_max, "plan_ms": plan_ms, "skew": plan.skew(), "launches": launches,
            "rows": [dp.real_rows(m) for m in range(MB)], "rows_cap": plan.rows_cap}
     if want_detail:
-        gemm_ms = sum(a.elapsed_time(b) for a, b, _ in dp.gemm_events) / args.steps
-        gemm_flop = sum(f for _, _, f in dp.gemm_events) / args.steps
+        gemm_ms = sum(a.elapsed_time(b) for a, b, _, _ in dp.gemm_events) / args.steps
+        gemm_flop = sum(f for _, _, f, _ in dp.gemm_events) / args.steps
+        kinds = {}
+        for a, b, f, kd in dp.gemm_events:
+            ms_f = kinds.setdefault(kd, [0.0, 0.0])
+            ms_f[0] += a.elapsed_time(b) / args.steps
+            ms_f[1] += f / args.steps
+        res["gemm_kinds"] = {kd: {"ms": round(v[0], 4), "tflops": round(v[1] / v[0] / 1e9, 1)} for kd, v in kinds.items()}
         res.update(gemm_ms=gemm_ms, gemm_flop=gemm_flop, gemm_launches=len(dp.gemm_events) // args.steps,
                    clocks=clocks)
         # e2e through the host-buffer API (pinned host tensors, copies inside the timed region)
@@ -290,7 +296,8 @@ def run_ours(args, comm):
                      "frac": round(gemm_tflops / peak_tf, 4), "traffic": None,
                      "peak_source": f"bf16_tflops_sustained, {peak_src}",
                      "flops_per_step": head["gemm_flop"], "gemm_ms_per_step": round(head["gemm_ms"], 4),
-                     "gemm_share_of_step": round(head["gemm_ms"] / head["ms"], 4)},
+                     "gemm_share_of_step": round(head["gemm_ms"] / head["ms"], 4),
+                     "per_kind": head["gemm_kinds"]},
         "e2e": {"value": tokens_step / (head["e2e_ms"] / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": head["h2d"],
                 "d2h_bytes_per_step": head["d2h"], "ms_per_step": head["e2e_ms"]},
         "gpu_launches": head["launches"],

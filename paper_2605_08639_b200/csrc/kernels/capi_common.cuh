@@ -53,9 +53,9 @@ inline PFN_encodeTiled get_encode_tiled() {
   return fn;
 }
 
-// 2-D bf16 tensor map, SWIZZLE_128B: dims {inner, outer}, row pitch in bytes, box {box_inner, box_outer}.
-inline int make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
-                             uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_outer) {
+// 2-D tensor map, SWIZZLE_128B: dims {inner, outer}, row pitch in bytes, box {box_inner, box_outer}.
+inline int make_tmap_2d(CUtensorMap* map, CUtensorMapDataType dtype, const void* base, uint64_t inner,
+                        uint64_t outer, uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_outer) {
   PFN_encodeTiled enc = get_encode_tiled();
   if (!enc) return set_error(MB_ECUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
   if (outer == 0) outer = 1;
@@ -63,7 +63,7 @@ inline int make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner,
   cuuint64_t strides[1] = {row_pitch_bytes};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estride[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estride,
+  CUresult r = enc(map, dtype, 2, const_cast<void*>(base), dims, strides, box, estride,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
@@ -71,6 +71,12 @@ inline int make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner,
                      (unsigned long long)inner, (unsigned long long)outer, (unsigned long long)row_pitch_bytes,
                      box_inner, box_outer);
   return MB_OK;
+}
+
+inline int make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                             uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_outer) {
+  return make_tmap_2d(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, base, inner, outer, row_pitch_bytes, box_inner,
+                      box_outer);
 }
 
 inline int device_sm_count() {

@@ -68,9 +68,24 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
   p.C = C; p.ldc = ldc; p.c_slot_stride = c_slot_stride;
   p.C2 = C2; p.ldc2 = ldc2; p.aux = aux; p.ld_aux = ld_aux;
   p.rscale = row_scale; p.rpart = row_partial;
+  if (const char* dbg = std::getenv("MB_GEMM_DEBUG")) p.debug = std::atoi(dbg);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const bool pair = !force_single && N % 256 == 0 && (mode != MB_GEMM_WGRAD || M % 256 == 0);
   int rc;
+  if (pair || mode == MB_GEMM_DGRAD_DSWIGLU_GATED) {
+    // epilogue TMA store maps: 32-row x 128-byte boxes (64 bf16 / 32 fp32 columns)
+    if (mode == MB_GEMM_WGRAD) {
+      MB_CHECK_ARG(c_slot_stride == static_cast<int64_t>(M) * ldc, "wgrad output must be [slots][M][ldc]");
+      if ((rc = make_tmap_2d(&p.tmC, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, C, ldc, static_cast<uint64_t>(M) * kMaxGroups,
+                             ldc * 4, 32, 32)))
+        return rc;
+    } else {
+      MB_CHECK_ARG(ldc % 64 == 0 && (!C2 || ldc2 % 64 == 0), "output widths must be multiples of 64");
+      if ((rc = make_tmap_bf16_2d(&p.tmC, C, ldc, a_rows, ldc * 2, 64, 32))) return rc;
+      if (C2 && (rc = make_tmap_bf16_2d(&p.tmC2, C2, ldc2, a_rows, ldc2 * 2, 64, 32))) return rc;
+      if (aux && (rc = make_tmap_bf16_2d(&p.tmAux, aux, ld_aux, a_rows, ld_aux * 2, 64, 32))) return rc;
+    }
+  }
   switch (mode) {
     case MB_GEMM_FWD_STORE:
     case MB_GEMM_FWD_SWIGLU: {

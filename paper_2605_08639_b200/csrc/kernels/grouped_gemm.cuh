@@ -54,6 +54,9 @@ struct GemmParams {
   CUtensorMap tmA;
   CUtensorMap tmB0;
   CUtensorMap tmB1;
+  CUtensorMap tmC;   // epilogue TMA store maps (CTA-pair kernel): output C (box 32 rows x 128 B)
+  CUtensorMap tmC2;  // secondary output C2
+  CUtensorMap tmAux; // epilogue TMA load map of the auxiliary input (H for the dSwiGLU epilogues)
   const GemmGroup* groups;
   const GemmSeg* segs;
   int num_groups;
@@ -67,6 +70,7 @@ struct GemmParams {
   int64_t ld_aux;
   const float* rscale;  // per-row scale (gate) for EPI_DSWIGLU_GATED
   float* rpart;         // per-row partial sums [rows][N/128] for EPI_DSWIGLU_GATED
+  int debug;            // bit0: skip the epilogue (TMEM drained, nothing stored) -- profiling only
 };
 
 template <int BN>

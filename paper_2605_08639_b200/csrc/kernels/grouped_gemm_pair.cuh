@@ -4,10 +4,18 @@
 // and its 128-wide half of B per k-block (32 KB instead of 48 KB), so the shared-memory port
 // of each SM carries half the B operand traffic of the 1-CTA kernel; the leader CTA issues
 // tcgen05.mma.cta_group::2 (M=256, N=256, K=16) reading both CTAs' smem and writing both
-// CTAs' TMEM (128 lanes each), and commits multicast to both CTAs' mbarriers.  Both CTAs run
-// the epilogue on their own TMEM half.  Roles per CTA as in the 1-CTA kernel:
-//   warp 0 TMA producer (both CTAs; bytes complete on the leader's full barrier)
-//   warp 1 MMA issuer (leader only) + TMEM allocator (both, cta_group::2)
+// CTAs' TMEM (128 lanes each), and commits multicast to both CTAs' mbarriers.
+//
+// Epilogue: every output leaves through TMA.  An epilogue warp drains 32 TMEM lanes x 32 or
+// 64 columns, applies the fused math, writes one 32-row x 128-byte box into a 128B-swizzled
+// staging buffer (double-buffered per warp) and one lane issues cp.async.bulk.tensor (store,
+// or reduce-add for the fp32 gradient accumulation, so the L2 does the read-modify-write).
+// Row-per-thread global stores were the measured bottleneck of every variant (the mainloop
+// alone runs at 1.4-1.9 PFLOP/s).
+//
+// Roles per CTA:
+//   warp 0     TMA producer (both CTAs; bytes complete on the leader's full barrier)
+//   warp 1     MMA issuer (leader only) + TMEM allocator (both, cta_group::2)
 //   warps 2..9 epilogue (both; two warps per TMEM lane quarter split the columns; release the
 //              accumulator on the leader's tmem_empty barrier)
 #pragma once
@@ -16,12 +24,15 @@
 namespace mb {
 
 struct PairCfg {
-  static constexpr int kStages = 6;
+  static constexpr int kStages = 4;
   static constexpr int kABytes = 128 * BK * 2;  // this CTA's 128 rows of A
   static constexpr int kBBytes = 128 * BK * 2;  // this CTA's 128 columns of B
   static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kEpiWarps = 8;
+  static constexpr int kBoxBytes = 32 * 128;  // one 32-row x 128-byte TMA box
+  static constexpr int kStagingBytes = kEpiWarps * 2 * kBoxBytes;
   static constexpr int kMetaBytes = 10240;
-  static constexpr int kSmemBytes = kStages * kStageBytes + kMetaBytes + 1024;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kStagingBytes + kMetaBytes + 1024;
   static constexpr int TM = 256, TN = 256;
 };
 
@@ -43,6 +54,43 @@ __device__ __forceinline__ TileCoord decode_tile_pair(int t, const int* tile_sta
   return c;
 }
 
+// Per-warp double-buffered TMA store staging: 2 boxes of 32 rows x 128 B, 128B swizzle.
+struct BoxStager {
+  uint8_t* base;
+  int buf = 0;
+  int lane;
+  int debug = 0;
+  // write this lane's 128-byte row of the next box (32 words) and issue the store
+  template <bool kReduce>
+  __device__ __forceinline__ void put(const uint32_t (&w)[32], const CUtensorMap* map, int32_t c0, int32_t c1) {
+    uint8_t* b = base + buf * PairCfg::kBoxBytes;
+    if (lane == 0) bulk_wait_read<1>();  // the store that last used this buffer has read it
+    __syncwarp();
+    uint4* row = reinterpret_cast<uint4*>(b + lane * 128);
+    if (!(debug & 4)) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) row[j ^ (lane & 7)] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (debug & 2) return;
+    if (lane == 0) {
+      const uint64_t pol = (debug & 8) ? l2_evict_last_policy() : l2_evict_first_policy();
+      if (kReduce) tma_reduce_add_2d(map, b, c0, c1, pol);
+      else tma_store_2d(map, b, c0, c1, pol);
+      bulk_commit();
+    }
+    buf ^= 1;
+  }
+};
+
+__device__ __forceinline__ void pack_bf16_words(const uint32_t (&a)[32], const uint32_t (&b)[32], uint32_t (&w)[32]) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) w[i] = pack_bf16x2(__uint_as_float(a[2 * i]), __uint_as_float(a[2 * i + 1]));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) w[16 + i] = pack_bf16x2(__uint_as_float(b[2 * i]), __uint_as_float(b[2 * i + 1]));
+}
+
 template <bool kW, bool kAmn, bool kBmn, int kEpi>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     grouped_gemm_pair_kernel(const __grid_constant__ GemmParams p) {
@@ -53,12 +101,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kABytes;
-  uint8_t* meta = smem + S * Cfg::kStageBytes;
+  uint8_t* sStage = smem + S * Cfg::kStageBytes;
+  uint8_t* meta = sStage + Cfg::kStagingBytes;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(meta);
   uint64_t* empty_bar = full_bar + S;
   uint64_t* tfull_bar = empty_bar + S;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* hbar_base = reinterpret_cast<uint64_t*>(meta + 128);  // one per epilogue warp (H tile loads)
   int* tile_start = reinterpret_cast<int*>(meta + 256);
   GemmGroup* sg = reinterpret_cast<GemmGroup*>(meta + 256 + 4 * (kMaxGroups + 8));
 
@@ -75,6 +125,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     tma_prefetch_desc(&p.tmA);
     tma_prefetch_desc(&p.tmB0);
     tma_prefetch_desc(&p.tmB1);
+    tma_prefetch_desc(&p.tmC);
     for (int i = 0; i < S; ++i) {
       mbar_init(&full_bar[i], 1);
       mbar_init(&empty_bar[i], 1);
@@ -83,6 +134,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       mbar_init(&tfull_bar[i], 1);
       mbar_init(&tempty_bar[i], 16);  // 8 epilogue warps x 2 CTAs
     }
+    for (int i = 0; i < Cfg::kEpiWarps; ++i) mbar_init(&hbar_base[i], 1);
     fence_barrier_init();
     fence_proxy_async_smem();
   }
@@ -205,6 +257,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty_bar[1]), 0);
+    BoxStager st{sStage + (warp - 2) * 2 * Cfg::kBoxBytes, 0, lane, p.debug};
+    uint64_t* hbar = hbar_base + (warp - 2);
+    uint32_t hphase = 0;
     int it = 0;
     for (int t = cluster; t < total_tiles; t += nclusters, ++it) {
       const TileCoord tc = decode_tile_pair<kW>(t, tile_start, sg, ng, p);
@@ -213,219 +268,181 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t t_acc = tmem_base + lane_off + acc * 256;
-      const int tile_row = tc.mb * TM + static_cast<int>(rank) * 128 + row_in_cta;  // row inside the group / M
-      const bool valid = kW || tile_row < gg.rows;
+      const int warp_row0 = tc.mb * TM + static_cast<int>(rank) * 128 + q * 32;  // first row of this warp's box
+      const int tile_row = warp_row0 + lane;
+      const bool valid = kW || warp_row0 < gg.rows;   // groups are 128-row padded: uniform per warp
+      const int32_t out_row0 = kW ? gg.slot * p.M + warp_row0 : gg.a0 + warp_row0;
+      bool released = false;
+      // hand the accumulator back to the MMA warp as soon as this warp holds its columns
+      auto release = [&]() {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) mbar_arrive(&tempty_bar[acc]);
+          else mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+        }
+        released = true;
+      };
 
-      if constexpr (kEpi == EPI_STORE_BF16) {
-        const int64_t row = gg.a0 + tile_row;
-        __nv_bfloat16* crow = reinterpret_cast<__nv_bfloat16*>(p.C) + row * p.ldc + tc.nb * TN + ch2 * 128;
-#pragma unroll 1
-        for (int ch = 0; ch < 4; ++ch) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(t_acc + ch2 * 128 + ch * 32, r);
+      if (p.debug & 1) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_acc + ch2 * 128, r);
+        tmem_ld_wait();
+        if (r[0] == 0x7fffffffu && r[31] == 0x7fffffffu) p.rpart[0] = 0.0f;  // keep the load alive
+      } else if (valid) {
+        if constexpr (kEpi == EPI_STORE_BF16) {
+          uint32_t a0[32], a1[32], b0[32], b1[32], w[32];
+          tmem_ld_32x32b_x32(t_acc + ch2 * 128, a0);
+          tmem_ld_32x32b_x32(t_acc + ch2 * 128 + 32, a1);
+          tmem_ld_32x32b_x32(t_acc + ch2 * 128 + 64, b0);
+          tmem_ld_32x32b_x32(t_acc + ch2 * 128 + 96, b1);
           tmem_ld_wait();
-          if (valid) {
-            uint4* dst = reinterpret_cast<uint4*>(crow + ch * 32);
+          release();
+          pack_bf16_words(a0, a1, w);
+          st.put<false>(w, &p.tmC, tc.nb * TN + ch2 * 128, out_row0);
+          pack_bf16_words(b0, b1, w);
+          st.put<false>(w, &p.tmC, tc.nb * TN + ch2 * 128 + 64, out_row0);
+        } else if constexpr (kEpi == EPI_SWIGLU) {
+          // gate columns [0,128), up columns [128,256); this warp owns gate/up columns [ch2*64, +64)
+          uint32_t g0[32], g1[32], u0[32], u1[32], w[32];
+          tmem_ld_32x32b_x32(t_acc + ch2 * 64, g0);
+          tmem_ld_32x32b_x32(t_acc + ch2 * 64 + 32, g1);
+          tmem_ld_32x32b_x32(t_acc + 128 + ch2 * 64, u0);
+          tmem_ld_32x32b_x32(t_acc + 128 + ch2 * 64 + 32, u1);
+          tmem_ld_wait();
+          release();
+          pack_bf16_words(g0, g1, w);
+          st.put<false>(w, &p.tmC, tc.nb * TN + ch2 * 64, out_row0);
+          pack_bf16_words(u0, u1, w);
+          st.put<false>(w, &p.tmC, tc.nb * TN + 128 + ch2 * 64, out_row0);
 #pragma unroll
-            for (int v = 0; v < 4; ++v)
-              dst[v] = make_uint4(pack_bf16x2(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1])),
-                                  pack_bf16x2(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3])),
-                                  pack_bf16x2(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5])),
-                                  pack_bf16x2(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7])));
+          for (int i = 0; i < 16; ++i) {
+            const float a0 = __uint_as_float(g0[2 * i]), a1 = __uint_as_float(g0[2 * i + 1]);
+            const float b0 = __uint_as_float(u0[2 * i]), b1 = __uint_as_float(u0[2 * i + 1]);
+            w[i] = pack_bf16x2(__fdividef(a0, 1.0f + __expf(-a0)) * b0, __fdividef(a1, 1.0f + __expf(-a1)) * b1);
           }
-        }
-      } else if constexpr (kEpi == EPI_SWIGLU) {
-        // gate columns [0,128), up columns [128,256); this warp owns gate/up columns [ch2*64, ch2*64+64)
-        const int64_t row = gg.a0 + tile_row;
-        __nv_bfloat16* hrow = reinterpret_cast<__nv_bfloat16*>(p.C) + row * p.ldc + tc.nb * TN;
-        __nv_bfloat16* arow = reinterpret_cast<__nv_bfloat16*>(p.C2) + row * p.ldc2 + tc.nb * (TN / 2);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float a0 = __uint_as_float(g1[2 * i]), a1 = __uint_as_float(g1[2 * i + 1]);
+            const float b0 = __uint_as_float(u1[2 * i]), b1 = __uint_as_float(u1[2 * i + 1]);
+            w[16 + i] = pack_bf16x2(__fdividef(a0, 1.0f + __expf(-a0)) * b0, __fdividef(a1, 1.0f + __expf(-a1)) * b1);
+          }
+          st.put<false>(w, &p.tmC2, tc.nb * (TN / 2) + ch2 * 64, out_row0);
+        } else if constexpr (kEpi == EPI_DSWIGLU || kEpi == EPI_DSWIGLU_GATED) {
+          // dAct columns [ch2*128, +128) = interleave block blk: gate|up 256 columns of H / dH
+          // H (gate|up) comes in through TMA into the warp's two staging buffers, is read back row
+          // per lane, and the same buffers then carry dH (and gate*act) out through TMA stores.
+          constexpr bool kGated = kEpi == EPI_DSWIGLU_GATED;
+          const int64_t row = gg.a0 + tile_row;
+          const bool real = !kGated || tile_row < gg.rows_real;
+          const int blk = tc.nb * 2 + ch2;
+          const float gate = kGated ? (real ? p.rscale[row] : 0.0f) : 1.0f;
+          float part = 0.0f;
+          uint8_t* bufA = st.base;
+          uint8_t* bufB = st.base + Cfg::kBoxBytes;
+          uint4* rowA = reinterpret_cast<uint4*>(bufA + lane * 128);
+          uint4* rowB = reinterpret_cast<uint4*>(bufB + lane * 128);
+          const int sw = lane & 7;
 #pragma unroll 1
-        for (int cc = 0; cc < 2; ++cc) {
-          const int ch = ch2 * 2 + cc;
-          uint32_t g[32], u[32];
-          tmem_ld_32x32b_x32(t_acc + ch * 32, g);
-          tmem_ld_32x32b_x32(t_acc + TN / 2 + ch * 32, u);
-          tmem_ld_wait();
-          if (!valid) continue;
-          uint4* dg = reinterpret_cast<uint4*>(hrow + ch * 32);
-          uint4* du = reinterpret_cast<uint4*>(hrow + TN / 2 + ch * 32);
-          uint4* da = reinterpret_cast<uint4*>(arow + ch * 32);
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            uint32_t pg[4], pu[4], pa[4];
-#pragma unroll
-            for (int w = 0; w < 4; ++w) {
-              const float g0 = __uint_as_float(g[8 * v + 2 * w]), g1 = __uint_as_float(g[8 * v + 2 * w + 1]);
-              const float u0 = __uint_as_float(u[8 * v + 2 * w]), u1 = __uint_as_float(u[8 * v + 2 * w + 1]);
-              pg[w] = pack_bf16x2(g0, g1);
-              pu[w] = pack_bf16x2(u0, u1);
-              pa[w] = pack_bf16x2(__fdividef(g0, 1.0f + __expf(-g0)) * u0, __fdividef(g1, 1.0f + __expf(-g1)) * u1);
+          for (int hh = 0; hh < 2; ++hh) {
+            if (lane == 0) {
+              bulk_wait_read<0>();  // earlier stores have drained both buffers
+              mbar_arrive_expect_tx(hbar, 2 * Cfg::kBoxBytes);
+              tma_load_2d(bufA, &p.tmAux, hbar, blk * 256 + hh * 64, out_row0);
+              tma_load_2d(bufB, &p.tmAux, hbar, blk * 256 + 128 + hh * 64, out_row0);
             }
-            dg[v] = make_uint4(pg[0], pg[1], pg[2], pg[3]);
-            du[v] = make_uint4(pu[0], pu[1], pu[2], pu[3]);
-            da[v] = make_uint4(pa[0], pa[1], pa[2], pa[3]);
-          }
-        }
-      } else if constexpr (kEpi == EPI_DSWIGLU) {
-        // dAct columns [ch2*128, ch2*128+128) = interleave block (2*nb + ch2): gate|up 256 cols of H/dH
-        const int64_t row = gg.a0 + tile_row;
-        const int64_t hcol = static_cast<int64_t>(tc.nb * 2 + ch2) * 256;
-        const __nv_bfloat16* hrow = reinterpret_cast<const __nv_bfloat16*>(p.aux) + row * p.ld_aux + hcol;
-        __nv_bfloat16* drow = reinterpret_cast<__nv_bfloat16*>(p.C) + row * p.ldc + hcol;
-        uint4 hgv[4], huv[4], ngv[4], nuv[4];
-        if (valid) {
+            uint32_t d0[32], d1[32];
+            tmem_ld_32x32b_x32(t_acc + ch2 * 128 + hh * 64, d0);
+            tmem_ld_32x32b_x32(t_acc + ch2 * 128 + hh * 64 + 32, d1);
+            mbar_wait(hbar, hphase);
+            hphase ^= 1;
+            uint4 hg[8], hu[8];
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            hgv[v] = reinterpret_cast<const uint4*>(hrow)[v];
-            huv[v] = reinterpret_cast<const uint4*>(hrow + 128)[v];
-          }
-        }
-#pragma unroll 1
-        for (int ch = 0; ch < 4; ++ch) {
-          uint32_t d[32];
-          tmem_ld_32x32b_x32(t_acc + ch2 * 128 + ch * 32, d);
-          if (valid && ch + 1 < 4) {  // prefetch H of the next chunk
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              ngv[v] = reinterpret_cast<const uint4*>(hrow + (ch + 1) * 32)[v];
-              nuv[v] = reinterpret_cast<const uint4*>(hrow + 128 + (ch + 1) * 32)[v];
+            for (int v = 0; v < 8; ++v) {
+              hg[v] = rowA[v ^ sw];
+              hu[v] = rowB[v ^ sw];
             }
-          }
-          tmem_ld_wait();
-          if (valid) {
-            uint4* og = reinterpret_cast<uint4*>(drow + ch * 32);
-            uint4* ou = reinterpret_cast<uint4*>(drow + 128 + ch * 32);
+            tmem_ld_wait();
+            __syncwarp();  // every lane holds its H row before the buffers are rewritten
+            uint32_t wa[32];
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              const uint32_t gw[4] = {hgv[v].x, hgv[v].y, hgv[v].z, hgv[v].w};
-              const uint32_t uw[4] = {huv[v].x, huv[v].y, huv[v].z, huv[v].w};
-              uint32_t rg[4], ru[4];
+            for (int v = 0; v < 8; ++v) {
+              const uint32_t gw[4] = {hg[v].x, hg[v].y, hg[v].z, hg[v].w};
+              const uint32_t uw[4] = {hu[v].x, hu[v].y, hu[v].z, hu[v].w};
+              uint32_t og[4], ou[4];
 #pragma unroll
-              for (int w = 0; w < 4; ++w) {
-                float dg2[2], du2[2];
+              for (int x = 0; x < 4; ++x) {
+                float dg2[2], du2[2], ag2[2];
 #pragma unroll
                 for (int h2 = 0; h2 < 2; ++h2) {
-                  const float gv = h2 ? bf16hi(gw[w]) : bf16lo(gw[w]);
-                  const float uv = h2 ? bf16hi(uw[w]) : bf16lo(uw[w]);
-                  const float dav = __uint_as_float(d[8 * v + 2 * w + h2]);
+                  const int col = v * 8 + x * 2 + h2;  // 0..63 within this half
+                  const float gv = h2 ? bf16hi(gw[x]) : bf16lo(gw[x]);
+                  const float uv = h2 ? bf16hi(uw[x]) : bf16lo(uw[x]);
+                  const float raw = __uint_as_float(col < 32 ? d0[col] : d1[col - 32]);
                   const float s = __fdividef(1.0f, 1.0f + __expf(-gv));
-                  du2[h2] = dav * gv * s;
-                  dg2[h2] = dav * uv * s * (1.0f + gv * (1.0f - s));
+                  const float act = gv * s * uv;
+                  if (kGated) part += raw * act;
+                  const float dav = gate * raw;
+                  du2[h2] = real ? dav * gv * s : 0.0f;
+                  dg2[h2] = real ? dav * uv * s * (1.0f + gv * (1.0f - s)) : 0.0f;
+                  ag2[h2] = real ? gate * act : 0.0f;
                 }
-                rg[w] = pack_bf16x2(dg2[0], dg2[1]);
-                ru[w] = pack_bf16x2(du2[0], du2[1]);
+                og[x] = pack_bf16x2(dg2[0], dg2[1]);
+                ou[x] = pack_bf16x2(du2[0], du2[1]);
+                wa[v * 4 + x] = pack_bf16x2(ag2[0], ag2[1]);
               }
-              og[v] = make_uint4(rg[0], rg[1], rg[2], rg[3]);
-              ou[v] = make_uint4(ru[0], ru[1], ru[2], ru[3]);
+              rowA[v ^ sw] = make_uint4(og[0], og[1], og[2], og[3]);
+              rowB[v ^ sw] = make_uint4(ou[0], ou[1], ou[2], ou[3]);
             }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              const uint64_t pol = l2_evict_first_policy();
+              tma_store_2d(&p.tmC, bufA, blk * 256 + hh * 64, out_row0, pol);
+              tma_store_2d(&p.tmC, bufB, blk * 256 + 128 + hh * 64, out_row0, pol);
+              bulk_commit();
+            }
+            if (kGated) {
+              if (lane == 0) bulk_wait_read<0>();
+              __syncwarp();
 #pragma unroll
-            for (int v = 0; v < 4; ++v) { hgv[v] = ngv[v]; huv[v] = nuv[v]; }
-          }
-        }
-      } else if constexpr (kEpi == EPI_DSWIGLU_GATED) {
-        // acc = dout.W2 (the dout rows arrive unscaled); block b = 2*nb + ch2 of H / dH / Act
-        const int64_t row = gg.a0 + tile_row;
-        const bool real = valid && tile_row < gg.rows_real;
-        const int blk = tc.nb * 2 + ch2;
-        const int64_t hcol = static_cast<int64_t>(blk) * 256;
-        const __nv_bfloat16* hrow = reinterpret_cast<const __nv_bfloat16*>(p.aux) + row * p.ld_aux + hcol;
-        __nv_bfloat16* drow = reinterpret_cast<__nv_bfloat16*>(p.C) + row * p.ldc + hcol;
-        __nv_bfloat16* arow = reinterpret_cast<__nv_bfloat16*>(p.C2) + row * p.ldc2 + static_cast<int64_t>(blk) * 128;
-        const float gate = real ? p.rscale[row] : 0.0f;
-        float part = 0.0f;
-        uint4 hgv[4], huv[4], ngv[4], nuv[4];
-        if (real) {
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            hgv[v] = reinterpret_cast<const uint4*>(hrow)[v];
-            huv[v] = reinterpret_cast<const uint4*>(hrow + 128)[v];
-          }
-        }
-#pragma unroll 1
-        for (int ch = 0; ch < 4; ++ch) {
-          uint32_t d[32];
-          tmem_ld_32x32b_x32(t_acc + ch2 * 128 + ch * 32, d);
-          if (real && ch + 1 < 4) {
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              ngv[v] = reinterpret_cast<const uint4*>(hrow + (ch + 1) * 32)[v];
-              nuv[v] = reinterpret_cast<const uint4*>(hrow + 128 + (ch + 1) * 32)[v];
+              for (int j = 0; j < 8; ++j) rowA[j ^ sw] = make_uint4(wa[4 * j], wa[4 * j + 1], wa[4 * j + 2], wa[4 * j + 3]);
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(&p.tmC2, bufA, blk * 128 + hh * 64, out_row0, l2_evict_first_policy());
+                bulk_commit();
+              }
             }
           }
+          if (kGated && real) p.rpart[row * (p.N / 128) + blk] = part;
+        } else {  // EPI_ACC_F32: fp32 boxes of 32 columns, reduce-add into the accumulator or store
+          const bool accumulate = (gg.flags & 1) != 0;
+          uint32_t r0[32], r1[32], r2[32], r3[32];
+          tmem_ld_32x32b_x32(t_acc + ch2 * 128, r0);
+          tmem_ld_32x32b_x32(t_acc + ch2 * 128 + 32, r1);
+          tmem_ld_32x32b_x32(t_acc + ch2 * 128 + 64, r2);
+          tmem_ld_32x32b_x32(t_acc + ch2 * 128 + 96, r3);
           tmem_ld_wait();
-          if (!valid) continue;
-          uint4* og = reinterpret_cast<uint4*>(drow + ch * 32);
-          uint4* ou = reinterpret_cast<uint4*>(drow + 128 + ch * 32);
-          uint4* oa = reinterpret_cast<uint4*>(arow + ch * 32);
-          if (!real) {  // padding rows: zero dH and gate*act so the wgrad sees exact zeros
-#pragma unroll
-            for (int v = 0; v < 4; ++v) og[v] = ou[v] = oa[v] = make_uint4(0, 0, 0, 0);
-            continue;
-          }
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const uint32_t gw[4] = {hgv[v].x, hgv[v].y, hgv[v].z, hgv[v].w};
-            const uint32_t uw[4] = {huv[v].x, huv[v].y, huv[v].z, huv[v].w};
-            uint32_t rg[4], ru[4], ra[4];
-#pragma unroll
-            for (int w = 0; w < 4; ++w) {
-              float dg2[2], du2[2], ag2[2];
-#pragma unroll
-              for (int h2 = 0; h2 < 2; ++h2) {
-                const float gv = h2 ? bf16hi(gw[w]) : bf16lo(gw[w]);
-                const float uv = h2 ? bf16hi(uw[w]) : bf16lo(uw[w]);
-                const float raw = __uint_as_float(d[8 * v + 2 * w + h2]);
-                const float s = __fdividef(1.0f, 1.0f + __expf(-gv));
-                const float act = gv * s * uv;
-                part += raw * act;
-                const float dav = gate * raw;
-                du2[h2] = dav * gv * s;
-                dg2[h2] = dav * uv * s * (1.0f + gv * (1.0f - s));
-                ag2[h2] = gate * act;
-              }
-              rg[w] = pack_bf16x2(dg2[0], dg2[1]);
-              ru[w] = pack_bf16x2(du2[0], du2[1]);
-              ra[w] = pack_bf16x2(ag2[0], ag2[1]);
-            }
-            og[v] = make_uint4(rg[0], rg[1], rg[2], rg[3]);
-            ou[v] = make_uint4(ru[0], ru[1], ru[2], ru[3]);
-            oa[v] = make_uint4(ra[0], ra[1], ra[2], ra[3]);
-          }
-#pragma unroll
-          for (int v = 0; v < 4; ++v) { hgv[v] = ngv[v]; huv[v] = nuv[v]; }
-        }
-        if (real) p.rpart[row * (p.N / 128) + blk] = part;
-      } else {  // EPI_ACC_F32
-        const bool accumulate = (gg.flags & 1) != 0;
-        float* crow = reinterpret_cast<float*>(p.C) + gg.slot * p.c_slot_stride +
-                      static_cast<int64_t>(tile_row) * p.ldc + tc.nb * TN + ch2 * 128;
-#pragma unroll 1
-        for (int ch = 0; ch < 4; ++ch) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(t_acc + ch2 * 128 + ch * 32, r);
-          float4* dst = reinterpret_cast<float4*>(crow + ch * 32);
-          float4 old[8];
+          release();
+          const int32_t c0 = tc.nb * TN + ch2 * 128;
           if (accumulate) {
-#pragma unroll
-            for (int v = 0; v < 8; ++v) old[v] = dst[v];
-          }
-          tmem_ld_wait();
-#pragma unroll
-          for (int v = 0; v < 8; ++v) {
-            float4 o = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                   __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
-            if (accumulate) { o.x += old[v].x; o.y += old[v].y; o.z += old[v].z; o.w += old[v].w; }
-            dst[v] = o;
+            st.put<true>(r0, &p.tmC, c0, out_row0);
+            st.put<true>(r1, &p.tmC, c0 + 32, out_row0);
+            st.put<true>(r2, &p.tmC, c0 + 64, out_row0);
+            st.put<true>(r3, &p.tmC, c0 + 96, out_row0);
+          } else {
+            st.put<false>(r0, &p.tmC, c0, out_row0);
+            st.put<false>(r1, &p.tmC, c0 + 32, out_row0);
+            st.put<false>(r2, &p.tmC, c0 + 64, out_row0);
+            st.put<false>(r3, &p.tmC, c0 + 96, out_row0);
           }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (leader) mbar_arrive(&tempty_bar[acc]);
-        else mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
-      }
+      if (!released) release();
     }
+    if (lane == 0) bulk_wait<0>();  // every TMA store of this warp has completed
+    __syncwarp();
   }
   tc_fence_before();
   __syncthreads();

@@ -258,11 +258,11 @@ class MoEDataPlane:
         self.cps = torch.cuda.Stream(device=self.device)     # copy-engine stream: replica pushes
         self.launches = 0
         self.timing = False       # record CUDA events around every K4 launch (bench roofline)
-        self.gemm_events = []     # (start, end, algorithmic FLOPs)
+        self.gemm_events = []     # (start, end, algorithmic FLOPs, kind)
         self.load_plan(plan)
 
     # ------------------------------------------------------------------ helpers
-    def _timed(self, flops: float):
+    def _timed(self, flops: float, kind: str = "gemm"):
         """Context manager recording CUDA events on the current stream around a K4 launch."""
         dp = self
 
@@ -276,7 +276,7 @@ class MoEDataPlane:
             def __exit__(self, *a):
                 if dp.timing:
                     self.e.record()
-                    dp.gemm_events.append((self.s, self.e, flops))
+                    dp.gemm_events.append((self.s, self.e, flops, kind))
         return _T()
 
     def real_rows(self, m: int) -> int:
@@ -442,10 +442,10 @@ class MoEDataPlane:
             if ng:
                 g = self.groups[m][:ng]
                 rows = self.real_rows(m)
-                with self._timed(4.0 * rows * h * hp):
+                with self._timed(4.0 * rows * h * hp, "fwd_swiglu"):
                     K.grouped_gemm(K.GEMM_FWD_SWIGLU, self.Xr[m], self.W1, g, N=2 * hp, K=h, C=self.H[m],
                                    C2=self.Act[m], B1=self.W1r[m])
-                with self._timed(2.0 * rows * h * hp):
+                with self._timed(2.0 * rows * h * hp, "fwd_down"):
                     K.grouped_gemm(K.GEMM_FWD_STORE, self.Act[m], self.W2, g, N=h, K=hp, C=self.Y[m],
                                    B1=self.W2r[m])
                 self.launches += 2
@@ -477,11 +477,11 @@ class MoEDataPlane:
                 rows = self.real_rows(m)
                 # dAct = dout.W2 with the combine backward fused in the epilogue: gate applied per row,
                 # dgate partials <dout.W2, act> = <dout, Y>, gate*act written over Act for dW2
-                with self._timed(2.0 * rows * h * hp):
+                with self._timed(2.0 * rows * h * hp, "dgrad_act_gated"):
                     K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU_GATED, self.dYr[m], self.W2, g, N=hp, K=h, C=self.dH[m],
                                    C2=self.Act[m], aux=self.H[m], B1=self.W2r[m], row_scale=self.gate_r[m],
                                    row_partial=self.dgate_r[m])
-                with self._timed(4.0 * rows * h * hp):
+                with self._timed(4.0 * rows * h * hp, "dgrad_x"):
                     K.grouped_gemm(K.GEMM_DGRAD_STORE, self.dH[m], self.W1, g, N=h, K=2 * hp, C=self.dXp[m],
                                    B1=self.W1r[m])
                 self.launches += 2
@@ -516,10 +516,10 @@ class MoEDataPlane:
         if not self.wgroups.shape[0]:
             return
         rows = sum(self.real_rows(m) for m in range(MB))
-        with self._timed(2.0 * rows * h * hp):
+        with self._timed(2.0 * rows * h * hp, "wgrad_down"):
             K.grouped_gemm(K.GEMM_WGRAD, self.dYr.view(MB * R, h), self.Act.view(MB * R, hp), self.wgroups, M=h, N=hp,
                            C=self.gW2, c_slot_stride=h * hp, segs=self.wsegs)
-        with self._timed(4.0 * rows * h * hp):
+        with self._timed(4.0 * rows * h * hp, "wgrad_gate_up"):
             K.grouped_gemm(K.GEMM_WGRAD, self.dH.view(MB * R, 2 * hp), self.Xr.view(MB * R, h), self.wgroups,
                            M=2 * hp, N=h, C=self.gW1, c_slot_stride=2 * hp * h, segs=self.wsegs)
         self.launches += 2
