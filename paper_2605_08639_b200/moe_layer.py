@@ -17,7 +17,8 @@ One process per GPU; every rank runs, per step of MB micro-batches:
 
 Two streams: the compute stream runs the GEMMs, the comm stream runs dispatch / combine and
 every device barrier (totally ordered per rank), linked by per-micro-batch events, so the
-NVLink all-to-all of one micro-batch overlaps the tensor-core work of another.  Routing is
+NVLink all-to-all of one micro-batch overlaps the tensor-core work of another (two micro-batches
+in flight, see schedule()).  Routing is
 replayed, so every count, row offset and replica is known before the step: the host planners
 run once per step (StepPlan) and the kernels never exchange sizes.
 """
@@ -188,6 +189,30 @@ def deinterleave_w1(w1: torch.Tensor) -> tuple:
 
 
 # ----------------------------------------------------------------------------- data plane
+
+
+def schedule(mb: int):
+    """Per-rank issue order of one step, two micro-batches in flight (the two-batch overlap of
+    EP training systems): compute runs F0 F1 B0 F2 B1 ... F(n-1) B(n-2) B(n-1), the comm stream
+    D0 D1 C0 [D(m) C(m-1) X(m-2)]... so every all-to-all overlaps a GEMM phase of the neighbouring
+    micro-batch, while each combine is still a global sync point: a rank can run at most one
+    phase ahead of the slowest rank, so load imbalance is paid per micro-batch (as the
+    reference's cost model sums it, sim.py:89-110), not averaged over the step.
+    F = fwd GEMMs, B = bwd GEMMs, D = dispatch, C = combine + dout dispatch, X = dX un-permute."""
+    comp = [("F", 0)]
+    for m in range(1, mb):
+        comp += [("F", m), ("B", m - 1)]
+    comp.append(("B", mb - 1))
+    comm = [("D", 0)]
+    if mb > 1:
+        comm += [("D", 1)]
+    comm.append(("C", 0))
+    for m in range(2, mb):
+        comm += [("D", m), ("C", m - 1), ("X", m - 2)]
+    if mb > 1:
+        comm += [("C", mb - 1), ("X", mb - 2)]
+    comm.append(("X", mb - 1))
+    return comm, comp
 
 
 class MoEDataPlane:
@@ -413,9 +438,9 @@ class MoEDataPlane:
                 nat.check(lib.mb_memcpy_async(d2, self.W2[loc].data_ptr(), self.w2_bytes, self.cps.cuda_stream),
                           lib, "replica push")
             xs.wait_stream(self.cps)
-        # ---- dispatch of every micro-batch (comm stream)
-        ev_disp = []
-        for m in range(MB):
+        ev_comm, ev_comp = {}, {}
+
+        def dispatch(m):  # D(m): K1 histogram, K2 ranks, K3 scatter into every rank's receive rows
             if hooks:
                 hooks.inputs_ready(m, xs)
             self._k("mb_expert_histogram", idx[m].data_ptr(), 1, T, k, E, self.counts[m].data_ptr(),
@@ -431,13 +456,25 @@ class MoEDataPlane:
             self._k("mb_scatter_rows", x[m].data_ptr(), T, k, h, self.perm[m].data_ptr(), self.ptr_xr[m].data_ptr(),
                     st_x)
             A.barrier(xs)  # rows of micro-batch m have landed everywhere
-            ev = torch.cuda.Event()
-            ev.record(xs)
-            ev_disp.append(ev)
-        # ---- forward GEMMs (compute stream)
-        ev_fwd = []
-        for m in range(MB):
-            cs.wait_event(ev_disp[m])
+
+        def combine(m):  # C(m): K6 gate-weighted combine of Y, then the raw dout rows out (K3)
+            A.barrier(xs)  # Y of micro-batch m complete on every rank
+            self._k("mb_combine_rows", self.ptr_y[m].data_ptr(), self.perm[m].data_ptr(), gates[m].data_ptr(),
+                    T, k, h, out[m].data_ptr(), None, None, 1, st_x)
+            if hooks:
+                hooks.after_forward(m, xs)
+            self._k("mb_scatter_rows", dout[m].data_ptr(), T, k, h, self.perm[m].data_ptr(),
+                    self.ptr_dyr[m].data_ptr(), st_x)
+            A.barrier(xs)  # dout rows of micro-batch m have landed everywhere
+
+        def unpermute(m):  # X(m): dX un-permute + dgate gather
+            A.barrier(xs)  # dX rows / dgate partials of micro-batch m complete everywhere
+            self._k("mb_combine_rows", self.ptr_dxp[m].data_ptr(), self.perm[m].data_ptr(), None, T, k, h,
+                    dx[m].data_ptr(), self.ptr_dgate[m].data_ptr(), dgate[m].data_ptr(), self.npart, st_x)
+            if hooks:
+                hooks.after_backward(m, xs)
+
+        def forward(m):  # F(m): gate/up GEMM + SwiGLU, down GEMM
             ng = self.nslots[m]
             if ng:
                 g = self.groups[m][:ng]
@@ -449,28 +486,8 @@ class MoEDataPlane:
                     K.grouped_gemm(K.GEMM_FWD_STORE, self.Act[m], self.W2, g, N=h, K=hp, C=self.Y[m],
                                    B1=self.W2r[m])
                 self.launches += 2
-            ev = torch.cuda.Event()
-            ev.record(cs)
-            ev_fwd.append(ev)
-        # ---- combine + raw-dout dispatch (comm stream)
-        ev_dout = []
-        for m in range(MB):
-            xs.wait_event(ev_fwd[m])
-            A.barrier(xs)  # Y of micro-batch m complete on every rank
-            self._k("mb_combine_rows", self.ptr_y[m].data_ptr(), self.perm[m].data_ptr(), gates[m].data_ptr(),
-                    T, k, h, out[m].data_ptr(), None, None, 1, st_x)
-            if hooks:
-                hooks.after_forward(m, xs)
-            self._k("mb_scatter_rows", dout[m].data_ptr(), T, k, h, self.perm[m].data_ptr(),
-                    self.ptr_dyr[m].data_ptr(), st_x)
-            A.barrier(xs)  # dout rows of micro-batch m have landed everywhere
-            ev = torch.cuda.Event()
-            ev.record(xs)
-            ev_dout.append(ev)
-        # ---- backward GEMMs (compute stream)
-        ev_bwd = []
-        for m in range(MB):
-            cs.wait_event(ev_dout[m])
+
+        def backward(m):  # B(m): dAct (combine backward + dSwiGLU fused in the epilogue), dX
             ng = self.nslots[m]
             if ng:
                 g = self.groups[m][:ng]
@@ -485,17 +502,36 @@ class MoEDataPlane:
                     K.grouped_gemm(K.GEMM_DGRAD_STORE, self.dH[m], self.W1, g, N=h, K=2 * hp, C=self.dXp[m],
                                    B1=self.W1r[m])
                 self.launches += 2
-            ev = torch.cuda.Event()
-            ev.record(cs)
-            ev_bwd.append(ev)
-        # ---- dX un-permute + dgate gather (comm stream), overlapping the weight gradients
-        for m in range(MB):
-            xs.wait_event(ev_bwd[m])
-            A.barrier(xs)  # dX rows / dgate partials of micro-batch m complete everywhere
-            self._k("mb_combine_rows", self.ptr_dxp[m].data_ptr(), self.perm[m].data_ptr(), None, T, k, h,
-                    dx[m].data_ptr(), self.ptr_dgate[m].data_ptr(), dgate[m].data_ptr(), self.npart, st_x)
-            if hooks:
-                hooks.after_backward(m, xs)
+
+        comm_fn = {"D": dispatch, "C": combine, "X": unpermute}
+        comp_fn = {"F": forward, "B": backward}
+        comm_needs = {"C": "F", "X": "B"}   # comm op waits for this compute op of the same micro-batch
+        comp_needs = {"F": "D", "B": "C"}
+        comm_ops, comp_ops = schedule(MB)
+        ci = pi = 0
+        # host issue order only has to respect the cross-stream event dependencies; each stream
+        # then runs its own sequence in order on the device
+        while ci < len(comm_ops) or pi < len(comp_ops):
+            if ci < len(comm_ops):
+                cop, cm = comm_ops[ci]
+                dep = (comm_needs[cop], cm) if cop in comm_needs else None
+                if dep is None or dep in ev_comp:
+                    if dep is not None:
+                        xs.wait_event(ev_comp[dep])
+                    comm_fn[cop](cm)
+                    ev_comm[(cop, cm)] = torch.cuda.Event()
+                    ev_comm[(cop, cm)].record(xs)
+                    ci += 1
+                    continue
+            op, m = comp_ops[pi]
+            dep = (comp_needs[op], m)
+            if dep not in ev_comm:
+                raise RuntimeError(f"step schedule deadlock at {op}{m}")
+            cs.wait_event(ev_comm[dep])
+            comp_fn[op](m)
+            ev_comp[(op, m)] = torch.cuda.Event()
+            ev_comp[(op, m)].record(cs)
+            pi += 1
         # ---- weight gradients (compute stream), K over every micro-batch of the step
         self._wgrad()
         ev = torch.cuda.Event()

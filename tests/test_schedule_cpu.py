@@ -1,0 +1,47 @@
+"""Step schedule of the data plane (moe_layer.schedule): every phase of every micro-batch issued
+once, and the two in-order streams linked by their events cannot deadlock."""
+
+import pytest
+
+from paper_2605_08639_b200.moe_layer import schedule
+
+COMM_NEEDS = {"C": "F", "X": "B"}
+COMP_NEEDS = {"F": "D", "B": "C"}
+
+
+def _simulate(comm, comp):
+    """Run both in-order queues to completion; an op starts once its dependency finished."""
+    done, ci, pi, order = set(), 0, 0, []
+    while ci < len(comm) or pi < len(comp):
+        progressed = False
+        if ci < len(comm):
+            op, m = comm[ci]
+            if op not in COMM_NEEDS or (COMM_NEEDS[op], m) in done:
+                done.add((op, m)); order.append((op, m)); ci += 1; progressed = True
+        if pi < len(comp):
+            op, m = comp[pi]
+            if (COMP_NEEDS[op], m) in done:
+                done.add((op, m)); order.append((op, m)); pi += 1; progressed = True
+        if not progressed:
+            raise AssertionError(f"deadlock at comm {comm[ci:ci+1]} compute {comp[pi:pi+1]}")
+    return order
+
+
+@pytest.mark.parametrize("mb", [1, 2, 3, 4, 8, 16])
+def test_schedule_complete_and_deadlock_free(mb):
+    comm, comp = schedule(mb)
+    assert sorted(comm) == sorted((p, m) for m in range(mb) for p in "DCX")
+    assert sorted(comp) == sorted((p, m) for m in range(mb) for p in "FB")
+    order = _simulate(comm, comp)
+    pos = {o: i for i, o in enumerate(order)}
+    for m in range(mb):
+        assert pos[("D", m)] < pos[("F", m)] < pos[("C", m)] < pos[("B", m)] < pos[("X", m)]
+
+
+def test_at_most_two_micro_batches_ahead():
+    # the dispatch of micro-batch m is queued behind the combine of m-2: a rank can never start
+    # the GEMMs of a micro-batch while two earlier ones have not been combined everywhere
+    comm, _ = schedule(8)
+    pos = {o: i for i, o in enumerate(comm)}
+    for m in range(2, 8):
+        assert pos[("C", m - 2)] < pos[("D", m)]
