@@ -26,11 +26,11 @@ static int launch_pair(const GemmParams& p, cudaStream_t stream) {
   auto kern = grouped_gemm_pair_kernel<kW, kAmn, kBmn, kEpi>;
   static bool attr_set = false;
   if (!attr_set) {
-    MB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg::kSmemBytes));
+    MB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<kEpi>::kSmemBytes));
     attr_set = true;
   }
   const int grid = device_sm_count() & ~1;
-  kern<<<grid, 320, PairCfg::kSmemBytes, stream>>>(p);
+  kern<<<grid, 320, PairCfg<kEpi>::kSmemBytes, stream>>>(p);
   MB_CUDA_TRY(cudaGetLastError());
   return MB_OK;
 }
@@ -94,6 +94,11 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
       if ((rc = make_tmap_bf16_2d(&p.tmA, A, a_cols, a_rows, a_cols * 2, 64, 128))) return rc;
       if ((rc = make_tmap_bf16_2d(&p.tmB0, B0, b_cols, b0_rows, b_cols * 2, 64, bbox))) return rc;
       if ((rc = make_tmap_bf16_2d(&p.tmB1, B1, b_cols, b1_rows, b_cols * 2, 64, bbox))) return rc;
+      if (pair) {  // tail tiles
+        if ((rc = make_tmap_bf16_2d(&p.tmAh, A, a_cols, a_rows, a_cols * 2, 64, 64))) return rc;
+        if ((rc = make_tmap_bf16_2d(&p.tmB0h, B0, b_cols, b0_rows, b_cols * 2, 64, 64))) return rc;
+        if ((rc = make_tmap_bf16_2d(&p.tmB1h, B1, b_cols, b1_rows, b_cols * 2, 64, 64))) return rc;
+      }
       if (mode == MB_GEMM_FWD_STORE)
         return pair ? launch_pair<false, false, false, EPI_STORE_BF16>(p, s)
                     : launch_gemm<false, false, false, 256, EPI_STORE_BF16>(p, s);
@@ -106,6 +111,7 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
                    "gated dSwiGLU GEMM needs the CTA-pair kernel and N %% 256 == 0 (N=%d K=%d)", N, K);
       MB_CHECK_ARG(aux && C2 && row_scale && row_partial, "gated dSwiGLU needs H, Act out, gate and partials");
       if ((rc = make_tmap_bf16_2d(&p.tmA, A, a_cols, a_rows, a_cols * 2, 64, 128))) return rc;
+      if ((rc = make_tmap_bf16_2d(&p.tmAh, A, a_cols, a_rows, a_cols * 2, 64, 64))) return rc;
       if ((rc = make_tmap_bf16_2d(&p.tmB0, B0, b_cols, b0_rows, b_cols * 2, 64, 64))) return rc;
       if ((rc = make_tmap_bf16_2d(&p.tmB1, B1, b_cols, b1_rows, b_cols * 2, 64, 64))) return rc;
       return launch_pair<false, false, true, EPI_DSWIGLU_GATED>(p, s);
@@ -114,6 +120,7 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
     case MB_GEMM_DGRAD_DSWIGLU: {
       MB_CHECK_ARG(K % 64 == 0 && a_cols == K && b_cols == N, "dgrad GEMM shape N=%d K=%d", N, K);
       if ((rc = make_tmap_bf16_2d(&p.tmA, A, a_cols, a_rows, a_cols * 2, 64, 128))) return rc;
+      if (pair && (rc = make_tmap_bf16_2d(&p.tmAh, A, a_cols, a_rows, a_cols * 2, 64, 64))) return rc;
       if ((rc = make_tmap_bf16_2d(&p.tmB0, B0, b_cols, b0_rows, b_cols * 2, 64, 64))) return rc;
       if ((rc = make_tmap_bf16_2d(&p.tmB1, B1, b_cols, b1_rows, b_cols * 2, 64, 64))) return rc;
       if (mode == MB_GEMM_DGRAD_STORE) {

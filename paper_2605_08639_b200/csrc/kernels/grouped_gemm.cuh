@@ -27,21 +27,23 @@ enum GemmEpi : int {
   EPI_ACC_F32 = 3,     // C_slot (+)= acc (fp32)
   EPI_DSWIGLU_GATED = 4,  // acc = dout.W2 (unscaled); aux = H; rscale = gate per row:
                           //   C = dH of gate*acc, C2 = gate*act (in place of Act, feeds dW2),
-                          //   rpart[row][N/128] = partial <acc, act> (dgate = <dout, Y>)
+                          //   rpart[row][N/64] = partial <acc, act> (dgate = <dout, Y>)
 };
 
 // Per-group descriptor (device memory, written by the dispatch-plan tables).
 struct GemmGroup {
-  int32_t rows;       // F: rows of the group (multiple of 128). W: total K rows (multiple of 64).
+  int32_t rows;       // F: rows of the group (multiple of 128). W: total K rows (multiple of 16).
   int32_t a0;         // F: first row in A (and C). W: first token row in A and B (single segment).
   int32_t slot;       // F: weight slot index in the selected B tensor. W: output slot.
   int32_t flags;      // bit0: accumulate into C (W). bit1: B from tensor map 1 (replica slots).
   int32_t seg_begin;  // W: first entry in the segment table (K split over micro-batches)
   int32_t seg_count;  // W: number of segments; 0 means the single segment (a0, rows)
   int32_t rows_real;  // F: rows holding tokens (the rest of `rows` is padding); used by gated epilogues
-  int32_t pad1;
+  int32_t kblocks;    // W: sum over segments of ceil(rows / 64); 0 = ceil(rows / 64) (single segment)
 };
-// W-mode K segment: `rows` token rows (multiple of 64) starting at token row `a0`.
+// W-mode K segment: `rows` token rows (multiple of 16) starting at token row `a0`.  The last
+// k-block of a segment may be partial: its TMA box reads past the segment (harmless rows of the
+// next slot, or zero fill past the tensor end) and only ceil(rest / 16) K16 MMAs are issued.
 struct GemmSeg {
   int32_t a0, rows;
 };
@@ -50,6 +52,31 @@ constexpr int kMaxGroups = 256;
 constexpr int BM = 128;
 constexpr int BK = 64;
 
+// Walks the k-blocks of a W-mode group over its K segments (one per micro-batch).
+struct KWalker {
+  const GemmSeg* segs;
+  int next, row, left;
+  __device__ __forceinline__ KWalker(const GemmGroup& gg, const GemmSeg* s)
+      : segs(s), next(gg.seg_begin), row(gg.a0), left(gg.seg_count ? 0 : gg.rows) {}
+  // token row of the next k-block; nk16 = K16 steps it holds (1..4)
+  __device__ __forceinline__ int step(int& nk16) {
+    while (left <= 0) {
+      const GemmSeg g = segs[next++];
+      row = g.a0;
+      left = g.rows;
+    }
+    const int krow = row;
+    nk16 = left >= BK ? BK / 16 : (left + 15) >> 4;
+    row += BK;
+    left -= BK;
+    return krow;
+  }
+};
+
+__device__ __forceinline__ int w_kblocks(const GemmGroup& gg) {
+  return gg.kblocks ? gg.kblocks : (gg.rows + BK - 1) / BK;
+}
+
 struct GemmParams {
   CUtensorMap tmA;
   CUtensorMap tmB0;
@@ -57,6 +84,9 @@ struct GemmParams {
   CUtensorMap tmC;   // epilogue TMA store maps (CTA-pair kernel): output C (box 32 rows x 128 B)
   CUtensorMap tmC2;  // secondary output C2
   CUtensorMap tmAux; // epilogue TMA load map of the auxiliary input (H for the dSwiGLU epilogues)
+  CUtensorMap tmAh;  // CTA-pair tail tiles: 64-row boxes of A (K-major) and B (K-major)
+  CUtensorMap tmB0h;
+  CUtensorMap tmB1h;
   const GemmGroup* groups;
   const GemmSeg* segs;
   int num_groups;
@@ -69,7 +99,7 @@ struct GemmParams {
   const void* aux;
   int64_t ld_aux;
   const float* rscale;  // per-row scale (gate) for EPI_DSWIGLU_GATED
-  float* rpart;         // per-row partial sums [rows][N/128] for EPI_DSWIGLU_GATED
+  float* rpart;         // per-row partial sums [rows][N/64] for EPI_DSWIGLU_GATED
   int debug;            // bit0: skip the epilogue (TMEM drained, nothing stored) -- profiling only
 };
 
@@ -102,7 +132,7 @@ __device__ __forceinline__ TileCoord decode_tile(int t, const int* tile_start, c
   const int n_tiles = p.N / BN;
   c.mb = local / n_tiles;
   c.nb = local - c.mb * n_tiles;
-  c.kblocks = kW ? (sg[lo].rows / BK) : (p.K / BK);
+  c.kblocks = kW ? w_kblocks(sg[lo]) : (p.K / BK);
   return c;
 }
 
@@ -185,18 +215,10 @@ __global__ void __launch_bounds__(192, 1) grouped_gemm_kernel(const __grid_const
         const GemmGroup gg = sg[tc.g];
         const CUtensorMap* tmB = (gg.flags & 2) ? &p.tmB1 : &p.tmB0;
         // W mode: walk the K segments (one per micro-batch); F mode: a single implicit segment
-        int seg = 0, seg_row = gg.a0, seg_left = kW ? (gg.seg_count ? 0 : gg.rows / BK) : tc.kblocks;
+        KWalker kw(gg, p.segs);
         for (int kb = 0; kb < tc.kblocks; ++kb) {
-          if (kW) {
-            while (seg_left == 0) {
-              const GemmSeg sgm = p.segs[gg.seg_begin + seg++];
-              seg_row = sgm.a0;
-              seg_left = sgm.rows / BK;
-            }
-            --seg_left;
-          }
-          const int krow = seg_row;  // W: token row of this k-block
-          if (kW) seg_row += BK;
+          int nk16 = BK / 16;
+          const int krow = kW ? kw.step(nk16) : 0;  // W: token row of this k-block
           mbar_wait(&empty_bar[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
           uint8_t* a_dst = sA + stage * Cfg::kABytes;
@@ -236,13 +258,17 @@ __global__ void __launch_bounds__(192, 1) grouped_gemm_kernel(const __grid_const
         mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * 256;
+        KWalker kw(sg[tc.g], p.segs);
         for (int kb = 0; kb < tc.kblocks; ++kb) {
+          int nk16 = BK / 16;
+          if (kW) kw.step(nk16);
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * Cfg::kABytes);
           const uint32_t b_addr = smem_u32(sB + stage * Cfg::kBBytes);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
+            if (k >= nk16) break;
             const uint64_t adesc = kAmn ? make_sw128_desc(a_addr + k * 2048, 8192, 1024)
                                         : make_sw128_desc(a_addr + k * 32, 16, 1024);
             const uint64_t bdesc = kBmn ? make_sw128_desc(b_addr + k * 2048, 8192, 1024)

@@ -23,17 +23,27 @@
 
 namespace mb {
 
-struct PairCfg {
-  static constexpr int kStages = 4;
+struct PairTile {
+  static constexpr int TM = 256, TN = 256;
+  static constexpr int kBoxBytes = 32 * 128;  // one 32-row x 128-byte TMA box
+};
+
+// Shared-memory budget per epilogue kind: the dSwiGLU epilogues stage H gate|up in two boxes per
+// warp and keep 4 operand stages; the others single-buffer their output box and spend the 32 KB
+// on a 5th stage (more bytes in flight: at MoE shapes the weight stream makes the mainloop
+// latency-sensitive).
+template <int kEpi>
+struct PairCfg : PairTile {
+  static constexpr int kBoxesPerWarp = (kEpi == EPI_DSWIGLU || kEpi == EPI_DSWIGLU_GATED) ? 2 : 1;
+  static constexpr int kStages = kBoxesPerWarp == 2 ? 4 : 5;
   static constexpr int kABytes = 128 * BK * 2;  // this CTA's 128 rows of A
   static constexpr int kBBytes = 128 * BK * 2;  // this CTA's 128 columns of B
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kEpiWarps = 8;
-  static constexpr int kBoxBytes = 32 * 128;  // one 32-row x 128-byte TMA box
-  static constexpr int kStagingBytes = kEpiWarps * 2 * kBoxBytes;
+  static constexpr int kStagingBytes = kEpiWarps * kBoxesPerWarp * kBoxBytes;
   static constexpr int kMetaBytes = 10240;
   static constexpr int kSmemBytes = kStages * kStageBytes + kStagingBytes + kMetaBytes + 1024;
-  static constexpr int TM = 256, TN = 256;
+  static_assert(kSmemBytes <= 232448, "shared memory budget");
 };
 
 template <bool kW>
@@ -47,29 +57,47 @@ __device__ __forceinline__ TileCoord decode_tile_pair(int t, const int* tile_sta
   TileCoord c;
   c.g = lo;
   const int local = t - tile_start[lo];
-  const int n_tiles = p.N / PairCfg::TN;
+  const int n_tiles = p.N / PairTile::TN;
   c.mb = local / n_tiles;
   c.nb = local - c.mb * n_tiles;
-  c.kblocks = kW ? (sg[lo].rows / BK) : (p.K / BK);
+  c.kblocks = kW ? w_kblocks(sg[lo]) : (p.K / BK);
   return c;
 }
 
+// F-mode tail tile: the last 128 padded rows of a group whose row count is an odd multiple of 128.
+// It runs as M=128 cta_group::2 MMAs (64 rows per CTA) issued twice with N=128 (the two 128-wide
+// column blocks of the 256-wide tile), so no tensor-core work is spent on a half-empty pair tile.
+// TMEM layout of such an MMA (the "2x2" datapath layout): lanes 0-63 hold columns [0, 64) and
+// lanes 64-127 hold columns [64, 128) of the CTA's 64 rows; block j lands at TMEM column j*64.
+__device__ __forceinline__ bool half_tile(const GemmGroup& gg, const TileCoord& tc, int debug) {
+  return gg.rows - tc.mb * PairTile::TM <= 128 && !(debug & 16);  // debug 16: full tiles only (A/B)
+}
+
 // Per-warp double-buffered TMA store staging: 2 boxes of 32 rows x 128 B, 128B swizzle.
+template <int kBufs>
 struct BoxStager {
   uint8_t* base;
   int buf = 0;
   int lane;
   int debug = 0;
-  // write this lane's 128-byte row of the next box (32 words) and issue the store
+  // write this lane's 128-byte row of the next box (words lo[0..15] then hi[0..15]) and issue the store
   template <bool kReduce>
   __device__ __forceinline__ void put(const uint32_t (&w)[32], const CUtensorMap* map, int32_t c0, int32_t c1) {
-    uint8_t* b = base + buf * PairCfg::kBoxBytes;
-    if (lane == 0) bulk_wait_read<1>();  // the store that last used this buffer has read it
+    put2<kReduce>(w, w + 16, map, c0, c1);
+  }
+  template <bool kReduce>
+  __device__ __forceinline__ void put2(const uint32_t* lo, const uint32_t* hi, const CUtensorMap* map, int32_t c0,
+                                       int32_t c1) {
+    uint8_t* b = base + buf * PairTile::kBoxBytes;
+    if (lane == 0) bulk_wait_read<kBufs - 1>();  // the store that last used this buffer has read it
     __syncwarp();
     uint4* row = reinterpret_cast<uint4*>(b + lane * 128);
     if (!(debug & 4)) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) row[j ^ (lane & 7)] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+      for (int j = 0; j < 4; ++j) row[j ^ (lane & 7)] = make_uint4(lo[4 * j], lo[4 * j + 1], lo[4 * j + 2], lo[4 * j + 3]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        row[(4 + j) ^ (lane & 7)] = make_uint4(hi[4 * j], hi[4 * j + 1], hi[4 * j + 2], hi[4 * j + 3]);
     }
     fence_proxy_async_smem();
     __syncwarp();
@@ -80,7 +108,7 @@ struct BoxStager {
       else tma_store_2d(map, b, c0, c1, pol);
       bulk_commit();
     }
-    buf ^= 1;
+    if (kBufs > 1) buf ^= 1;
   }
 };
 
@@ -94,7 +122,7 @@ __device__ __forceinline__ void pack_bf16_words(const uint32_t (&a)[32], const u
 template <bool kW, bool kAmn, bool kBmn, int kEpi>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     grouped_gemm_pair_kernel(const __grid_constant__ GemmParams p) {
-  using Cfg = PairCfg;
+  using Cfg = PairCfg<kEpi>;
   constexpr int S = Cfg::kStages;
   constexpr int TM = Cfg::TM, TN = Cfg::TN;
   extern __shared__ uint8_t smem_raw[];
@@ -178,37 +206,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         const TileCoord tc = decode_tile_pair<kW>(t, tile_start, sg, ng, p);
         const GemmGroup gg = sg[tc.g];
         const CUtensorMap* tmB = (gg.flags & 2) ? &p.tmB1 : &p.tmB0;
-        int seg = 0, seg_row = gg.a0, seg_left = kW ? (gg.seg_count ? 0 : gg.rows / BK) : tc.kblocks;
+        const CUtensorMap* tmBh = (gg.flags & 2) ? &p.tmB1h : &p.tmB0h;
+        const bool half = !kW && half_tile(gg, tc, p.debug);
+        const int bytes = half ? 2 * (Cfg::kABytes / 2 + Cfg::kBBytes) : 2 * Cfg::kStageBytes;
+        KWalker kw(gg, p.segs);
         for (int kb = 0; kb < tc.kblocks; ++kb) {
-          if (kW) {
-            while (seg_left == 0) {
-              const GemmSeg sgm = p.segs[gg.seg_begin + seg++];
-              seg_row = sgm.a0;
-              seg_left = sgm.rows / BK;
-            }
-            --seg_left;
-          }
-          const int krow = seg_row;
-          if (kW) seg_row += BK;
+          int nk16 = BK / 16;
+          const int krow = kW ? kw.step(nk16) : 0;
           mbar_wait(&empty_bar[stage], phase ^ 1);
           const uint32_t lbar = mapa_shared(smem_u32(&full_bar[stage]), 0);
-          if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::kStageBytes);
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], bytes);
           uint8_t* a_dst = sA + stage * Cfg::kABytes;
           uint8_t* b_dst = sB + stage * Cfg::kBBytes;
           if (!kAmn) {
-            tma_load_2d_pair(a_dst, &p.tmA, lbar, kb * BK, gg.a0 + tc.mb * TM + rank * 128);
+            if (half) tma_load_2d_pair(a_dst, &p.tmAh, lbar, kb * BK, gg.a0 + tc.mb * TM + rank * 64);
+            else tma_load_2d_pair(a_dst, &p.tmA, lbar, kb * BK, gg.a0 + tc.mb * TM + rank * 128);
           } else {
 #pragma unroll
             for (int j = 0; j < 2; ++j)
               tma_load_2d_pair(a_dst + j * 8192, &p.tmA, lbar, tc.mb * TM + rank * 128 + j * 64, krow);
           }
           if (!kBmn) {
-            tma_load_2d_pair(b_dst, tmB, lbar, kb * BK, gg.slot * p.N + tc.nb * TN + rank * 128);
+            if (half) {
+              // this CTA's 64-column halves of both 128-column blocks
+#pragma unroll
+              for (int j = 0; j < 2; ++j)
+                tma_load_2d_pair(b_dst + j * 8192, tmBh, lbar, kb * BK, gg.slot * p.N + tc.nb * TN + j * 128 + rank * 64);
+            } else {
+              tma_load_2d_pair(b_dst, tmB, lbar, kb * BK, gg.slot * p.N + tc.nb * TN + rank * 128);
+            }
           } else {
             const int row0 = kW ? krow : (gg.slot * p.K + kb * BK);
 #pragma unroll
-            for (int j = 0; j < 2; ++j)
-              tma_load_2d_pair(b_dst + j * 8192, tmB, lbar, tc.nb * TN + rank * 128 + j * 64, row0);
+            for (int j = 0; j < 2; ++j) {
+              const int col = half ? tc.nb * TN + j * 128 + rank * 64 : tc.nb * TN + rank * 128 + j * 64;
+              tma_load_2d_pair(b_dst + j * 8192, tmB, lbar, col, row0);
+            }
           }
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
@@ -219,6 +252,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     // ------------------------------------------------------------ MMA issuer (leader CTA)
     if (leader && lane == 0) {
       constexpr uint32_t idesc = make_idesc_bf16(TM, TN, kAmn ? 1u : 0u, kBmn ? 1u : 0u);
+      constexpr uint32_t idesc_h = make_idesc_bf16(128, 128, kAmn ? 1u : 0u, kBmn ? 1u : 0u);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -228,18 +262,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * 256;
+        const GemmGroup gg = sg[tc.g];
+        const bool half = !kW && half_tile(gg, tc, p.debug);
+        KWalker kw(gg, p.segs);
         for (int kb = 0; kb < tc.kblocks; ++kb) {
+          int nk16 = BK / 16;
+          if (kW) kw.step(nk16);
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * Cfg::kABytes);
           const uint32_t b_addr = smem_u32(sB + stage * Cfg::kBBytes);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
+            if (k >= nk16) break;
+            const uint32_t accum = (kb | k) != 0 ? 1u : 0u;
             const uint64_t adesc = kAmn ? make_sw128_desc(a_addr + k * 2048, 8192, 1024)
                                         : make_sw128_desc(a_addr + k * 32, 16, 1024);
-            const uint64_t bdesc = kBmn ? make_sw128_desc(b_addr + k * 2048, 8192, 1024)
-                                        : make_sw128_desc(b_addr + k * 32, 16, 1024);
-            umma_bf16_pair(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+            if (!half) {
+              const uint64_t bdesc = kBmn ? make_sw128_desc(b_addr + k * 2048, 8192, 1024)
+                                          : make_sw128_desc(b_addr + k * 32, 16, 1024);
+              umma_bf16_pair(d_tmem, adesc, bdesc, idesc, accum);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const uint64_t bdesc = kBmn ? make_sw128_desc(b_addr + j * 8192 + k * 2048, 8192, 1024)
+                                            : make_sw128_desc(b_addr + j * 8192 + k * 32, 16, 1024);
+                umma_bf16_pair(d_tmem + j * 64, adesc, bdesc, idesc_h, accum);
+              }
+            }
           }
           umma_commit_pair(&empty_bar[stage], 0x3);
           if (++stage == S) { stage = 0; phase ^= 1; }
@@ -257,7 +307,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty_bar[1]), 0);
-    BoxStager st{sStage + (warp - 2) * 2 * Cfg::kBoxBytes, 0, lane, p.debug};
+    BoxStager<Cfg::kBoxesPerWarp> st{sStage + (warp - 2) * Cfg::kBoxesPerWarp * Cfg::kBoxBytes, 0, lane, p.debug};
     uint64_t* hbar = hbar_base + (warp - 2);
     uint32_t hphase = 0;
     int it = 0;
@@ -268,9 +318,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t t_acc = tmem_base + lane_off + acc * 256;
-      const int warp_row0 = tc.mb * TM + static_cast<int>(rank) * 128 + q * 32;  // first row of this warp's box
+      // full tile: this warp owns rows q*32.. of the CTA's 128 and columns [ch2*128, +128);
+      // tail tile (half_tile): rows (q&1)*32.. of the CTA's 64; lane group q>>1 holds columns
+      // [(q>>1)*64, +64) of both 128-column blocks; the ch2 = 1 warps have nothing to do
+      const bool half = !kW && half_tile(gg, tc, p.debug);
+      const int warp_row0 = half ? tc.mb * TM + static_cast<int>(rank) * 64 + (q & 1) * 32
+                                 : tc.mb * TM + static_cast<int>(rank) * 128 + q * 32;
       const int tile_row = warp_row0 + lane;
-      const bool valid = kW || warp_row0 < gg.rows;   // groups are 128-row padded: uniform per warp
+      // 64-column segment s of this warp: TMEM column and output column (within the 256-wide tile)
+      auto tcol = [&](int s) { return half ? s * 64 : ch2 * 128 + s * 64; };
+      auto ocol = [&](int s) { return half ? s * 128 + (q >> 1) * 64 : ch2 * 128 + s * 64; };
+      const bool valid = (kW || warp_row0 < gg.rows) && !(half && ch2);  // 128-row padded groups
       const int32_t out_row0 = kW ? gg.slot * p.M + warp_row0 : gg.a0 + warp_row0;
       bool released = false;
       // hand the accumulator back to the MMA warp as soon as this warp holds its columns
@@ -292,52 +350,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       } else if (valid) {
         if constexpr (kEpi == EPI_STORE_BF16) {
           uint32_t a0[32], a1[32], b0[32], b1[32], w[32];
-          tmem_ld_32x32b_x32(t_acc + ch2 * 128, a0);
-          tmem_ld_32x32b_x32(t_acc + ch2 * 128 + 32, a1);
-          tmem_ld_32x32b_x32(t_acc + ch2 * 128 + 64, b0);
-          tmem_ld_32x32b_x32(t_acc + ch2 * 128 + 96, b1);
+          tmem_ld_32x32b_x32(t_acc + tcol(0), a0);
+          tmem_ld_32x32b_x32(t_acc + tcol(0) + 32, a1);
+          tmem_ld_32x32b_x32(t_acc + tcol(1), b0);
+          tmem_ld_32x32b_x32(t_acc + tcol(1) + 32, b1);
           tmem_ld_wait();
           release();
           pack_bf16_words(a0, a1, w);
-          st.put<false>(w, &p.tmC, tc.nb * TN + ch2 * 128, out_row0);
+          st.put<false>(w, &p.tmC, tc.nb * TN + ocol(0), out_row0);
           pack_bf16_words(b0, b1, w);
-          st.put<false>(w, &p.tmC, tc.nb * TN + ch2 * 128 + 64, out_row0);
+          st.put<false>(w, &p.tmC, tc.nb * TN + ocol(1), out_row0);
         } else if constexpr (kEpi == EPI_SWIGLU) {
-          // gate columns [0,128), up columns [128,256); this warp owns gate/up columns [ch2*64, +64)
+          // gate columns [0,128), up columns [128,256); this warp owns gate/up features [f0, +64)
+          // (tail tile: gate block at TMEM [0,64), up block at [64,128))
+          const int f0 = half ? (q >> 1) * 64 : ch2 * 64;
+          const int tg = half ? 0 : ch2 * 64, tu = half ? 64 : 128 + ch2 * 64;
           uint32_t g0[32], g1[32], u0[32], u1[32], w[32];
-          tmem_ld_32x32b_x32(t_acc + ch2 * 64, g0);
-          tmem_ld_32x32b_x32(t_acc + ch2 * 64 + 32, g1);
-          tmem_ld_32x32b_x32(t_acc + 128 + ch2 * 64, u0);
-          tmem_ld_32x32b_x32(t_acc + 128 + ch2 * 64 + 32, u1);
+          tmem_ld_32x32b_x32(t_acc + tg, g0);
+          tmem_ld_32x32b_x32(t_acc + tg + 32, g1);
+          tmem_ld_32x32b_x32(t_acc + tu, u0);
+          tmem_ld_32x32b_x32(t_acc + tu + 32, u1);
           tmem_ld_wait();
           release();
-          pack_bf16_words(g0, g1, w);
-          st.put<false>(w, &p.tmC, tc.nb * TN + ch2 * 64, out_row0);
-          pack_bf16_words(u0, u1, w);
-          st.put<false>(w, &p.tmC, tc.nb * TN + 128 + ch2 * 64, out_row0);
+          // pack H in place (word i of each half from values 2i, 2i+1); the activation is
+          // computed from the bf16-rounded H, exactly what the backward pass recomputes
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const float a0 = __uint_as_float(g0[2 * i]), a1 = __uint_as_float(g0[2 * i + 1]);
-            const float b0 = __uint_as_float(u0[2 * i]), b1 = __uint_as_float(u0[2 * i + 1]);
+            g0[i] = pack_bf16x2(__uint_as_float(g0[2 * i]), __uint_as_float(g0[2 * i + 1]));
+            u0[i] = pack_bf16x2(__uint_as_float(u0[2 * i]), __uint_as_float(u0[2 * i + 1]));
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            g1[i] = pack_bf16x2(__uint_as_float(g1[2 * i]), __uint_as_float(g1[2 * i + 1]));
+            u1[i] = pack_bf16x2(__uint_as_float(u1[2 * i]), __uint_as_float(u1[2 * i + 1]));
+          }
+          st.put2<false>(g0, g1, &p.tmC, tc.nb * TN + f0, out_row0);
+          st.put2<false>(u0, u1, &p.tmC, tc.nb * TN + 128 + f0, out_row0);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const uint32_t gw = i < 16 ? g0[i] : g1[i - 16];
+            const uint32_t uw = i < 16 ? u0[i] : u1[i - 16];
+            const float a0 = bf16lo(gw), a1 = bf16hi(gw), b0 = bf16lo(uw), b1 = bf16hi(uw);
             w[i] = pack_bf16x2(__fdividef(a0, 1.0f + __expf(-a0)) * b0, __fdividef(a1, 1.0f + __expf(-a1)) * b1);
           }
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float a0 = __uint_as_float(g1[2 * i]), a1 = __uint_as_float(g1[2 * i + 1]);
-            const float b0 = __uint_as_float(u1[2 * i]), b1 = __uint_as_float(u1[2 * i + 1]);
-            w[16 + i] = pack_bf16x2(__fdividef(a0, 1.0f + __expf(-a0)) * b0, __fdividef(a1, 1.0f + __expf(-a1)) * b1);
-          }
-          st.put<false>(w, &p.tmC2, tc.nb * (TN / 2) + ch2 * 64, out_row0);
+          st.put<false>(w, &p.tmC2, tc.nb * (TN / 2) + f0, out_row0);
         } else if constexpr (kEpi == EPI_DSWIGLU || kEpi == EPI_DSWIGLU_GATED) {
-          // dAct columns [ch2*128, +128) = interleave block blk: gate|up 256 columns of H / dH
-          // H (gate|up) comes in through TMA into the warp's two staging buffers, is read back row
-          // per lane, and the same buffers then carry dH (and gate*act) out through TMA stores.
+          // dAct columns of 64-column segment hh = features [fo, +64) of interleave block blk:
+          // gate|up 256 columns of H / dH.  H (gate|up) comes in through TMA into the warp's two
+          // staging buffers, is read back row per lane, and the same buffers then carry dH (and
+          // gate*act) out through TMA stores.
           constexpr bool kGated = kEpi == EPI_DSWIGLU_GATED;
           const int64_t row = gg.a0 + tile_row;
           const bool real = !kGated || tile_row < gg.rows_real;
-          const int blk = tc.nb * 2 + ch2;
           const float gate = kGated ? (real ? p.rscale[row] : 0.0f) : 1.0f;
-          float part = 0.0f;
           uint8_t* bufA = st.base;
           uint8_t* bufB = st.base + Cfg::kBoxBytes;
           uint4* rowA = reinterpret_cast<uint4*>(bufA + lane * 128);
@@ -345,15 +410,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
           const int sw = lane & 7;
 #pragma unroll 1
           for (int hh = 0; hh < 2; ++hh) {
+            const int blk = tc.nb * 2 + ocol(hh) / 128;
+            const int fo = ocol(hh) % 128;
+            float part = 0.0f;
             if (lane == 0) {
               bulk_wait_read<0>();  // earlier stores have drained both buffers
               mbar_arrive_expect_tx(hbar, 2 * Cfg::kBoxBytes);
-              tma_load_2d(bufA, &p.tmAux, hbar, blk * 256 + hh * 64, out_row0);
-              tma_load_2d(bufB, &p.tmAux, hbar, blk * 256 + 128 + hh * 64, out_row0);
+              tma_load_2d(bufA, &p.tmAux, hbar, blk * 256 + fo, out_row0);
+              tma_load_2d(bufB, &p.tmAux, hbar, blk * 256 + 128 + fo, out_row0);
             }
             uint32_t d0[32], d1[32];
-            tmem_ld_32x32b_x32(t_acc + ch2 * 128 + hh * 64, d0);
-            tmem_ld_32x32b_x32(t_acc + ch2 * 128 + hh * 64 + 32, d1);
+            tmem_ld_32x32b_x32(t_acc + tcol(hh), d0);
+            tmem_ld_32x32b_x32(t_acc + tcol(hh) + 32, d1);
             mbar_wait(hbar, hphase);
             hphase ^= 1;
             uint4 hg[8], hu[8];
@@ -398,8 +466,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
             __syncwarp();
             if (lane == 0) {
               const uint64_t pol = l2_evict_first_policy();
-              tma_store_2d(&p.tmC, bufA, blk * 256 + hh * 64, out_row0, pol);
-              tma_store_2d(&p.tmC, bufB, blk * 256 + 128 + hh * 64, out_row0, pol);
+              tma_store_2d(&p.tmC, bufA, blk * 256 + fo, out_row0, pol);
+              tma_store_2d(&p.tmC, bufB, blk * 256 + 128 + fo, out_row0, pol);
               bulk_commit();
             }
             if (kGated) {
@@ -410,12 +478,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
               fence_proxy_async_smem();
               __syncwarp();
               if (lane == 0) {
-                tma_store_2d(&p.tmC2, bufA, blk * 128 + hh * 64, out_row0, l2_evict_first_policy());
+                tma_store_2d(&p.tmC2, bufA, blk * 128 + fo, out_row0, l2_evict_first_policy());
                 bulk_commit();
               }
             }
+            // partial <dAct, act> over these 64 features: rpart[row][N/64]
+            if (kGated && real) p.rpart[row * (p.N / 64) + blk * 2 + fo / 64] = part;
           }
-          if (kGated && real) p.rpart[row * (p.N / 128) + blk] = part;
         } else {  // EPI_ACC_F32: fp32 boxes of 32 columns, reduce-add into the accumulator or store
           const bool accumulate = (gg.flags & 1) != 0;
           uint32_t r0[32], r1[32], r2[32], r3[32];

@@ -33,17 +33,19 @@ def _need_cuda(*tensors):
             raise ValueError("data-plane ops take CUDA tensors (there is no CPU path)")
 
 
-def make_groups(rows, a0, slot, flags=None, seg_begin=None, seg_count=None, rows_real=None,
+def make_groups(rows, a0, slot, flags=None, seg_begin=None, seg_count=None, rows_real=None, kblocks=None,
                 device="cuda") -> torch.Tensor:
-    """Pack per-group (rows, a0, slot, flags, seg_begin, seg_count, rows_real) into the int32 [G, 8] table."""
+    """Pack per-group (rows, a0, slot, flags, seg_begin, seg_count, rows_real, kblocks) into the
+    int32 [G, 8] table.  kblocks (wgrad): sum over the group's K segments of ceil(rows / 64)."""
     n = len(rows)
     z = [0] * n
     flags = z if flags is None else flags
     seg_begin = z if seg_begin is None else seg_begin
     seg_count = z if seg_count is None else seg_count
     rows_real = rows if rows_real is None else rows_real
+    kblocks = z if kblocks is None else kblocks
     tab = np.zeros((n, GROUP_FIELDS), dtype=np.int32)
-    for c, v in enumerate((rows, a0, slot, flags, seg_begin, seg_count, rows_real)):
+    for c, v in enumerate((rows, a0, slot, flags, seg_begin, seg_count, rows_real, kblocks)):
         tab[:, c] = np.asarray(v, dtype=np.int64)
     return torch.from_numpy(tab).to(device)
 

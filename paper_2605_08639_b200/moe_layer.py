@@ -233,7 +233,7 @@ class MoEDataPlane:
         self.slots = max(plan.slots, 1)
         self.rep_cap = max(1, self.slots * micro_batches)
         bf, f4 = 2, 4
-        self.npart = hp // 128   # dgate partials per row (one per 128-column block of h')
+        self.npart = hp // 64    # dgate partials per row (one per 64 features of h')
         R, MB = self.R, micro_batches
         S = self.M + self.rep_cap
         self.w1_bytes, self.w2_bytes = 2 * hp * h * bf, h * hp * bf
@@ -352,29 +352,30 @@ class MoEDataPlane:
         self.nslots = nsl
         self.pushes = pushes
         # ---- wgrad groups: home experts (accumulate) then experts replicated onto this rank
+        # K segments = the slot's real rows rounded up to 16 (pad rows are zero in both operands;
+        # the kernel issues K16 MMAs only up to the segment end)
         wg, segs = [], []
         R = self.R
-        for loc, ex in enumerate(self.home_experts):
-            s0, tot = len(segs), 0
-            for m, mbp in enumerate(plan.mbs):
-                st = mbp.slot_tab[d]
-                for s in range(int(mbp.nslots[d])):
-                    if st[s, 3] == ex and mbp.slot_w[d][s, 1] == 0 and st[s, 2] > 0:
-                        segs.append((m * R + int(st[s, 0]), int(st[s, 2])))
-                        tot += int(st[s, 2])
-            wg.append((tot, 0, loc, K.FLAG_ACCUMULATE, s0, len(segs) - s0))
-        for q, ex in enumerate(plan.rep_experts[d]):
-            s0, tot = len(segs), 0
+
+        def add_group(ex, replica, out_slot, flags):
+            s0, tot, kb = len(segs), 0, 0
             for m, mbp in enumerate(plan.mbs):
                 st, sw = mbp.slot_tab[d], mbp.slot_w[d]
                 for s in range(int(mbp.nslots[d])):
-                    if st[s, 3] == ex and sw[s, 1] == 1 and st[s, 2] > 0:
-                        segs.append((m * R + int(st[s, 0]), int(st[s, 2])))
-                        tot += int(st[s, 2])
-            wg.append((tot, 0, self.M + q, 0, s0, len(segs) - s0))
+                    if st[s, 3] == ex and sw[s, 1] == replica and st[s, 1] > 0:
+                        r16 = (int(st[s, 1]) + 15) // 16 * 16
+                        segs.append((m * R + int(st[s, 0]), r16))
+                        tot += r16
+                        kb += (r16 + 63) // 64
+            wg.append((tot, 0, out_slot, flags, s0, len(segs) - s0, 0, kb))
+
+        for loc, ex in enumerate(self.home_experts):
+            add_group(ex, 0, loc, K.FLAG_ACCUMULATE)
+        for q, ex in enumerate(plan.rep_experts[d]):
+            add_group(ex, 1, self.M + q, 0)
         wtab = np.zeros((len(wg), K.GROUP_FIELDS), dtype=np.int32)
         for i, row in enumerate(wg):
-            wtab[i, :6] = row
+            wtab[i] = row
         self.wgroups = torch.from_numpy(wtab).to(dev)
         self.wsegs = torch.from_numpy(np.asarray(segs if segs else [(0, 0)], dtype=np.int32).reshape(-1, 2)).to(dev)
         # ---- replica gradient reduce lists (this rank as owner): only replicas that served rows

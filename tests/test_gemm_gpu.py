@@ -116,11 +116,12 @@ def test_dgrad_dswiglu():
         assert rel_err(dH[sl], ref) < 2e-2
 
 
-def test_dgrad_dswiglu_gated():
-    """Fused combine-backward: raw dout rows in, gate per row, dgate partials, gate*act out."""
+@pytest.mark.parametrize("rows,real", [([256, 128], [200, 128]), ([384, 128, 512], [300, 77, 512])])
+def test_dgrad_dswiglu_gated(rows, real):
+    """Fused combine-backward: raw dout rows in, gate per row, dgate partials, gate*act out.
+    Odd multiples of 128 rows exercise the M=128 tail tiles of the CTA-pair kernel."""
     torch.manual_seed(7)
     hp, hd = 512, 256
-    rows, real = [256, 128], [200, 128]
     a0, R = _row_groups(rows)
     dout = torch.randn(R, hd, device=DEV).bfloat16()
     W2 = (torch.randn(2, hd, hp, device=DEV) * hd ** -0.5).bfloat16()
@@ -128,11 +129,13 @@ def test_dgrad_dswiglu_gated():
     gate = torch.rand(R, device=DEV)
     dH = torch.full((R, 2 * hp), float("nan"), device=DEV).bfloat16()
     actg = torch.full((R, hp), float("nan"), device=DEV).bfloat16()
-    part = torch.zeros(R, hp // 128, device=DEV)
-    K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU_GATED, dout, W2, K.make_groups(rows, a0, [0, 1], rows_real=real), N=hp, K=hd,
-                   C=dH, C2=actg, aux=H, row_scale=gate, row_partial=part)
+    part = torch.zeros(R, hp // 64, device=DEV)
+    S = len(rows)
+    W2 = (torch.randn(S, hd, hp, device=DEV) * hd ** -0.5).bfloat16()
+    K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU_GATED, dout, W2, K.make_groups(rows, a0, list(range(S)), rows_real=real),
+                   N=hp, K=hd, C=dH, C2=actg, aux=H, row_scale=gate, row_partial=part)
     torch.cuda.synchronize()
-    for g in range(2):
+    for g in range(S):
         sl = slice(a0[g], a0[g] + real[g])
         raw = dout[sl].float() @ W2[g].float()
         hb = H[sl].float().view(real[g], -1, 2, 128)
@@ -189,6 +192,35 @@ def test_wgrad_accumulate():
         if flags[g] & K.FLAG_ACCUMULATE:
             ref = ref + C0[s]
         assert rel_err(C[s], ref) < 1e-3
+
+
+def test_wgrad_segments_16_rows():
+    """K split over segments whose row counts are multiples of 16 (partial last k-blocks)."""
+    torch.manual_seed(9)
+    Md, Nd = 256, 256
+    R = 1024
+    A = torch.randn(R, Md, device=DEV).bfloat16()
+    B = torch.randn(R, Nd, device=DEV).bfloat16()
+    segs_g = [[(0, 48), (128, 16), (512, 112)], [(256, 64), (640, 208)], [(900, 16)]]
+    segs, seg_begin, seg_count, tot, kblocks = [], [], [], [], []
+    for sg in segs_g:
+        seg_begin.append(len(segs))
+        seg_count.append(len(sg))
+        segs.extend(sg)
+        tot.append(sum(r for _, r in sg))
+        kblocks.append(sum((r + 63) // 64 for _, r in sg))
+    groups = K.make_groups(tot, [0] * 3, [2, 0, 1], [0, K.FLAG_ACCUMULATE, 0], seg_begin, seg_count,
+                           kblocks=kblocks)
+    C0 = torch.randn(3, Md, Nd, device=DEV)
+    C = C0.clone()
+    K.grouped_gemm(K.GEMM_WGRAD, A, B, groups, M=Md, N=Nd, C=C, c_slot_stride=Md * Nd,
+                   segs=torch.tensor(segs, dtype=torch.int32, device=DEV))
+    torch.cuda.synchronize()
+    for g, (sg, slot) in enumerate(zip(segs_g, [2, 0, 1])):
+        ref = sum(A[a:a + r].float().T @ B[a:a + r].float() for a, r in sg)
+        if g == 1:
+            ref = ref + C0[slot]
+        assert rel_err(C[slot], ref) < 1e-3
 
 
 def test_histogram_matches_bincount():

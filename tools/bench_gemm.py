@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--h", type=int, default=2048)
     ap.add_argument("--hp", type=int, default=768)
     ap.add_argument("--only", default="")
+    ap.add_argument("--zipf-rows", action="store_true",
+                    help="group rows = micro-batch 0 of the bench's skewed Qwen3 routing at EP=1 (128-padded)")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     a = ap.parse_args()
@@ -41,7 +43,13 @@ def main():
     R = G * r
     dev = "cuda"
     rows = [r] * G
-    a0 = [i * r for i in range(G)]
+    if a.zipf_rows:
+        from paper_2605_08639_b200.workload import SHAPES, make_routing
+        rt = make_routing(SHAPES["qwen3-30b-a3b"]["shape"], 8192, 1, 1, 0)
+        rows = [int((c + 127) // 128 * 128) for c in rt.mats[0, 0]]
+        G = len(rows)
+    a0 = [sum(rows[:i]) for i in range(G)]
+    R = sum(rows)
     groups = K.make_groups(rows, a0, list(range(G)))
     wg = K.make_groups(rows, a0, list(range(G)), [K.FLAG_ACCUMULATE] * G)
     X = torch.randn(R, h, device=dev).bfloat16()
@@ -65,7 +73,7 @@ def main():
     if not only or "fwd2_store" in only: res["fwd2_store"] = (timeit(lambda: K.grouped_gemm(K.GEMM_FWD_STORE, Act, W2, groups, N=h, K=hp, C=Y)), flop)
     if not only or "dgrad_dswiglu" in only: res["dgrad_dswiglu"] = (timeit(lambda: K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU, dY, W2, groups, N=hp, K=h, C=dH, aux=H)), flop)
     gate = torch.rand(R, device=dev)
-    part = torch.empty(R, hp // 128, device=dev)
+    part = torch.empty(R, hp // 64, device=dev)
     if only and "dgrad_gated" in only: res["dgrad_gated"] = (timeit(lambda: K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU_GATED, dY, W2, groups, N=hp, K=h, C=dH, C2=Act, aux=H, row_scale=gate, row_partial=part)), flop)
     if not only or "dgrad_dx" in only: res["dgrad_dx"] = (timeit(lambda: K.grouped_gemm(K.GEMM_DGRAD_STORE, dH, W1, groups, N=h, K=2 * hp, C=dX)), 2 * flop)
     if not only or "wgrad_w2" in only: res["wgrad_w2"] = (timeit(lambda: K.grouped_gemm(K.GEMM_WGRAD, dY, Act, wg, M=h, N=hp, C=gW2, c_slot_stride=h * hp)), flop)
