@@ -204,15 +204,22 @@ def measure_policy(args, comm, policy, shape, cfg, routing, topo, model, cfgs, w
     res = {"ms": ms_max, "plan_ms": plan_ms, "skew": plan.skew(), "launches": launches,
            "rows": [dp.real_rows(m) for m in range(MB)], "rows_cap": plan.rows_cap}
     if want_detail:
-        gemm_ms = sum(a.elapsed_time(b) for a, b, _, _ in dp.gemm_events) / args.steps
-        gemm_flop = sum(f for _, _, f, _ in dp.gemm_events) / args.steps
+        gev = [ev for ev in dp.gemm_events if not ev[3].startswith("comm_")]
+        cev = [ev for ev in dp.gemm_events if ev[3].startswith("comm_")]
+        gemm_ms = sum(a.elapsed_time(b) for a, b, _, _ in gev) / args.steps
+        gemm_flop = sum(f for _, _, f, _ in gev) / args.steps
         kinds = {}
         for a, b, f, kd in dp.gemm_events:
             ms_f = kinds.setdefault(kd, [0.0, 0.0])
             ms_f[0] += a.elapsed_time(b) / args.steps
             ms_f[1] += f / args.steps
-        res["gemm_kinds"] = {kd: {"ms": round(v[0], 4), "tflops": round(v[1] / v[0] / 1e9, 1)} for kd, v in kinds.items()}
-        res.update(gemm_ms=gemm_ms, gemm_flop=gemm_flop, gemm_launches=len(dp.gemm_events) // args.steps,
+        res["gemm_kinds"] = {kd: {"ms": round(v[0], 4), "tflops": round(v[1] / v[0] / 1e9, 1)}
+                             for kd, v in kinds.items() if not kd.startswith("comm_")}
+        # comm phases on the comm stream (barriers included): NVLink bytes this rank moves / time
+        res["comm_kinds"] = {kd[5:]: {"ms": round(v[0], 4), "nvlink_gb": round(v[1] / 1e9, 4),
+                                      "gb_per_s": round(v[1] / v[0] / 1e6, 1) if v[0] > 0 else 0.0}
+                             for kd, v in kinds.items() if kd.startswith("comm_")}
+        res.update(gemm_ms=gemm_ms, gemm_flop=gemm_flop, gemm_launches=len(gev) // args.steps,
                    clocks=clocks)
         # e2e through the host-buffer API (pinned host tensors, copies inside the timed region)
         host = {k: v.cpu().pin_memory() for k, v in dev.items()}
@@ -273,6 +280,14 @@ def run_ours(args, comm):
     results = {}
     for pol in policies:
         routing = balanced if pol == "balanced_oracle" else skewed
+        if pol == "relibra_box":
+            # ReLibra with the whole NVSwitch box as one replication group (group = EP)
+            if group == world:
+                continue
+            box = b200_box_topology(world, world, b200_profile(shape.hidden))
+            results[pol] = measure_policy(args, comm, "relibra", shape, cfg, routing, box, model, cfgs,
+                                          want_detail=False)
+            continue
         results[pol] = measure_policy(args, comm, pol, shape, cfg, routing, topo, model, cfgs,
                                       want_detail=(pol == args.headline))
     head = results[args.headline]
@@ -298,6 +313,7 @@ def run_ours(args, comm):
                      "flops_per_step": head["gemm_flop"], "gemm_ms_per_step": round(head["gemm_ms"], 4),
                      "gemm_share_of_step": round(head["gemm_ms"] / head["ms"], 4),
                      "per_kind": head["gemm_kinds"]},
+        "comm": head["comm_kinds"],
         "e2e": {"value": tokens_step / (head["e2e_ms"] / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": head["h2d"],
                 "d2h_bytes_per_step": head["d2h"], "ms_per_step": head["e2e_ms"]},
         "gpu_launches": head["launches"],
@@ -331,7 +347,8 @@ def main():
     ap.add_argument("--slots", type=int, default=None)
     ap.add_argument("--group", type=int, default=0)
     ap.add_argument("--sa-chains", type=int, default=8)
-    ap.add_argument("--policies", default="relibra,static,eplb_like,balanced_oracle")
+    ap.add_argument("--policies", default="relibra,static,eplb_like,balanced_oracle,relibra_box",
+                    help="relibra_box = relibra with one replication group spanning all EP GPUs (run when EP > group)")
     ap.add_argument("--headline", default="relibra")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

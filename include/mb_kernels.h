@@ -29,6 +29,11 @@ int mb_version(void);
 int mb_expert_histogram(const int32_t* idx, int64_t nb, int64_t tokens, int32_t topk, int32_t num_experts,
                         uint32_t* counts, uint32_t* chunk_counts, int32_t chunk_tokens, void* stream);
 
+/* SMs the persistent grouped GEMM may occupy (0 = all; env MB_GEMM_SMS overrides).  The SMs left
+ * free run the dispatch / combine kernels of the comm stream while the GEMM runs (the
+ * reference models comm and compute as separate resources, costmodel.py:205-213). */
+int mb_set_gemm_sms(int sms);
+
 /* ---------------------------------------------------------------- K4 grouped GEMM
  * tcgen05/TMEM/TMA persistent grouped GEMM (bf16 in, fp32 accumulate).
  * Replaces: costmodel.comp_time (costmodel.py:161-163), the modelled 6*h*h' FLOP/token expert

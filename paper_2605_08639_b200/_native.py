@@ -37,6 +37,7 @@ _KERNEL_SIGS = {
     "mb_last_error": (c_char_p, []),
     "mb_version": (c_int, []),
     "mb_expert_histogram": (c_int, [c_vp, c_i64, c_i64, c_i32, c_i32, c_vp, c_vp, c_i32, c_vp]),
+    "mb_set_gemm_sms": (c_int, [c_int]),
     "mb_grouped_gemm": (
         c_int,
         [c_int, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp, c_int, c_int, c_int, c_int,

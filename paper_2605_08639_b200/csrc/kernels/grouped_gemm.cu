@@ -8,6 +8,8 @@
 
 namespace mb {
 
+static int gemm_sms();
+
 template <bool kW, bool kAmn, bool kBmn, int BN, int kEpi>
 static int launch_gemm(const GemmParams& p, cudaStream_t stream) {
   auto kern = grouped_gemm_kernel<kW, kAmn, kBmn, BN, kEpi>;
@@ -29,10 +31,20 @@ static int launch_pair(const GemmParams& p, cudaStream_t stream) {
     MB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<kEpi>::kSmemBytes));
     attr_set = true;
   }
-  const int grid = device_sm_count() & ~1;
+  const int grid = gemm_sms() & ~1;
   kern<<<grid, 320, PairCfg<kEpi>::kSmemBytes, stream>>>(p);
   MB_CUDA_TRY(cudaGetLastError());
   return MB_OK;
+}
+
+// SMs the persistent GEMM occupies (mb_set_gemm_sms / MB_GEMM_SMS, default all): the rest stay
+// free for the dispatch / combine kernels the comm stream runs concurrently.
+static int g_gemm_sms = 0;
+static int gemm_sms() {
+  const int n = device_sm_count();
+  int v = g_gemm_sms;
+  if (const char* e = std::getenv("MB_GEMM_SMS")) v = std::atoi(e);
+  return (v >= 2 && v <= n) ? v : n;
 }
 
 static bool pair_enabled() {
@@ -47,6 +59,12 @@ static bool pair_enabled() {
 }  // namespace mb
 
 using namespace mb;
+
+extern "C" int mb_set_gemm_sms(int sms) {
+  MB_CHECK_ARG(sms >= 0, "sms must be >= 0 (0 = all)");
+  g_gemm_sms = sms;
+  return MB_OK;
+}
 
 extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t a_cols, const void* B0,
                                int64_t b0_rows, const void* B1, int64_t b1_rows, int64_t b_cols,

@@ -39,6 +39,10 @@ from .cluster import ClusterTopology, HardwareProfile
 from .comm import Comm, SymmetricArena
 
 PAD = 128       # receive-slot row padding = GEMM M tile
+# SMs left to the comm stream while the persistent GEMM runs (measured on B200, qwen3 shape:
+# N=4 step 24.1 ms with all 148 SMs in the GEMM, 19.7 ms with 28 left free; N=1 best at 20)
+COMM_SMS = {1: 20}
+COMM_SMS_MULTI = 28
 CHUNK = 32      # tokens per permutation chunk
 GATE_BLOCK = 128  # gate|up interleave block of W1 rows (= half the 256-wide SwiGLU tile)
 
@@ -220,11 +224,16 @@ class MoEDataPlane:
     fp32 gradients, per-micro-batch receive/activation buffers and the step tables."""
 
     def __init__(self, comm: Comm, shape: LayerShape, tokens: int, micro_batches: int, plan: StepPlan,
-                 device: torch.device | None = None):
+                 device: torch.device | None = None, comm_sms: int | None = None):
         shape.check()
         self.comm, self.shape, self.T, self.MB = comm, shape, tokens, micro_batches
         self.rank, self.world = comm.rank, comm.world
         self.device = device or torch.device("cuda", torch.cuda.current_device())
+        if comm_sms is None:
+            comm_sms = COMM_SMS.get(self.world, COMM_SMS_MULTI)
+        sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+        lib = nat.kernels()
+        nat.check(lib.mb_set_gemm_sms(max(2, sms - comm_sms)), lib, "mb_set_gemm_sms")
         E, h, hp = shape.num_experts, shape.hidden, shape.ffn
         if E % self.world:
             raise ValueError(f"{E} experts not divisible by {self.world} GPUs")
@@ -287,8 +296,9 @@ class MoEDataPlane:
         self.load_plan(plan)
 
     # ------------------------------------------------------------------ helpers
-    def _timed(self, flops: float, kind: str = "gemm"):
-        """Context manager recording CUDA events on the current stream around a K4 launch."""
+    def _timed(self, amount: float, kind: str = "gemm", stream=None):
+        """Context manager recording CUDA events around a launch sequence on `stream` (default:
+        the current stream).  amount = algorithmic FLOPs (K4) or NVLink bytes (comm phases)."""
         dp = self
 
         class _T:
@@ -296,13 +306,19 @@ class MoEDataPlane:
                 if dp.timing:
                     self.s = torch.cuda.Event(enable_timing=True)
                     self.e = torch.cuda.Event(enable_timing=True)
-                    self.s.record()
+                    self.s.record(stream)
 
             def __exit__(self, *a):
                 if dp.timing:
-                    self.e.record()
-                    dp.gemm_events.append((self.s, self.e, flops, kind))
+                    self.e.record(stream)
+                    dp.gemm_events.append((self.s, self.e, amount, kind))
         return _T()
+
+    def remote_rows(self, m: int) -> tuple[int, int]:
+        """(rows this rank sends to peers, rows peers send to it) in one A2A phase of micro-batch m."""
+        f = self.plan.mbs[m].flow
+        me = self.rank
+        return int(f[me].sum() - f[me, me]), int(f[:, me].sum() - f[me, me])
 
     def real_rows(self, m: int) -> int:
         """Token rows this rank's experts serve in micro-batch m (padding excluded)."""
@@ -431,6 +447,8 @@ class MoEDataPlane:
         if self.pushes:
             self.cps.wait_stream(cs)
             lib = nat.kernels()
+            push_t = self._timed(len(self.pushes) * (self.w1_bytes + self.w2_bytes), "comm_replica_push", self.cps)
+            push_t.__enter__()
             for dst, m, slot, loc in self.pushes:
                 d1 = A.peer_ptr(dst, self.off["w1r"]) + (m * self.slots + slot) * self.w1_bytes
                 d2 = A.peer_ptr(dst, self.off["w2r"]) + (m * self.slots + slot) * self.w2_bytes
@@ -438,10 +456,25 @@ class MoEDataPlane:
                           lib, "replica push")
                 nat.check(lib.mb_memcpy_async(d2, self.W2[loc].data_ptr(), self.w2_bytes, self.cps.cuda_stream),
                           lib, "replica push")
+            push_t.__exit__(None, None, None)
             xs.wait_stream(self.cps)
         ev_comm, ev_comp = {}, {}
 
+        row_b = 2 * h
+
         def dispatch(m):  # D(m): K1 histogram, K2 ranks, K3 scatter into every rank's receive rows
+            with self._timed(self.remote_rows(m)[0] * row_b, "comm_dispatch", xs):
+                _dispatch(m)
+
+        def combine(m):
+            with self._timed(sum(self.remote_rows(m)) * row_b, "comm_combine_dout", xs):
+                _combine(m)
+
+        def unpermute(m):
+            with self._timed(self.remote_rows(m)[0] * row_b, "comm_unpermute", xs):
+                _unpermute(m)
+
+        def _dispatch(m):
             if hooks:
                 hooks.inputs_ready(m, xs)
             self._k("mb_expert_histogram", idx[m].data_ptr(), 1, T, k, E, self.counts[m].data_ptr(),
@@ -458,7 +491,7 @@ class MoEDataPlane:
                     st_x)
             A.barrier(xs)  # rows of micro-batch m have landed everywhere
 
-        def combine(m):  # C(m): K6 gate-weighted combine of Y, then the raw dout rows out (K3)
+        def _combine(m):  # C(m): K6 gate-weighted combine of Y, then the raw dout rows out (K3)
             A.barrier(xs)  # Y of micro-batch m complete on every rank
             self._k("mb_combine_rows", self.ptr_y[m].data_ptr(), self.perm[m].data_ptr(), gates[m].data_ptr(),
                     T, k, h, out[m].data_ptr(), None, None, 1, st_x)
@@ -468,7 +501,7 @@ class MoEDataPlane:
                     self.ptr_dyr[m].data_ptr(), st_x)
             A.barrier(xs)  # dout rows of micro-batch m have landed everywhere
 
-        def unpermute(m):  # X(m): dX un-permute + dgate gather
+        def _unpermute(m):  # X(m): dX un-permute + dgate gather
             A.barrier(xs)  # dX rows / dgate partials of micro-batch m complete everywhere
             self._k("mb_combine_rows", self.ptr_dxp[m].data_ptr(), self.perm[m].data_ptr(), None, T, k, h,
                     dx[m].data_ptr(), self.ptr_dgate[m].data_ptr(), dgate[m].data_ptr(), self.npart, st_x)
@@ -539,12 +572,13 @@ class MoEDataPlane:
         ev.record(cs)
         xs.wait_event(ev)
         if self.world > 1:
-            A.barrier(xs)  # every rank's replica gradients are complete
             mn1, mn2 = 2 * hp * h, h * hp
-            for loc, p1, p2, n in self.reduce:
-                self._k("mb_accumulate_f32", self.gW1[loc].data_ptr(), p1.data_ptr(), n, mn1, st_x)
-                self._k("mb_accumulate_f32", self.gW2[loc].data_ptr(), p2.data_ptr(), n, mn2, st_x)
-            A.barrier(xs)  # peers finished reading our replica gradients (next step may overwrite)
+            with self._timed(sum(n for _, _, _, n in self.reduce) * (mn1 + mn2) * 4, "comm_replica_grad_reduce", xs):
+                A.barrier(xs)  # every rank's replica gradients are complete
+                for loc, p1, p2, n in self.reduce:
+                    self._k("mb_accumulate_f32", self.gW1[loc].data_ptr(), p1.data_ptr(), n, mn1, st_x)
+                    self._k("mb_accumulate_f32", self.gW2[loc].data_ptr(), p2.data_ptr(), n, mn2, st_x)
+                A.barrier(xs)  # peers finished reading our replica gradients (next step may overwrite)
         cs.wait_stream(xs)
 
     def _wgrad(self):
