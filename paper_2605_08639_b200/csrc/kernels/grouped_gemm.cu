@@ -1,5 +1,6 @@
 // Host launcher + C-ABI for the K4 tcgen05 grouped GEMM (grouped_gemm.cuh: 1-CTA 128xBN
 // tiles; grouped_gemm_pair.cuh: CTA-pair 256x256 tiles, the default when the shape allows).
+#include <cstdio>
 #include <cstdlib>
 
 #include "grouped_gemm_pair.cuh"
@@ -32,8 +33,29 @@ static int launch_pair(const GemmParams& p, cudaStream_t stream) {
     attr_set = true;
   }
   const int grid = gemm_sms() & ~1;
-  kern<<<grid, 320, PairCfg<kEpi>::kSmemBytes, stream>>>(p);
+  static unsigned long long* prof = nullptr;
+#ifdef MB_GEMM_PROFILE
+  const bool profile = std::getenv("MB_GEMM_PROF") != nullptr;
+#else
+  const bool profile = false;
+#endif
+  GemmParams q = p;
+  if (profile) {
+    if (!prof) MB_CUDA_TRY(cudaMalloc(&prof, 8 * sizeof(unsigned long long)));
+    MB_CUDA_TRY(cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), stream));
+    q.prof = prof;
+  }
+  kern<<<grid, 320, PairCfg<kEpi>::kSmemBytes, stream>>>(q);
   MB_CUDA_TRY(cudaGetLastError());
+  if (profile) {  // profiling only: synchronous readback, per-cluster averages in cycles
+    unsigned long long h[8];
+    MB_CUDA_TRY(cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    MB_CUDA_TRY(cudaStreamSynchronize(stream));
+    const double n = grid / 2;
+    std::fprintf(stderr, "[gemm-prof] epi=%d W=%d kernel=%.0f producer_wait_empty=%.0f mma_wait_full=%.0f "
+                 "mma_wait_tempty=%.0f epi_wait_tfull=%.0f cycles/cluster\n", kEpi, (int)kW, h[4] / n, h[0] / n,
+                 h[1] / n, h[2] / n, h[3] / n);
+  }
   return MB_OK;
 }
 

@@ -100,6 +100,7 @@ struct GemmParams {
   int64_t ld_aux;
   const float* rscale;  // per-row scale (gate) for EPI_DSWIGLU_GATED
   float* rpart;         // per-row partial sums [rows][N/64] for EPI_DSWIGLU_GATED
+  unsigned long long* prof;  // optional wait-cycle counters (MB_GEMM_PROF): producer/MMA/epilogue
   int debug;            // bit0: skip the epilogue (TMEM drained, nothing stored) -- profiling only
 };
 

@@ -196,6 +196,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total_tiles = tile_start[ng];
+#ifdef MB_GEMM_PROFILE
+  constexpr bool kProf = true;   // build with -DMB_GEMM_PROFILE: per-role wait-cycle counters
+#else
+  constexpr bool kProf = false;
+#endif
+  long long w_empty = 0, w_full = 0, w_tempty = 0, w_tfull = 0;
+  const long long t_kernel0 = kProf ? clock64() : 0;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
@@ -213,7 +220,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         for (int kb = 0; kb < tc.kblocks; ++kb) {
           int nk16 = BK / 16;
           const int krow = kW ? kw.step(nk16) : 0;
-          mbar_wait(&empty_bar[stage], phase ^ 1);
+          {
+            const long long t0 = kProf ? clock64() : 0;
+            mbar_wait(&empty_bar[stage], phase ^ 1);
+            if (kProf) w_empty += clock64() - t0;
+          }
           const uint32_t lbar = mapa_shared(smem_u32(&full_bar[stage]), 0);
           if (leader) mbar_arrive_expect_tx(&full_bar[stage], bytes);
           uint8_t* a_dst = sA + stage * Cfg::kABytes;
@@ -259,7 +270,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       for (int t = cluster; t < total_tiles; t += nclusters, ++it) {
         const TileCoord tc = decode_tile_pair<kW>(t, tile_start, sg, ng, p);
         const int acc = it & 1;
-        mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
+        {
+          const long long t0 = kProf ? clock64() : 0;
+          mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
+          if (kProf) w_tempty += clock64() - t0;
+        }
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * 256;
         const GemmGroup gg = sg[tc.g];
@@ -268,7 +283,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         for (int kb = 0; kb < tc.kblocks; ++kb) {
           int nk16 = BK / 16;
           if (kW) kw.step(nk16);
-          mbar_wait(&full_bar[stage], phase);
+          {
+            const long long t0 = kProf ? clock64() : 0;
+            mbar_wait(&full_bar[stage], phase);
+            if (kProf) w_full += clock64() - t0;
+          }
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * Cfg::kABytes);
           const uint32_t b_addr = smem_u32(sB + stage * Cfg::kBBytes);
@@ -315,7 +334,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       const TileCoord tc = decode_tile_pair<kW>(t, tile_start, sg, ng, p);
       const GemmGroup gg = sg[tc.g];
       const int acc = it & 1;
-      mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
+      {
+        const long long t0 = kProf ? clock64() : 0;
+        mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
+        if (kProf) w_tfull += clock64() - t0;
+      }
       tc_fence_after();
       const uint32_t t_acc = tmem_base + lane_off + acc * 256;
       // full tile: this warp owns rows q*32.. of the CTA's 128 and columns [ch2*128, +128);
@@ -512,6 +535,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     }
     if (lane == 0) bulk_wait<0>();  // every TMA store of this warp has completed
     __syncwarp();
+  }
+  if (kProf && p.prof && lane == 0 && leader) {
+    if (warp == 0) { atomicAdd(&p.prof[0], (unsigned long long)w_empty); atomicAdd(&p.prof[4], (unsigned long long)(clock64() - t_kernel0)); }
+    if (warp == 1) { atomicAdd(&p.prof[1], (unsigned long long)w_full); atomicAdd(&p.prof[2], (unsigned long long)w_tempty); }
+    if (warp == 2) atomicAdd(&p.prof[3], (unsigned long long)w_tfull);
   }
   tc_fence_before();
   __syncthreads();

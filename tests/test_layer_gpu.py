@@ -43,7 +43,8 @@ def _run(name, T, MB, zipf_s=1.0, balanced=False):
     return shape, routing, plan, dp, (wg, wu, wd), (x, dout, idx, gates), (out, dx, dgate)
 
 
-@pytest.mark.parametrize("name,T,MB", [("tiny", 256, 2), ("qwen3-30b-a3b", 512, 2)])
+@pytest.mark.parametrize("name,T,MB", [("tiny", 256, 2), ("qwen3-30b-a3b", 512, 2), ("mixtral-8x7b", 256, 1),
+                                       ("qwen3-235b-a22b", 256, 1)])
 def test_layer_step_matches_oracle(name, T, MB):
     shape, routing, plan, dp, (wg, wu, wd), (x, dout, idx, gates), (out, dx, dgate) = _run(name, T, MB)
     E = shape.num_experts
