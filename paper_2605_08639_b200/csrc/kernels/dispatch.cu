@@ -14,6 +14,8 @@
 //   row_base is fixed by the receive layout of the destination GPU: slots (home experts
 //   ascending, then replicated experts ascending) x source GPU ascending x rank, each slot padded
 //   to a multiple of 128 rows (the GEMM M tile).
+#include <cstdlib>
+
 #include "capi_common.cuh"
 #include "sm100_ptx.cuh"
 #include "../../../include/mb_kernels.h"
@@ -281,9 +283,24 @@ __global__ void __launch_bounds__(256) accumulate_f32_kernel(float4* __restrict_
   }
 }
 
+// Row-moving kernels run concurrently with the persistent GEMM.  comm_smem() > 0 reserves that
+// much dynamic shared memory per block so the blocks cannot co-reside with a GEMM CTA (they
+// stay on the SMs the GEMM leaves free); comm_grid() caps the grid (experiment knobs:
+// MB_COMM_SMEM, MB_COMM_GRID).
+inline int comm_smem() {
+  static int v = -1;
+  if (v < 0) { const char* e = std::getenv("MB_COMM_SMEM"); v = e ? std::atoi(e) : 0; }
+  return v;
+}
+inline int64_t comm_grid() {
+  static int64_t v = -1;
+  if (v < 0) { const char* e = std::getenv("MB_COMM_GRID"); v = e ? std::atoll(e) : 0; }
+  return v;
+}
+
 inline int grid_for(int64_t work_items, int per_block) {
   int64_t g = (work_items + per_block - 1) / per_block;
-  const int64_t cap = static_cast<int64_t>(device_sm_count()) * 8;
+  const int64_t cap = comm_grid() > 0 ? comm_grid() : static_cast<int64_t>(device_sm_count()) * 8;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return static_cast<int>(g);
@@ -330,11 +347,11 @@ extern "C" int mb_scatter_rows(const void* x, int64_t T, int32_t k, int32_t h, c
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int vrow = h / 8;
   if (vrow <= 64)
-    scatter_rows_kernel<2><<<grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(x), T, k, h, reinterpret_cast<const int2*>(perm), dst_rows);
+    scatter_rows_kernel<2><<<grid, 256, comm_smem(), s>>>(reinterpret_cast<const uint4*>(x), T, k, h, reinterpret_cast<const int2*>(perm), dst_rows);
   else if (vrow <= 128)
-    scatter_rows_kernel<4><<<grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(x), T, k, h, reinterpret_cast<const int2*>(perm), dst_rows);
+    scatter_rows_kernel<4><<<grid, 256, comm_smem(), s>>>(reinterpret_cast<const uint4*>(x), T, k, h, reinterpret_cast<const int2*>(perm), dst_rows);
   else
-    scatter_rows_kernel<8><<<grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(x), T, k, h, reinterpret_cast<const int2*>(perm), dst_rows);
+    scatter_rows_kernel<8><<<grid, 256, comm_smem(), s>>>(reinterpret_cast<const uint4*>(x), T, k, h, reinterpret_cast<const int2*>(perm), dst_rows);
   MB_CUDA_TRY(cudaGetLastError());
   return MB_OK;
 }
@@ -352,11 +369,11 @@ extern "C" int mb_combine_rows(const void* const* src_rows, const int32_t* perm,
   const int2* pr = reinterpret_cast<const int2*>(perm);
   uint4* o = reinterpret_cast<uint4*>(out);
   if (vrow <= 64)
-    combine_rows_kernel<2><<<grid, 256, 0, s>>>(src_rows, pr, gate, T, k, h, o, src_scalar, scalar_out, npart);
+    combine_rows_kernel<2><<<grid, 256, comm_smem(), s>>>(src_rows, pr, gate, T, k, h, o, src_scalar, scalar_out, npart);
   else if (vrow <= 128)
-    combine_rows_kernel<4><<<grid, 256, 0, s>>>(src_rows, pr, gate, T, k, h, o, src_scalar, scalar_out, npart);
+    combine_rows_kernel<4><<<grid, 256, comm_smem(), s>>>(src_rows, pr, gate, T, k, h, o, src_scalar, scalar_out, npart);
   else
-    combine_rows_kernel<8><<<grid, 256, 0, s>>>(src_rows, pr, gate, T, k, h, o, src_scalar, scalar_out, npart);
+    combine_rows_kernel<8><<<grid, 256, comm_smem(), s>>>(src_rows, pr, gate, T, k, h, o, src_scalar, scalar_out, npart);
   MB_CUDA_TRY(cudaGetLastError());
   return MB_OK;
 }

@@ -154,6 +154,23 @@ def build_step_plan(policy: str, mats: np.ndarray, topo: ClusterTopology, model:
     return plan
 
 
+def migration_moves(old_home: np.ndarray, new_home: np.ndarray, world: int) -> list:
+    """Per rank: [(new local slot, source rank, source local slot)] for every expert of its new
+    home set.  Local slots order a rank's home experts ascending (as the receive layout does);
+    an expert that stays on its rank may still change slot."""
+    old_home, new_home = np.asarray(old_home), np.asarray(new_home)
+    if old_home.shape != new_home.shape:
+        raise ValueError("old and new assignments cover different expert counts")
+    old_slot = {}
+    for g in range(world):
+        for s, e in enumerate(np.flatnonzero(old_home == g)):
+            old_slot[int(e)] = s
+    out = []
+    for d in range(world):
+        out.append([(s, int(old_home[e]), old_slot[int(e)]) for s, e in enumerate(np.flatnonzero(new_home == d))])
+    return out
+
+
 def gather_routing(comm: Comm, local_counts: np.ndarray) -> np.ndarray:
     """(MB, E) expert counts of this rank (the K1 histogram rows) -> (MB, G, E) of every rank,
     i.e. RoutingTrace.matrices[:, layer] (routing.py:151-168) assembled across processes."""
@@ -224,7 +241,11 @@ class MoEDataPlane:
     fp32 gradients, per-micro-batch receive/activation buffers and the step tables."""
 
     def __init__(self, comm: Comm, shape: LayerShape, tokens: int, micro_batches: int, plan: StepPlan,
-                 device: torch.device | None = None, comm_sms: int | None = None):
+                 device: torch.device | None = None, comm_sms: int | None = None,
+                 expert_state: dict | None = None, rows_cap: int = 0):
+        """expert_state: optional per-expert tensors that follow their expert when the reorder
+        plan migrates it (e.g. optimizer moments): {name: (per-expert shape, torch dtype)}.
+        rows_cap: receive rows per micro-batch to allocate (>= every plan this layer will load)."""
         shape.check()
         self.comm, self.shape, self.T, self.MB = comm, shape, tokens, micro_batches
         self.rank, self.world = comm.rank, comm.world
@@ -238,7 +259,7 @@ class MoEDataPlane:
         if E % self.world:
             raise ValueError(f"{E} experts not divisible by {self.world} GPUs")
         self.M = E // self.world
-        self.R = plan.rows_cap
+        self.R = max(plan.rows_cap, (rows_cap + PAD - 1) // PAD * PAD)
         self.slots = max(plan.slots, 1)
         self.rep_cap = max(1, self.slots * micro_batches)
         bf, f4 = 2, 4
@@ -251,9 +272,18 @@ class MoEDataPlane:
             "xr": MB * R * h * bf, "y": MB * R * h * bf, "dyr": MB * R * h * bf, "dxp": MB * R * h * bf,
             "gate_r": MB * R * f4, "dgate_r": MB * R * self.npart * f4,
             "w1r": MB * self.slots * self.w1_bytes, "w2r": MB * self.slots * self.w2_bytes,
+            # home-expert weights, fp32 gradients and expert state live in two banks: a migration
+            # (new reorder plan) pulls every new home expert into the idle bank, then swaps
             "w1": self.M * self.w1_bytes, "w2": self.M * self.w2_bytes,
             "gw1": S * 2 * hp * h * f4, "gw2": S * h * hp * f4,
+            "w1b": self.M * self.w1_bytes, "w2b": self.M * self.w2_bytes,
+            "gw1b": S * 2 * hp * h * f4, "gw2b": S * h * hp * f4,
         }
+        self.state_spec = {}
+        for name, (eshape, dtype) in (expert_state or {}).items():
+            nbytes = int(np.prod(eshape)) * torch.empty((), dtype=dtype).element_size()
+            self.state_spec[name] = (tuple(eshape), dtype, nbytes)
+            sizes["st_" + name] = sizes["st_" + name + "b"] = self.M * nbytes
         total = sum((v + 1023) // 1024 * 1024 for v in sizes.values()) + 1024 * len(sizes)
         self.arena = SymmetricArena(comm, total, self.device)
         self.off = {key: self.arena.alloc(v) for key, v in sizes.items()}
@@ -266,10 +296,9 @@ class MoEDataPlane:
         self.dgate_r = A.local(self.off["dgate_r"], (MB, R, self.npart), torch.float32)
         self.W1r = A.local(self.off["w1r"], (MB, self.slots, 2 * hp, h), torch.bfloat16)
         self.W2r = A.local(self.off["w2r"], (MB, self.slots, h, hp), torch.bfloat16)
-        self.W1 = A.local(self.off["w1"], (self.M, 2 * hp, h), torch.bfloat16)
-        self.W2 = A.local(self.off["w2"], (self.M, h, hp), torch.bfloat16)
-        self.gW1 = A.local(self.off["gw1"], (S, 2 * hp, h), torch.float32)
-        self.gW2 = A.local(self.off["gw2"], (S, h, hp), torch.float32)
+        self.S = S
+        self.bank = 0
+        self._bind_bank()
         # ---- local activations
         self.H = torch.empty((MB, R, 2 * hp), dtype=torch.bfloat16, device=self.device)
         self.Act = torch.empty((MB, R, hp), dtype=torch.bfloat16, device=self.device)
@@ -409,12 +438,66 @@ class MoEDataPlane:
             srcs = [(p, plan.rep_experts[p].index(int(ex))) for p in range(self.world)
                     if p != d and int(ex) in plan.rep_experts[p] and rep_rows.get((p, int(ex)), 0) > 0]
             if srcs:
-                p1 = [self.arena.peer_ptr(p, self.off["gw1"]) + (self.M + q) * mn1 * 4 for p, q in srcs]
-                p2 = [self.arena.peer_ptr(p, self.off["gw2"]) + (self.M + q) * (mn1 // 2) * 4 for p, q in srcs]
+                p1 = [self.arena.peer_ptr(p, self.off_w["gw1"]) + (self.M + q) * mn1 * 4 for p, q in srcs]
+                p2 = [self.arena.peer_ptr(p, self.off_w["gw2"]) + (self.M + q) * (mn1 // 2) * 4 for p, q in srcs]
                 self.reduce.append((loc, torch.tensor(p1, dtype=torch.int64, device=dev),
                                     torch.tensor(p2, dtype=torch.int64, device=dev), len(srcs)))
 
     # ------------------------------------------------------------------ weights
+    def _bind_bank(self) -> None:
+        """Views of the current bank: W1/W2, fp32 gradients gW1/gW2, expert state."""
+        sfx = "b" if self.bank else ""
+        h, hp, A = self.shape.hidden, self.shape.ffn, self.arena
+        self.off_w = {k: self.off[k + sfx] for k in ("w1", "w2", "gw1", "gw2")}
+        self.W1 = A.local(self.off_w["w1"], (self.M, 2 * hp, h), torch.bfloat16)
+        self.W2 = A.local(self.off_w["w2"], (self.M, h, hp), torch.bfloat16)
+        self.gW1 = A.local(self.off_w["gw1"], (self.S, 2 * hp, h), torch.float32)
+        self.gW2 = A.local(self.off_w["gw2"], (self.S, h, hp), torch.float32)
+        self.state = {}
+        for name, (eshape, dtype, _) in self.state_spec.items():
+            off = self.off["st_" + name + sfx]
+            self.off_w["st_" + name] = off
+            self.state[name] = A.local(off, (self.M, *eshape), dtype)
+
+    def migrate(self, plan: StepPlan, grads: bool = True) -> dict:
+        """Switch to a step plan with a different reorder assignment (expert migration at a batch
+        boundary): every rank pulls its new home experts' weights, fp32
+        gradients and expert state from their old owners (copy engine over NVLink, or a local
+        copy) into its idle bank, then all ranks swap banks and upload the new plan.  Collective:
+        every rank calls it with the same plan.  grads=False skips the fp32 gradients (migration
+        right after an optimizer step, when they are zero: the new bank's are zeroed instead).
+        Returns {experts_moved, bytes_in}."""
+        old_home, new_home = np.asarray(self.plan.home), np.asarray(plan.home)
+        moves = migration_moves(old_home, new_home, self.world)[self.rank]
+        cur = torch.cuda.current_stream()
+        cps, A, lib = self.cps, self.arena, nat.kernels()
+        sfx_new = "" if self.bank else "b"
+        hp, h = self.shape.ffn, self.shape.hidden
+        items = [("w1", self.w1_bytes), ("w2", self.w2_bytes)]
+        if grads:
+            items += [("gw1", 2 * hp * h * 4), ("gw2", h * hp * 4)]
+        items += [("st_" + n, spec[2]) for n, spec in self.state_spec.items()]
+        cps.wait_stream(cur)
+        A.barrier(cps)  # every rank finished its last step: the current banks are stable
+        moved = nbytes = 0
+        for slot, src_rank, src_slot in moves:
+            if src_rank != self.rank:
+                moved += 1
+            for key, size in items:
+                src = A.peer_ptr(src_rank, self.off_w[key]) + src_slot * size
+                dst = A.peer_ptr(self.rank, self.off[key + sfx_new]) + slot * size
+                nat.check(lib.mb_memcpy_async(dst, src, size, cps.cuda_stream), lib, "migrate")
+                if src_rank != self.rank:
+                    nbytes += size
+        A.barrier(cps)  # every pull has landed; the old banks may be reused
+        cur.wait_stream(cps)
+        self.bank ^= 1
+        self._bind_bank()
+        if not grads:
+            self.zero_grads()
+        self.load_plan(plan)
+        return {"experts_moved": moved, "bytes_in": nbytes}
+
     def set_weights(self, w_gate: torch.Tensor, w_up: torch.Tensor, w_down: torch.Tensor) -> None:
         """Home expert weights of this rank (ascending expert id): gate/up [M,h',h], down [M,h,h']."""
         self.W1.copy_(interleave_w1(w_gate, w_up))

@@ -45,3 +45,21 @@ def test_at_most_two_micro_batches_ahead():
     pos = {o: i for i, o in enumerate(comm)}
     for m in range(2, 8):
         assert pos[("C", m - 2)] < pos[("D", m)]
+
+
+def test_migration_moves_cover_every_expert_once():
+    import numpy as np
+    from paper_2605_08639_b200.moe_layer import migration_moves
+    rng = np.random.default_rng(0)
+    world, E = 4, 32
+    old = np.repeat(np.arange(world), E // world)
+    new = rng.permutation(old)
+    moves = migration_moves(old, new, world)
+    seen = []
+    for d, mv in enumerate(moves):
+        assert [s for s, _, _ in mv] == list(range(E // world))
+        for s, src, ss in mv:
+            e = int(np.flatnonzero(new == d)[s])
+            assert old[e] == src and int(np.flatnonzero(old == src)[ss]) == e
+            seen.append(e)
+    assert sorted(seen) == list(range(E))
