@@ -144,14 +144,18 @@ def run_reference(args, rank, world):
 
 # ----------------------------------------------------------------------------- B200 arm
 
-def measure_policy(args, comm, policy, shape, cfg, routing, topo, model, cfgs, want_detail):
+def measure_policy(args, comm, policy, shape, cfg, routing, topo, model, cfgs, want_detail, bundle=None):
     import torch
     from paper_2605_08639_b200.moe_layer import MoEDataPlane, build_step_plan, plan_digest
     from paper_2605_08639_b200.workload import make_activations, make_weights_for
     rank, world = comm.rank, comm.world
     T, MB = args.tokens, args.micro_batches
     t0 = time.perf_counter()
-    plan = build_step_plan(policy, routing.mats, topo, model, topo.profile, cfgs, shape)
+    if bundle is not None:  # plan files (planio.solve / the reference's `solve`)
+        from paper_2605_08639_b200.moe_layer import step_plan_from_bundle
+        plan = step_plan_from_bundle(policy, bundle, routing.mats, shape, layer=args.trace_layer)
+    else:
+        plan = build_step_plan(policy, routing.mats, topo, model, topo.profile, cfgs, shape)
     plan_ms = (time.perf_counter() - t0) * 1e3
     digests = comm.all_gather_object(plan_digest(plan))
     if len(set(digests)) != 1:
@@ -263,15 +267,45 @@ def run_ours(args, comm):
     slots = cfg["slots"] if args.slots is None else args.slots
     cfgs = SimConfigs(anneal=AnnealConfig(seeds=tuple(range(args.sa_chains))), replica=ReplicaConfig(slots),
                       threads=min(8, os.cpu_count() or 1))
+    trace, bundle = None, None
+    if args.trace:
+        # replay a recorded count trace (routing.bin + manifest.json, either implementation):
+        # tokens are realised per (micro-batch, source GPU) row with exactly the recorded counts
+        from paper_2605_08639_b200 import planio
+        from paper_2605_08639_b200.moe_layer import LayerShape
+        from paper_2605_08639_b200.traces import load_trace
+        trace = load_trace(args.trace)
+        if trace.topo.num_gpus != world:
+            raise SystemExit(f"trace has {trace.topo.num_gpus} GPUs, run with --gpus {trace.topo.num_gpus}")
+        if trace.tokens_per_gpu <= 0:
+            raise SystemExit("variable-token traces cannot be replayed on fixed token buffers")
+        tm = trace.model
+        shape = LayerShape(tm.num_experts, tm.top_k, tm.hidden_size, tm.intermediate_size)
+        topo, group = trace.topo, trace.topo.gpus_per_node
+        model = ModelProfile(1, shape.num_experts, shape.top_k, shape.hidden, shape.ffn)
+        cfg = {"shape": shape, "shift": 0, "slots": slots, "group": group}
+        args.tokens, args.micro_batches = trace.tokens_per_gpu, trace.num_micro_batches
+        if args.plans:
+            bundle = planio.load_plan_bundle(args.plans, trace)
     T, MB = args.tokens, args.micro_batches
 
     def routing_for(balanced):
         # each rank draws its own replayed routing, histograms it on the GPU (K1) and all-gathers
         # the counts into the (MB, G, E) trace every planner sees
-        r = make_routing(shape, T, MB, world, rank, zipf_s=args.zipf, shift=cfg["shift"], balanced=balanced,
-                         all_ranks=False)
+        if trace is not None and not balanced:
+            from paper_2605_08639_b200.traces import realize_tokens
+            from paper_2605_08639_b200.workload import Routing
+            rows = [realize_tokens(trace.matrices[m, args.trace_layer, rank], shape.top_k, seed=m * world + rank)
+                    for m in range(MB)]
+            r = Routing(idx=np.stack([a for a, _ in rows]), gates=np.stack([b for _, b in rows]), mats=None)
+        else:
+            r = make_routing(shape, T, MB, world, rank, zipf_s=args.zipf, shift=cfg["shift"], balanced=balanced,
+                             all_ranks=False)
         counts, _ = expert_histogram(torch.from_numpy(r.idx).cuda(), shape.num_experts)
         r.mats = gather_routing(comm, counts.cpu().numpy().astype(np.int64))
+        if trace is not None and not balanced and not np.array_equal(
+                r.mats, trace.matrices[:, args.trace_layer].astype(np.int64)):
+            raise RuntimeError("device histogram of the realised tokens differs from the trace counts")
         return r
 
     skewed = routing_for(False)
@@ -289,7 +323,8 @@ def run_ours(args, comm):
                                           want_detail=False)
             continue
         results[pol] = measure_policy(args, comm, pol, shape, cfg, routing, topo, model, cfgs,
-                                      want_detail=(pol == args.headline))
+                                      want_detail=(pol == args.headline),
+                                      bundle=bundle if pol == "relibra" else None)
     head = results[args.headline]
     tokens_step = world * T * MB
     value = tokens_step / (head["ms"] / 1e3)
@@ -300,7 +335,9 @@ def run_ours(args, comm):
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": head["ms"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"{args.config} MoE layer fwd+bwd, EP={world}, replayed Zipf routing",
+        "config": {"workload": (f"trace {trace.trace_id()} layer {args.trace_layer} MoE layer fwd+bwd, EP={world}"
+                                + (", plans from files" if bundle is not None else "")) if trace is not None
+                   else f"{args.config} MoE layer fwd+bwd, EP={world}, replayed Zipf routing",
                    "experts": shape.num_experts, "top_k": shape.top_k, "hidden": shape.hidden, "ffn": shape.ffn,
                    "tokens_per_gpu": T, "micro_batches": MB, "global_tokens_per_step": tokens_step,
                    "policy": args.headline, "zipf_s": args.zipf, "hot_shift": cfg["shift"], "ep": world,
@@ -325,7 +362,7 @@ def run_ours(args, comm):
         line["balance"]["speedup_vs_static"] = results["static"]["ms"] / head["ms"]
     if "balanced_oracle" in results:
         line["balance"]["frac_of_balanced"] = results["balanced_oracle"]["ms"] / head["ms"]
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and trace is None:
         tps, sample = cpu_reference_sample(args.config, T, world, args.zipf, budget_s=args.cpu_budget,
                                            threads=os.cpu_count() or 1)
         line["cpu_baseline"] = {"value": tps, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
@@ -352,6 +389,11 @@ def main():
     ap.add_argument("--headline", default="relibra")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--trace", default=None, help="replay a recorded routing trace directory (manifest.json + "
+                    "routing.bin) instead of synthetic Zipf routing")
+    ap.add_argument("--trace-layer", type=int, default=0)
+    ap.add_argument("--plans", default=None, help="with --trace: relibra uses the reorder.json / replication.json "
+                    "of this solve output directory instead of planning")
     args = ap.parse_args()
     if args.headline not in args.policies.split(","):
         args.policies = args.headline + "," + args.policies

@@ -21,8 +21,12 @@ from .reordering import (AnnealConfig, ReorderPlan, SamplePlacement, anneal_reor
 from .replication import (InstanceTooLargeError, ReplicaConfig, ReplicaPlacement, ReplicationEntry,
                           ReplicationPlan, SplitPlan, candidate_gpus, greedy_replicate, replica_memory, round_split,
                           solve_token_split_lp, validate_placement, validate_split)
-from .traces import (ModelProfile, RoutingTrace, TraceFormatError, ZipfRouting, aggregate_batch, build_trace,
-                     hot_expert_intersection, skewness, top_k_experts)
+from .traces import (ModelProfile, RoutingTrace, SampleTable, TraceFormatError, ZipfRouting, aggregate_batch,
+                     build_trace, hot_expert_intersection, load_trace, realize_tokens, save_trace, skewness,
+                     top_k_experts)
+from .planio import (PlanFormatError, chain_seeds, load_plan_bundle, load_reorder_plan, load_replication_plan,
+                     replication_plan_from_dict, replication_plan_to_dict, save_reorder_plan, save_replication_plan,
+                     solve)
 from ._native import LPError, NativeLibraryError
 
 __version__ = "0.1.0"

@@ -105,16 +105,26 @@ def build_step_plan(policy: str, mats: np.ndarray, topo: ClusterTopology, model:
     """Plan one step (one batch of MB micro-batches, one layer) from the gathered (MB, G, E)
     routing matrices, with the reference policies (sim.build_policy_bundle, sim.py:214-280).
     'balanced_oracle' is planned like 'static': its token routing must already be uniform."""
-    mbs_n, g, e = mats.shape
     trace = rt.build_trace(model, topo, mats[:, None], tokens_per_gpu=0)
     pol_name = "static" if policy == "balanced_oracle" else policy
     bundle, _ = pol.build_policy_bundle(trace, pol_name, topo, model, hw, cfgs)
-    home = np.asarray(bundle.reorder[0].assignment, dtype=np.int64)
-    plan = StepPlan(policy=policy, shape=shape, world=g, home=home, slots=cfgs.replica.slots_per_gpu)
+    return step_plan_from_bundle(policy, bundle, mats, shape, layer=0, slots=cfgs.replica.slots_per_gpu)
+
+
+def step_plan_from_bundle(policy: str, bundle: pol.PlanBundle, mats: np.ndarray, shape: LayerShape,
+                          layer: int = 0, slots: int = 0) -> StepPlan:
+    """Device tables of one layer's step from a PlanBundle (planned here, or loaded from the
+    reorder.json / replication.json files of planio.solve or the reference's `solve`)."""
+    mbs_n, g, e = mats.shape
+    home = np.asarray(bundle.reorder[layer].assignment, dtype=np.int64)
+    if slots <= 0:  # loaded plans: the largest per-GPU replica count the files use
+        slots = max([0] + [int(ent.placement.slot_usage(g).max())
+                           for (mb, l), ent in bundle.replication.entries.items() if l == layer])
+    plan = StepPlan(policy=policy, shape=shape, world=g, home=home, slots=slots)
     entries = []
     for mb in range(mbs_n):
         x = mats[mb].astype(np.float64)
-        entry = bundle.replication.entries.get((mb, 0))
+        entry = bundle.replication.entries.get((mb, layer))
         if entry is None:
             placement, split = rep.ReplicaPlacement(home=home.copy()), rep.SplitPlan()
         else:
@@ -122,7 +132,8 @@ def build_step_plan(policy: str, mats: np.ndarray, topo: ClusterTopology, model:
         counts = rep.round_split(split, placement, x)
         entries.append((placement, counts))
     plan.maxc = max([1] + [1 + len(p.replicas.get(ex, [])) for p, _ in entries for ex in p.replicas])
-    plan.max_slots = e // g + max(1, cfgs.replica.slots_per_gpu)
+    per_gpu_rep = max([0] + [int(p.slot_usage(g).max()) for p, _ in entries])
+    plan.max_slots = e // g + max(1, slots, per_gpu_rep)
     lib = nat.planner()
     for mb, (placement, counts) in enumerate(entries):
         x = np.ascontiguousarray(mats[mb], dtype=np.int64)

@@ -15,10 +15,11 @@ from __future__ import annotations
 import hashlib
 import json
 from dataclasses import dataclass, field
+from pathlib import Path
 
 import numpy as np
 
-from .cluster import ClusterTopology
+from .cluster import ClusterTopology, HardwareProfile, build_topology
 
 U32_MAX = 2**32 - 1
 DEFAULT_HIDDEN_SIZE = 1024
@@ -58,6 +59,27 @@ class ModelProfile:
         if self.num_experts % topo.num_gpus:
             raise ValueError(f"{self.num_experts} experts not divisible by {topo.num_gpus} GPUs")
         return self.num_experts // topo.num_gpus
+
+
+MANIFEST_VERSION = 1
+MANIFEST_REQUIRED = ("version", "num_layers", "num_experts", "top_k", "num_micro_batches", "num_nodes",
+                     "gpus_per_node", "tokens_per_gpu", "flops_per_gpu", "bw_nvlink_Bps", "bw_rdma_Bps",
+                     "bytes_per_token")
+
+
+@dataclass
+class SampleTable:
+    """Per-sample counts [sample][layer][expert] u32 and each sample's micro-batch, source GPU and
+    token length (routing.py:137-149; samples.bin / samples.json)."""
+
+    counts: np.ndarray
+    micro_batch: np.ndarray
+    source_gpu: np.ndarray
+    tokens: np.ndarray
+
+    @property
+    def num_samples(self) -> int:
+        return int(self.counts.shape[0])
 
 
 @dataclass
@@ -115,6 +137,122 @@ class RoutingTrace:
         if self.tokens_per_gpu > 0 and (sums != self.tokens_per_gpu * self.model.top_k).any():
             raise TraceFormatError(
                 f"row sums do not match tokens_per_gpu * top_k = {self.tokens_per_gpu * self.model.top_k}")
+        if self.samples is not None:
+            self._validate_samples()
+
+    def _validate_samples(self) -> None:
+        """Sample table consistency (routing.py:197-212)."""
+        s = self.samples
+        mb, layers, g, e = self.matrices.shape
+        if s.counts.shape[1:] != (layers, e):
+            raise TraceFormatError("sample counts disagree with trace dimensions")
+        if not (len(s.micro_batch) == len(s.source_gpu) == len(s.tokens) == s.counts.shape[0]):
+            raise TraceFormatError("sample index and sample counts disagree in length")
+        if s.micro_batch.min(initial=0) < 0 or s.micro_batch.max(initial=0) >= mb:
+            raise TraceFormatError("sample micro_batch out of range")
+        if s.source_gpu.min(initial=0) < 0 or s.source_gpu.max(initial=0) >= g:
+            raise TraceFormatError("sample source_gpu out of range")
+        rebuilt = np.zeros((mb, layers, g, e), dtype=np.int64)
+        np.add.at(rebuilt, (s.micro_batch, slice(None), s.source_gpu), s.counts.astype(np.int64))
+        if (rebuilt != self.matrices.astype(np.int64)).any():
+            raise TraceFormatError("per-GPU sums over samples do not reproduce the routing matrices")
+
+
+def save_trace(trace: RoutingTrace, path) -> None:
+    """manifest.json + routing.bin (+ samples.bin / samples.json), byte-compatible with
+    moebalance.routing.save_trace (routing.py:240-256)."""
+    trace.validate()
+    if trace.matrices.max(initial=0) > U32_MAX:
+        raise TraceFormatError("token counts exceed the u32 trace format")
+    out = Path(path)
+    out.mkdir(parents=True, exist_ok=True)
+    (out / "manifest.json").write_text(json.dumps(trace.manifest(), indent=2, sort_keys=True) + "\n")
+    (out / "routing.bin").write_bytes(np.ascontiguousarray(trace.matrices, dtype="<u4").tobytes())
+    if trace.samples is not None:
+        s = trace.samples
+        (out / "samples.bin").write_bytes(np.ascontiguousarray(s.counts, dtype="<u4").tobytes())
+        index = [{"micro_batch": int(s.micro_batch[i]), "source_gpu": int(s.source_gpu[i]),
+                  "tokens": int(s.tokens[i])} for i in range(s.num_samples)]
+        (out / "samples.json").write_text(json.dumps({"samples": index}, indent=2) + "\n")
+
+
+def load_trace(path) -> RoutingTrace:
+    """Read a trace directory written by either implementation (routing.py:259-322), validating
+    every invariant; errors are TraceFormatError (a ValueError) as in the reference."""
+    root = Path(path)
+    mpath = root / "manifest.json"
+    if not mpath.is_file():
+        raise TraceFormatError(f"missing manifest: {mpath}")
+    try:
+        man = json.loads(mpath.read_text())
+    except json.JSONDecodeError as err:
+        raise TraceFormatError(f"malformed manifest: {err}") from err
+    missing = [k for k in MANIFEST_REQUIRED if k not in man]
+    if missing:
+        raise TraceFormatError(f"manifest missing keys: {', '.join(missing)}")
+    if man["version"] != MANIFEST_VERSION:
+        raise TraceFormatError(f"unsupported trace version {man['version']}")
+    model = ModelProfile(num_layers=man["num_layers"], num_experts=man["num_experts"], top_k=man["top_k"],
+                         hidden_size=man.get("hidden_size", DEFAULT_HIDDEN_SIZE),
+                         intermediate_size=man.get("intermediate_size", DEFAULT_INTERMEDIATE_SIZE),
+                         expert_param_bytes=man.get("expert_param_bytes"))
+    topo = build_topology(man["num_nodes"], man["gpus_per_node"],
+                          HardwareProfile(flops_per_gpu=man["flops_per_gpu"], bw_nvlink=man["bw_nvlink_Bps"],
+                                          bw_rdma=man["bw_rdma_Bps"], bytes_per_token=man["bytes_per_token"]))
+    shape = (man["num_micro_batches"], model.num_layers, topo.num_gpus, model.num_experts)
+    bpath = root / "routing.bin"
+    if not bpath.is_file():
+        raise TraceFormatError(f"missing routing.bin in {root}")
+    payload = bpath.read_bytes()
+    expected = int(np.prod(shape)) * 4
+    if len(payload) != expected:
+        raise TraceFormatError(f"routing.bin holds {len(payload)} bytes, manifest implies {expected}")
+    matrices = np.frombuffer(payload, dtype="<u4").reshape(shape).copy()
+    samples = _load_samples(root, shape) if man.get("has_samples") else None
+    trace = RoutingTrace(model=model, topo=topo, matrices=matrices, tokens_per_gpu=man["tokens_per_gpu"],
+                         samples=samples, generator=man.get("generator", {}))
+    trace.validate()
+    return trace
+
+
+def _load_samples(root: Path, shape: tuple) -> SampleTable:
+    bpath, ipath = root / "samples.bin", root / "samples.json"
+    if not bpath.is_file() or not ipath.is_file():
+        raise TraceFormatError("manifest declares samples but sample files are missing")
+    index = json.loads(ipath.read_text())["samples"]
+    _, layers, _, experts = shape
+    payload = bpath.read_bytes()
+    expected = len(index) * layers * experts * 4
+    if len(payload) != expected:
+        raise TraceFormatError(f"samples.bin holds {len(payload)} bytes, index implies {expected}")
+    counts = np.frombuffer(payload, dtype="<u4").reshape(len(index), layers, experts).copy()
+    return SampleTable(counts=counts, micro_batch=np.array([s["micro_batch"] for s in index], dtype=np.int32),
+                       source_gpu=np.array([s["source_gpu"] for s in index], dtype=np.int32),
+                       tokens=np.array([s["tokens"] for s in index], dtype=np.int32))
+
+
+def realize_tokens(counts: np.ndarray, top_k: int, seed: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    """Token-level routing for one (micro-batch, layer, source GPU) count row of a recorded trace:
+    idx [T, k] int32 whose np.bincount equals `counts` exactly, each token with k distinct experts,
+    and softmax gates [T, k] float32.  Expert ids are laid out count-descending and dealt
+    column-major over the T x k grid (a run of c <= T ids never lands twice in one row); the
+    rows are then shuffled with `seed`.  Lets count traces (routing.bin) drive the data plane."""
+    counts = np.asarray(counts, dtype=np.int64)
+    total = int(counts.sum())
+    if total % top_k:
+        raise TraceFormatError("row sum is not divisible by top_k")
+    T = total // top_k
+    if counts.max(initial=0) > T:
+        raise TraceFormatError("an expert count exceeds the token count: no distinct top-k realisation")
+    order = np.argsort(-counts, kind="stable")
+    ids = np.repeat(order, counts[order]).astype(np.int32)
+    idx = ids.reshape(top_k, T).T.copy()
+    rng = np.random.default_rng(seed)
+    idx = idx[rng.permutation(T)]
+    logits = rng.standard_normal((T, top_k)).astype(np.float32)
+    gates = np.exp(logits - logits.max(axis=1, keepdims=True))
+    gates = (gates / gates.sum(axis=1, keepdims=True)).astype(np.float32)
+    return np.ascontiguousarray(idx), gates
 
 
 def aggregate_batch(trace: RoutingTrace, layer: int) -> np.ndarray:
