@@ -206,6 +206,7 @@ def measure_policy(args, comm, policy, shape, cfg, routing, topo, model, cfgs, w
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_max = float(t.item())
     res = {"ms": ms_max, "plan_ms": plan_ms, "skew": plan.skew(), "launches": launches,
+           "predicted_ms": plan.predicted_ms(topo, model, topo.profile),
            "rows": [dp.real_rows(m) for m in range(MB)], "rows_cap": plan.rows_cap}
     if want_detail:
         gev = [ev for ev in dp.gemm_events if not ev[3].startswith("comm_")]
@@ -356,7 +357,8 @@ def run_ours(args, comm):
         "gpu_launches": head["launches"],
         "clocks": head["clocks"],
         "balance": {p: {"tokens_per_s": tokens_step / (r["ms"] / 1e3), "ms_per_step": r["ms"], "skew": r["skew"],
-                        "planner_ms": r["plan_ms"]} for p, r in results.items()},
+                        "planner_ms": r["plan_ms"], "model_predicted_ms": round(r["predicted_ms"], 4)}
+                    for p, r in results.items()},
     }
     if "static" in results:
         line["balance"]["speedup_vs_static"] = results["static"]["ms"] / head["ms"]

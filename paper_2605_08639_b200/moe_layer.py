@@ -86,6 +86,24 @@ class StepPlan:
     rows_cap: int = PAD
     rep_experts: list = field(default_factory=list)   # per GPU: sorted experts replicated onto it this step
     slots: int = 0
+    mats: np.ndarray | None = None  # (MB, G, E) routing counts the plan was built for
+
+    def predicted_ms(self, topo: ClusterTopology, model: rt.ModelProfile, hw: HardwareProfile) -> float:
+        """The reference cost model's time for this step (sum over micro-batches of
+        costmodel.moe_time, costmodel.py:205-213) with the executed integer splits, for
+        predicted-vs-measured reporting (sim.evaluate_bundle, sim.py:64-110)."""
+        from . import loads as cm
+        total = 0.0
+        for m, mbp in enumerate(self.mbs):
+            x = self.mats[m].astype(np.float64)
+            splits = {}
+            for e, cnt in mbp.counts.items():
+                col = x[:, e][:, None]
+                frac = np.divide(cnt, col, out=np.zeros_like(cnt, dtype=np.float64), where=col > 0)
+                frac[x[:, e] == 0, 0] = 1.0
+                splits[e] = (np.array(mbp.placement.copies(e)), frac)
+            total += cm.moe_time(cm.compute_loads(x, mbp.placement.home, topo, splits=splits), model, hw).t_moe
+        return total * 1e3
 
     def executed_loads(self) -> np.ndarray:
         """(MB, G) GEMM rows per GPU actually executed (= costmodel comp with integer splits)."""
@@ -120,7 +138,7 @@ def step_plan_from_bundle(policy: str, bundle: pol.PlanBundle, mats: np.ndarray,
     if slots <= 0:  # loaded plans: the largest per-GPU replica count the files use
         slots = max([0] + [int(ent.placement.slot_usage(g).max())
                            for (mb, l), ent in bundle.replication.entries.items() if l == layer])
-    plan = StepPlan(policy=policy, shape=shape, world=g, home=home, slots=slots)
+    plan = StepPlan(policy=policy, shape=shape, world=g, home=home, slots=slots, mats=np.asarray(mats))
     entries = []
     for mb in range(mbs_n):
         x = mats[mb].astype(np.float64)
