@@ -42,6 +42,28 @@ def load_peaks():
         return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
 
 
+K4_TRAFFIC = os.path.join(ROOT, "profiles", "r01_launches_step_summary.json")
+
+
+def k4_traffic_per_step(config: str, world: int, tokens: int, mbs: int):
+    """DRAM bytes (read + write) of every K4 launch of one step, from the committed ncu launch
+    list of this same bench command (dram__bytes_read.sum + dram__bytes_write.sum per launch);
+    None for other configurations (no capture)."""
+    if (config, world, tokens, mbs) != ("qwen3-30b-a3b", 1, 8192, 8):
+        return None
+    try:
+        rows = json.load(open(K4_TRAFFIC))
+    except (OSError, ValueError):
+        return None
+    total = 0.0
+    for key, r in rows.items():
+        if not key.startswith("K4"):
+            continue
+        per_step = 2 if key.endswith("<1, 1, 1, 3>") else mbs   # wgrad: 2 launches per step
+        total += (r["dram_read_per_launch"] + r["dram_write_per_launch"]) * per_step
+    return total
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled every 50 ms while the timed region runs."""
 
@@ -346,7 +368,11 @@ def run_ours(args, comm):
                    "l2": "inputs larger than L2 (per-step working set >> 126 MB)"},
         "roofline": {"kernel": "K4 tcgen05 grouped GEMM (all fwd/dgrad/wgrad launches of the step)",
                      "bound": "tensor", "achieved": round(gemm_tflops, 1), "peak": peak_tf, "unit": "TFLOP/s",
-                     "frac": round(gemm_tflops / peak_tf, 4), "traffic": None,
+                     "frac": round(gemm_tflops / peak_tf, 4),
+                     "traffic": (None if trace is not None else
+                                 k4_traffic_per_step(args.config, world, args.tokens, args.micro_batches)),
+                     "traffic_unit": "DRAM bytes per step over all K4 launches (ncu, profiles/"
+                                     "r01_launches_step_summary.json)",
                      "peak_source": f"bf16_tflops_sustained, {peak_src}",
                      "flops_per_step": head["gemm_flop"], "gemm_ms_per_step": round(head["gemm_ms"], 4),
                      "gemm_share_of_step": round(head["gemm_ms"] / head["ms"], 4),
