@@ -142,6 +142,21 @@ def cpu_reference_sample(cfg_name: str, tokens: int, world: int, zipf: float, bu
     return tps, f"{done_tokens} tokens of {cfg_name} (1 GPU's share), fp32 torch CPU fwd+bwd + bincount, {elapsed:.1f}s"
 
 
+def synthetic_config(args, world):
+    """The `config` object of a synthetic-routing run (both arms print the same one)."""
+    from paper_2605_08639_b200.workload import SHAPES
+    cfg = SHAPES[args.config]
+    shape = cfg["shape"]
+    return {"workload": f"{args.config} MoE layer fwd+bwd, EP={world}, replayed Zipf routing",
+            "experts": shape.num_experts, "top_k": shape.top_k, "hidden": shape.hidden, "ffn": shape.ffn,
+            "tokens_per_gpu": args.tokens, "micro_batches": args.micro_batches,
+            "global_tokens_per_step": world * args.tokens * args.micro_batches, "policy": args.headline,
+            "zipf_s": args.zipf, "hot_shift": cfg["shift"], "ep": world,
+            "gpu_group": min(world, args.group or cfg["group"]),
+            "replica_slots": cfg["slots"] if args.slots is None else args.slots, "sa_chains": args.sa_chains,
+            "l2": "inputs larger than L2 (per-step working set >> 126 MB)"}
+
+
 def run_reference(args, rank, world):
     import torch
     if rank != 0:
@@ -158,7 +173,7 @@ def run_reference(args, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config} MoE layer (CPU reference arm)", "tokens_per_gpu": args.tokens},
+            "config": synthetic_config(args, world),
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -358,14 +373,13 @@ def run_ours(args, comm):
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": head["ms"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": (f"trace {trace.trace_id()} layer {args.trace_layer} MoE layer fwd+bwd, EP={world}"
-                                + (", plans from files" if bundle is not None else "")) if trace is not None
-                   else f"{args.config} MoE layer fwd+bwd, EP={world}, replayed Zipf routing",
-                   "experts": shape.num_experts, "top_k": shape.top_k, "hidden": shape.hidden, "ffn": shape.ffn,
-                   "tokens_per_gpu": T, "micro_batches": MB, "global_tokens_per_step": tokens_step,
-                   "policy": args.headline, "zipf_s": args.zipf, "hot_shift": cfg["shift"], "ep": world,
-                   "gpu_group": group, "replica_slots": slots, "sa_chains": args.sa_chains,
-                   "l2": "inputs larger than L2 (per-step working set >> 126 MB)"},
+        "config": synthetic_config(args, world) if trace is None else {
+            "workload": (f"trace {trace.trace_id()} layer {args.trace_layer} MoE layer fwd+bwd, EP={world}"
+                         + (", plans from files" if bundle is not None else "")),
+            "experts": shape.num_experts, "top_k": shape.top_k, "hidden": shape.hidden, "ffn": shape.ffn,
+            "tokens_per_gpu": T, "micro_batches": MB, "global_tokens_per_step": tokens_step,
+            "policy": args.headline, "ep": world, "gpu_group": group, "replica_slots": slots,
+            "sa_chains": args.sa_chains, "l2": "inputs larger than L2 (per-step working set >> 126 MB)"},
         "roofline": {"kernel": "K4 tcgen05 grouped GEMM (all fwd/dgrad/wgrad launches of the step)",
                      "bound": "tensor", "achieved": round(gemm_tflops, 1), "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": round(gemm_tflops / peak_tf, 4),
