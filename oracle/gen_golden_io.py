@@ -9,6 +9,7 @@ files from the same trace.
 
 Run in the build container (needs /root/reference):
     PYTHONDONTWRITEBYTECODE=1 python oracle/gen_golden_io.py
+    PYTHONDONTWRITEBYTECODE=1 python oracle/gen_golden_io.py --acceptance   (criteria 6/7 study, ~5 min)
 """
 
 import json
@@ -32,9 +33,10 @@ def main():
     from moebalance import cli  # noqa: E402
     from moebalance import routing as rt  # noqa: E402
 
-    if OUT.exists():
-        shutil.rmtree(OUT)
-    OUT.mkdir(parents=True)
+    OUT.mkdir(parents=True, exist_ok=True)
+    for name in CASES:  # the acceptance/ study is regenerated separately (--acceptance)
+        if (OUT / name).exists():
+            shutil.rmtree(OUT / name)
     meta = {}
     for name, (nodes, gpn, e, layers, mb, k, tok, dom, alpha, focus, spg, seed, seeds, slots) in CASES.items():
         tdir, pdir = OUT / name / "trace", OUT / name / "plans"
@@ -53,5 +55,47 @@ def main():
     print(f"wrote {OUT}")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--acceptance" not in sys.argv:
     main()
+
+
+def acceptance_study():
+    """Criteria 6/7 of the reference's acceptance suite (test_acceptance.py:289-368) at EP 8..64:
+    the reference generates the traces and runs run_baseline for every policy; the traces and the
+    exact per-policy results (total time as float.hex, per-micro-batch skew) are written to
+    tests/golden/io/acceptance/ so tests/test_acceptance_golden.py can replay them with this
+    package's planners."""
+    sys.path.insert(0, REF)
+    import numpy as np
+    from moebalance import replicate as rep
+    from moebalance import reorder as ro
+    from moebalance import routing as rt
+    from moebalance import sim
+    from moebalance.topology import HardwareProfile, build_topology
+
+    out = OUT / "acceptance"
+    out.mkdir(parents=True, exist_ok=True)
+    cfgs = sim.SimConfigs(anneal=ro.AnnealConfig(seeds=tuple(range(8)), cooling_rate=0.9995),
+                          replica=rep.ReplicaConfig(1), threads=2)
+    results = {}
+    for ep in (8, 16, 32, 64):
+        hw = HardwareProfile(2.577e10, 4.5e5, 2.5e4, 1.0)
+        topo = build_topology(max(ep // 8, 1), min(ep, 8), hw)
+        model = rt.ModelProfile(num_layers=1, num_experts=128, top_k=8)
+        spec = rt.TraceGenSpec(num_domains=3, dirichlet_alpha=4096.0, tokens_per_gpu=1024, rng_seed=11,
+                               domain_focus=0.82, redraw_concentration=64.0)
+        trace = rt.generate_synthetic_trace(spec, model, topo, 32)
+        rt.save_trace(trace, out / f"ep{ep}")
+        policies = ("static", "relibra") + (("lpt_only", "eplb_like", "lplb_like", "balanced_oracle")
+                                             if ep == 32 else ())
+        res = {}
+        for pol in policies:
+            r = sim.run_baseline(trace, pol, topo, model, hw, cfgs)
+            res[pol] = {"total_time": float(r.total_time).hex(), "skew": [float(v).hex() for v in r.skew.ravel()]}
+        results[f"ep{ep}"] = res
+        print(f"acceptance ep{ep} done", flush=True)
+    (out / "results.json").write_text(json.dumps(results, indent=1, sort_keys=True) + "\n")
+
+
+if __name__ == "__main__" and "--acceptance" in sys.argv:
+    acceptance_study()
