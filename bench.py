@@ -69,7 +69,7 @@ class ClockSampler:
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_power_cap,power.limit")
 
     def __init__(self, gpu: int):
         self.gpu = gpu
@@ -107,8 +107,11 @@ class ClockSampler:
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        pw = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        pl = [float(s[7]) for s in self.samples if len(s) > 7 and s[7].replace(".", "").isdigit()]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "power_w": statistics.median(pw) if pw else None, "power_limit_w": max(pl) if pl else None}
 
 
 # ----------------------------------------------------------------------------- CPU reference arm
