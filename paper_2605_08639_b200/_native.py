@@ -106,7 +106,8 @@ def _load(name: str, sigs: dict) -> ctypes.CDLL:
 
 
 def kernels() -> ctypes.CDLL:
-    return _load("libmb_sm100.so", _KERNEL_SIGS)
+    # MB_KERNELS_LIB selects an alternative build in lib/ (A/B experiments of kernel variants)
+    return _load(os.environ.get("MB_KERNELS_LIB", "libmb_sm100.so"), _KERNEL_SIGS)
 
 
 def planner() -> ctypes.CDLL:

@@ -45,7 +45,7 @@ static int launch_pair(const GemmParams& p, cudaStream_t stream) {
     MB_CUDA_TRY(cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), stream));
     q.prof = prof;
   }
-  kern<<<grid, 320, PairCfg<kEpi>::kSmemBytes, stream>>>(q);
+  kern<<<grid, PairCfg<kEpi>::kThreads, PairCfg<kEpi>::kSmemBytes, stream>>>(q);
   MB_CUDA_TRY(cudaGetLastError());
   if (profile) {  // profiling only: synchronous readback, per-cluster averages in cycles
     unsigned long long h[8];

@@ -28,18 +28,24 @@ struct PairTile {
   static constexpr int kBoxBytes = 32 * 128;  // one 32-row x 128-byte TMA box
 };
 
-// Shared-memory budget per epilogue kind: the dSwiGLU epilogues stage H gate|up in two boxes per
-// warp and keep 4 operand stages; the others single-buffer their output box and spend the 32 KB
-// on a 5th stage (more bytes in flight: at MoE shapes the weight stream makes the mainloop
-// latency-sensitive).
+#ifndef MB_PAIR_LIGHT_EPI_WARPS
+#define MB_PAIR_LIGHT_EPI_WARPS 4
+#endif
+// Shared-memory budget per epilogue kind: the dSwiGLU epilogues (heavy math, H staged in two
+// boxes per warp) run 8 epilogue warps and 4 operand stages; the light epilogues (store, SwiGLU,
+// fp32 gradient) run MB_PAIR_LIGHT_EPI_WARPS warps with one output box each and spend the rest
+// on operand stages (6 with 4 warps): at MoE shapes the weight stream makes the mainloop
+// latency-sensitive, and the light epilogues are idle most of a tile.
 template <int kEpi>
 struct PairCfg : PairTile {
-  static constexpr int kBoxesPerWarp = (kEpi == EPI_DSWIGLU || kEpi == EPI_DSWIGLU_GATED) ? 2 : 1;
-  static constexpr int kStages = kBoxesPerWarp == 2 ? 4 : 5;
+  static constexpr bool kHeavy = kEpi == EPI_DSWIGLU || kEpi == EPI_DSWIGLU_GATED;
+  static constexpr int kEpiWarps = kHeavy ? 8 : MB_PAIR_LIGHT_EPI_WARPS;
+  static constexpr int kThreads = 64 + 32 * kEpiWarps;
+  static constexpr int kBoxesPerWarp = kHeavy ? 2 : 1;
+  static constexpr int kStages = kHeavy ? 4 : (kEpiWarps == 4 ? 6 : 5);
   static constexpr int kABytes = 128 * BK * 2;  // this CTA's 128 rows of A
   static constexpr int kBBytes = 128 * BK * 2;  // this CTA's 128 columns of B
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kEpiWarps = 8;
   static constexpr int kStagingBytes = kEpiWarps * kBoxesPerWarp * kBoxBytes;
   static constexpr int kMetaBytes = 10240;
   static constexpr int kSmemBytes = kStages * kStageBytes + kStagingBytes + kMetaBytes + 1024;
@@ -120,7 +126,7 @@ __device__ __forceinline__ void pack_bf16_words(const uint32_t (&a)[32], const u
 }
 
 template <bool kW, bool kAmn, bool kBmn, int kEpi>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThreads, 1)
     grouped_gemm_pair_kernel(const __grid_constant__ GemmParams p) {
   using Cfg = PairCfg<kEpi>;
   constexpr int S = Cfg::kStages;
@@ -160,7 +166,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
-      mbar_init(&tempty_bar[i], 16);  // 8 epilogue warps x 2 CTAs
+      mbar_init(&tempty_bar[i], 2 * Cfg::kEpiWarps);  // every epilogue warp of both CTAs
     }
     for (int i = 0; i < Cfg::kEpiWarps; ++i) mbar_init(&hbar_base[i], 1);
     fence_barrier_init();
@@ -319,10 +325,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     __syncwarp();
   } else {
     // ------------------------------------------------------------ epilogue (both CTAs)
-    // 8 warps: warp w reads TMEM lane quarter (w & 3) and column half ch2 = (w - 2) / 4.
+    // warp w reads TMEM lane quarter (w & 3); with 8 epilogue warps column half ch2 = (w - 2) / 4,
+    // with 4 each warp makes two passes, one per column half
+    constexpr int kPasses = 8 / Cfg::kEpiWarps;
     const int q = warp & 3;
-    const int ch2 = (warp - 2) >> 2;
-    const int row_in_cta = q * 32 + lane;               // TMEM lane
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty_bar[1]), 0);
@@ -341,6 +347,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       }
       tc_fence_after();
       const uint32_t t_acc = tmem_base + lane_off + acc * 256;
+      bool released = false;
+      // hand the accumulator back to the MMA warp as soon as this warp holds all its columns
+      auto release_now = [&]() {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) mbar_arrive(&tempty_bar[acc]);
+          else mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+        }
+        released = true;
+      };
+#pragma unroll 1
+      for (int pass = 0; pass < kPasses; ++pass) {
+      const int ch2 = kPasses == 1 ? (warp - 2) >> 2 : pass;
+      auto release = [&]() {
+        if (pass == kPasses - 1) release_now();
+      };
       // full tile: this warp owns rows q*32.. of the CTA's 128 and columns [ch2*128, +128);
       // tail tile (half_tile): rows (q&1)*32.. of the CTA's 64; lane group q>>1 holds columns
       // [(q>>1)*64, +64) of both 128-column blocks; the ch2 = 1 warps have nothing to do
@@ -353,17 +376,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       auto ocol = [&](int s) { return half ? s * 128 + (q >> 1) * 64 : ch2 * 128 + s * 64; };
       const bool valid = (kW || warp_row0 < gg.rows) && !(half && ch2);  // 128-row padded groups
       const int32_t out_row0 = kW ? gg.slot * p.M + warp_row0 : gg.a0 + warp_row0;
-      bool released = false;
-      // hand the accumulator back to the MMA warp as soon as this warp holds its columns
-      auto release = [&]() {
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (leader) mbar_arrive(&tempty_bar[acc]);
-          else mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
-        }
-        released = true;
-      };
 
       if (p.debug & 1) {
         uint32_t r[32];
@@ -531,7 +543,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
           }
         }
       }
-      if (!released) release();
+      }  // passes
+      if (!released) release_now();
     }
     if (lane == 0) bulk_wait<0>();  // every TMA store of this warp has completed
     __syncwarp();

@@ -234,3 +234,45 @@ def test_histogram_matches_bincount():
         ref = torch.bincount(idx[b].flatten().long(), minlength=E)
         assert torch.equal(counts[b].long(), ref)
         assert torch.equal(chunks[b].sum(0).long(), ref)
+
+
+def test_fused_combine_backward_matches_unfused_path():
+    """The gated dSwiGLU epilogue (combine backward fused into the dAct GEMM) against the unfused
+    path: mb_combine_bwd_expert (dY = gate*dout, dgate = <dout, Y>) then the plain dSwiGLU GEMM."""
+    import numpy as np
+    from paper_2605_08639_b200 import _native as nat
+    torch.manual_seed(13)
+    hp, hd = 512, 256
+    rows, real = [384, 256], [300, 256]
+    a0, R = _row_groups(rows)
+    H = torch.randn(R, 2 * hp, device=DEV).bfloat16()
+    hb = H.float().view(R, -1, 2, 128)   # gate|up interleaved in blocks of 128
+    Act = (torch.nn.functional.silu(hb[:, :, 0]) * hb[:, :, 1]).reshape(R, hp).bfloat16()
+    W2 = (torch.randn(2, hd, hp, device=DEV) * hd ** -0.5).bfloat16()
+    g = K.make_groups(rows, a0, [0, 1], rows_real=real)
+    Y = torch.zeros(R, hd, device=DEV).bfloat16()
+    K.grouped_gemm(K.GEMM_FWD_STORE, Act, W2, g, N=hd, K=hp, C=Y)
+    dout = torch.randn(R, hd, device=DEV).bfloat16()
+    gate = torch.rand(R, device=DEV)
+    # fused
+    dH1 = torch.zeros(R, 2 * hp, device=DEV).bfloat16()
+    actg = torch.zeros(R, hp, device=DEV).bfloat16()
+    part = torch.zeros(R, hp // 64, device=DEV)
+    K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU_GATED, dout, W2, g, N=hp, K=hd, C=dH1, C2=actg, aux=H, row_scale=gate,
+                   row_partial=part)
+    # unfused
+    slot_tab = torch.tensor([[a0[i], real[i], rows[i], i] for i in range(2)], dtype=torch.int32, device=DEV)
+    dy = dout.clone()
+    dgate = torch.zeros(R, device=DEV)
+    lib = nat.kernels()
+    nat.check(lib.mb_combine_bwd_expert(dy.data_ptr(), Y.data_ptr(), gate.data_ptr(), dgate.data_ptr(),
+                                        slot_tab.data_ptr(), 2, R, hd, nat.stream_ptr()), lib, "combine_bwd")
+    dH2 = torch.zeros(R, 2 * hp, device=DEV).bfloat16()
+    K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU, dy, W2, g, N=hp, K=hd, C=dH2, aux=H)
+    torch.cuda.synchronize()
+    for i in range(2):
+        sl = slice(a0[i], a0[i] + real[i])
+        assert rel_err(dH1[sl], dH2[sl]) < 2e-2
+        assert rel_err(part[sl].sum(1), dgate[sl]) < 2e-2
+        pad = slice(a0[i] + real[i], a0[i] + rows[i])
+        assert torch.all(dH1[pad] == 0) and torch.all(dy[pad] == 0)

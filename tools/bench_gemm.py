@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--h", type=int, default=2048)
     ap.add_argument("--hp", type=int, default=768)
     ap.add_argument("--only", default="")
+    ap.add_argument("--cublas", action="store_true",
+                    help="also time torch.bmm (cuBLAS) on the same balanced shapes, plain GEMMs without epilogues")
     ap.add_argument("--zipf-rows", action="store_true",
                     help="group rows = micro-batch 0 of the bench's skewed Qwen3 routing at EP=1 (128-padded)")
     ap.add_argument("--iters", type=int, default=20)
@@ -82,6 +84,28 @@ def main():
     tot_ms = sum(v[0] for v in res.values())
     if not only:
         out["total"] = {"ms": round(tot_ms, 4), "tflops": round(9 * flop / tot_ms / 1e9, 1)}
+    if a.cublas:
+        # library baseline: batched cuBLAS GEMMs of the same (balanced) shapes, bf16 in / bf16 out
+        Xb = X.view(G, r, h)
+        W1t = W1.transpose(1, 2).contiguous()   # [G, h, 2h']
+        W2t = W2.transpose(1, 2).contiguous()   # [G, h', h]
+        Hb = torch.empty(G, r, 2 * hp, device=dev).bfloat16()
+        Ab = Act.view(G, r, hp)
+        dYb = dY.view(G, r, h)
+        dHb = torch.randn(G, r, 2 * hp, device=dev).bfloat16()
+        cub = {
+            "fwd1": (lambda: torch.bmm(Xb, W1t), 2 * flop),
+            "fwd2": (lambda: torch.bmm(Ab, W2t), flop),
+            "dgrad_act": (lambda: torch.bmm(dYb, W2), flop),
+            "dgrad_x": (lambda: torch.bmm(dHb, W1), 2 * flop),
+            "wgrad_w2": (lambda: torch.bmm(dYb.transpose(1, 2), Ab), flop),
+            "wgrad_w1": (lambda: torch.bmm(dHb.transpose(1, 2), Xb), 2 * flop),
+        }
+        out["cublas"] = {}
+        for k, (fn, fl) in cub.items():
+            ms = timeit(fn)
+            out["cublas"][k] = {"ms": round(ms, 4), "tflops": round(fl / ms / 1e9, 1)}
+        del Hb
     print(json.dumps({"shape": {"groups": G, "rows": r, "h": h, "hp": hp}, "gemm": out}))
 
 
