@@ -232,12 +232,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
             if (kProf) w_empty += clock64() - t0;
           }
           const uint32_t lbar = mapa_shared(smem_u32(&full_bar[stage]), 0);
+          if (p.debug & 32) {  // profiling only: no operand loads (MMAs read stale smem)
+            if (leader) mbar_arrive(&full_bar[stage]);
+            if (++stage == S) { stage = 0; phase ^= 1; }
+            continue;
+          }
           if (leader) mbar_arrive_expect_tx(&full_bar[stage], bytes);
           uint8_t* a_dst = sA + stage * Cfg::kABytes;
           uint8_t* b_dst = sB + stage * Cfg::kBBytes;
           if (!kAmn) {
             if (half) tma_load_2d_pair(a_dst, &p.tmAh, lbar, kb * BK, gg.a0 + tc.mb * TM + rank * 64);
-            else tma_load_2d_pair(a_dst, &p.tmA, lbar, kb * BK, gg.a0 + tc.mb * TM + rank * 128);
+            else tma_load_2d_pair(a_dst, &p.tmA, lbar, (p.debug & 64) ? 0 : kb * BK,
+                                  (p.debug & 64) ? rank * 128 : gg.a0 + tc.mb * TM + rank * 128);
           } else {
 #pragma unroll
             for (int j = 0; j < 2; ++j)
@@ -253,10 +259,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
               tma_load_2d_pair(b_dst, tmB, lbar, kb * BK, gg.slot * p.N + tc.nb * TN + rank * 128);
             }
           } else {
-            const int row0 = kW ? krow : (gg.slot * p.K + kb * BK);
+            const int row0 = (p.debug & 64) ? 0 : (kW ? krow : (gg.slot * p.K + kb * BK));
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
-              const int col = half ? tc.nb * TN + j * 128 + rank * 64 : tc.nb * TN + rank * 128 + j * 64;
+              const int col = (p.debug & 64) ? rank * 128 + j * 64
+                              : half ? tc.nb * TN + j * 128 + rank * 64 : tc.nb * TN + rank * 128 + j * 64;
               tma_load_2d_pair(b_dst + j * 8192, tmB, lbar, col, row0);
             }
           }
