@@ -78,3 +78,22 @@ def test_balanced_routing_is_uniform():
     counts = dp.counts[0].cpu().numpy()
     assert counts.max() - counts.min() <= 1
     dp.close()
+
+
+def test_step_host_matches_device_step():
+    """The user-facing host-buffer step (the e2e path) gives the same results as the device step."""
+    shape, routing, plan, dp, (wg, wu, wd), (x, dout, idx, gates), (out, dx, dgate) = _run("qwen3-30b-a3b", 512, 3)
+    g1, g2 = dp.gW1.clone(), dp.gW2.clone()
+    dp.zero_grads()
+    host = {"x": x.cpu().pin_memory(), "dout": dout.cpu().pin_memory(), "idx": idx.cpu().pin_memory(),
+            "gates": gates.cpu().pin_memory(), "out": torch.empty_like(out, device="cpu").pin_memory(),
+            "dx": torch.empty_like(dx, device="cpu").pin_memory(),
+            "dgate": torch.empty_like(dgate, device="cpu").pin_memory()}
+    dev = {k: torch.empty_like(v, device="cuda") for k, v in host.items()}
+    dp.step_host(host, dev)
+    assert torch.equal(host["out"], out.cpu())
+    assert torch.equal(host["dx"], dx.cpu())
+    assert torch.equal(host["dgate"], dgate.cpu())
+    torch.cuda.synchronize()
+    assert torch.equal(dp.gW1, g1) and torch.equal(dp.gW2, g2)
+    dp.close()
