@@ -214,6 +214,9 @@ def measure_policy(args, comm, policy, shape, cfg, routing, topo, model, cfgs, w
     dev["dgate"] = torch.empty(MB, T, shape.top_k, dtype=torch.float32, device="cuda")
 
     def step():
+        # one training step of the layer: optimizer.zero_grad() semantics (lazy: the weight-gradient
+        # GEMMs store instead of accumulating), then fwd + bwd over every micro-batch
+        dp.zero_grads()
         dp.step(dev["x"], dev["idx"], dev["gates"], dev["dout"], dev["out"], dev["dx"], dev["dgate"])
 
     for _ in range(args.warmup):
@@ -269,11 +272,13 @@ def measure_policy(args, comm, policy, shape, cfg, routing, topo, model, cfgs, w
         # e2e through the host-buffer API (pinned host tensors, copies inside the timed region)
         host = {k: v.cpu().pin_memory() for k, v in dev.items()}
         for _ in range(2):
+            dp.zero_grads()
             dp.step_host(host, dev)
         comm.host_barrier()
         t0 = time.perf_counter()
         n_e2e = max(2, min(args.steps, 5))
         for _ in range(n_e2e):
+            dp.zero_grads()
             dp.step_host(host, dev)
         comm.host_barrier()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / n_e2e

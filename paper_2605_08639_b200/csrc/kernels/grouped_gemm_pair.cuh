@@ -29,13 +29,12 @@ struct PairTile {
 };
 
 #ifndef MB_PAIR_LIGHT_EPI_WARPS
-#define MB_PAIR_LIGHT_EPI_WARPS 4
+#define MB_PAIR_LIGHT_EPI_WARPS 8   // 4 (6 stages) measured equal alone, 3-25% slower beside the comm kernels
 #endif
 // Shared-memory budget per epilogue kind: the dSwiGLU epilogues (heavy math, H staged in two
 // boxes per warp) run 8 epilogue warps and 4 operand stages; the light epilogues (store, SwiGLU,
 // fp32 gradient) run MB_PAIR_LIGHT_EPI_WARPS warps with one output box each and spend the rest
-// on operand stages (6 with 4 warps): at MoE shapes the weight stream makes the mainloop
-// latency-sensitive, and the light epilogues are idle most of a tile.
+// on operand stages (5 with 8 warps, 6 with 4).
 template <int kEpi>
 struct PairCfg : PairTile {
   static constexpr bool kHeavy = kEpi == EPI_DSWIGLU || kEpi == EPI_DSWIGLU_GATED;

@@ -451,6 +451,11 @@ class MoEDataPlane:
         for i, row in enumerate(wg):
             wtab[i] = row
         self.wgroups = torch.from_numpy(wtab).to(dev)
+        # the same table with plain stores for the home groups (first step after zero_grads)
+        wtab_store = wtab.copy()
+        wtab_store[:, 3] &= ~K.FLAG_ACCUMULATE
+        self.wgroups_store = torch.from_numpy(wtab_store).to(dev)
+        self.idle_home = [loc for loc, row in enumerate(wg[:len(self.home_experts)]) if row[0] == 0]
         self.wsegs = torch.from_numpy(np.asarray(segs if segs else [(0, 0)], dtype=np.int32).reshape(-1, 2)).to(dev)
         # ---- replica gradient reduce lists (this rank as owner): only replicas that served rows
         rep_rows = {}
@@ -503,6 +508,7 @@ class MoEDataPlane:
         sfx_new = "" if self.bank else "b"
         hp, h = self.shape.ffn, self.shape.hidden
         items = [("w1", self.w1_bytes), ("w2", self.w2_bytes)]
+        grads = grads and not getattr(self, "grads_pending_zero", False)
         if grads:
             items += [("gw1", 2 * hp * h * 4), ("gw2", h * hp * 4)]
         items += [("st_" + n, spec[2]) for n, spec in self.state_spec.items()]
@@ -523,7 +529,7 @@ class MoEDataPlane:
         self.bank ^= 1
         self._bind_bank()
         if not grads:
-            self.zero_grads()
+            self.zero_grads(lazy=True)
         self.load_plan(plan)
         return {"experts_moved": moved, "bytes_in": nbytes}
 
@@ -532,9 +538,23 @@ class MoEDataPlane:
         self.W1.copy_(interleave_w1(w_gate, w_up))
         self.W2.copy_(w_down)
 
-    def zero_grads(self) -> None:
-        self.gW1.zero_()
-        self.gW2.zero_()
+    def zero_grads(self, lazy: bool = True) -> None:
+        """Reset the fp32 expert gradients.  lazy (default): no memset; the next step's weight-
+        gradient GEMM stores instead of accumulating (0 + x == x exactly), as a trainer's
+        zero_grad() before backward would have it.  Read gradients through grads() to see the
+        zeros before that step."""
+        if lazy:
+            self.grads_pending_zero = True
+        else:
+            self.gW1.zero_()
+            self.gW2.zero_()
+            self.grads_pending_zero = False
+
+    def grads(self):
+        """(gW1, gW2) of the current bank, materialising a pending lazy zero."""
+        if getattr(self, "grads_pending_zero", False):
+            self.zero_grads(lazy=False)
+        return self.gW1, self.gW2
 
     # ------------------------------------------------------------------ step
     def _k(self, name, *args):
@@ -699,11 +719,18 @@ class MoEDataPlane:
         if not self.wgroups.shape[0]:
             return
         rows = sum(self.real_rows(m) for m in range(MB))
+        fresh = getattr(self, "grads_pending_zero", False)
+        wgroups = self.wgroups_store if fresh else self.wgroups
+        if fresh:
+            for loc in self.idle_home:  # home experts without rows this step get no wgrad tile
+                self.gW1[loc].zero_()
+                self.gW2[loc].zero_()
+            self.grads_pending_zero = False
         with self._timed(2.0 * rows * h * hp, "wgrad_down"):
-            K.grouped_gemm(K.GEMM_WGRAD, self.dYr.view(MB * R, h), self.Act.view(MB * R, hp), self.wgroups, M=h, N=hp,
+            K.grouped_gemm(K.GEMM_WGRAD, self.dYr.view(MB * R, h), self.Act.view(MB * R, hp), wgroups, M=h, N=hp,
                            C=self.gW2, c_slot_stride=h * hp, segs=self.wsegs)
         with self._timed(4.0 * rows * h * hp, "wgrad_gate_up"):
-            K.grouped_gemm(K.GEMM_WGRAD, self.dH.view(MB * R, 2 * hp), self.Xr.view(MB * R, h), self.wgroups,
+            K.grouped_gemm(K.GEMM_WGRAD, self.dH.view(MB * R, 2 * hp), self.Xr.view(MB * R, h), wgroups,
                            M=2 * hp, N=h, C=self.gW1, c_slot_stride=2 * hp * h, segs=self.wsegs)
         self.launches += 2
 
