@@ -25,6 +25,7 @@ run once per step (StepPlan) and the kernels never exchange sizes.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -39,10 +40,13 @@ from .cluster import ClusterTopology, HardwareProfile
 from .comm import Comm, SymmetricArena
 
 PAD = 128       # receive-slot row padding = GEMM M tile
+_SKIP_ROWS = os.environ.get("MB_PROFILE_SKIP_ROWS", "0") == "1"
 # SMs left to the comm stream while the persistent GEMM runs (measured on B200, qwen3 shape:
-# N=4 step 24.1 ms with all 148 SMs in the GEMM, 19.7 ms with 28 left free; N=1 best at 20)
+# N=4 step 24.1 ms with all 148 SMs in the GEMM, 19.7 ms with 28 left free)
 COMM_SMS = {1: 20}
 COMM_SMS_MULTI = 28
+# overlap=False runs every phase in issue order on one stream with all SMs in the GEMM: at world 1
+# (local row movers) it measured the same step time as the overlapped schedule (19.6 vs 19.4 ms).
 CHUNK = 32      # tokens per permutation chunk
 GATE_BLOCK = 128  # gate|up interleave block of W1 rows (= half the 256-wide SwiGLU tile)
 
@@ -271,16 +275,20 @@ class MoEDataPlane:
 
     def __init__(self, comm: Comm, shape: LayerShape, tokens: int, micro_batches: int, plan: StepPlan,
                  device: torch.device | None = None, comm_sms: int | None = None,
-                 expert_state: dict | None = None, rows_cap: int = 0):
+                 expert_state: dict | None = None, rows_cap: int = 0, overlap: bool | None = None):
         """expert_state: optional per-expert tensors that follow their expert when the reorder
         plan migrates it (e.g. optimizer moments): {name: (per-expert shape, torch dtype)}.
-        rows_cap: receive rows per micro-batch to allocate (>= every plan this layer will load)."""
+        rows_cap: receive rows per micro-batch to allocate (>= every plan this layer will load).
+        overlap: run dispatch / combine on their own stream beside the GEMMs (default)."""
         shape.check()
         self.comm, self.shape, self.T, self.MB = comm, shape, tokens, micro_batches
         self.rank, self.world = comm.rank, comm.world
         self.device = device or torch.device("cuda", torch.cuda.current_device())
+        if overlap is None and os.environ.get("MB_OVERLAP") in ("0", "1"):
+            overlap = os.environ["MB_OVERLAP"] == "1"
+        self.overlap = True if overlap is None else overlap
         if comm_sms is None:
-            comm_sms = COMM_SMS.get(self.world, COMM_SMS_MULTI)
+            comm_sms = COMM_SMS.get(self.world, COMM_SMS_MULTI) if self.overlap else 0
         sms = torch.cuda.get_device_properties(self.device).multi_processor_count
         lib = nat.kernels()
         nat.check(lib.mb_set_gemm_sms(max(2, sms - comm_sms)), lib, "mb_set_gemm_sms")
@@ -558,6 +566,8 @@ class MoEDataPlane:
 
     # ------------------------------------------------------------------ step
     def _k(self, name, *args):
+        if _SKIP_ROWS and name in ("mb_scatter_rows", "mb_combine_rows"):
+            return  # profiling only (MB_PROFILE_SKIP_ROWS): GEMM timing without the row movers
         lib = nat.kernels()
         nat.check(getattr(lib, name)(*args), lib, name)
         self.launches += 1
@@ -571,7 +581,8 @@ class MoEDataPlane:
         MB = self.MB
         h, hp, k, T = self.shape.hidden, self.shape.ffn, self.shape.top_k, self.T
         E = self.shape.num_experts
-        cs, xs, A = torch.cuda.current_stream(), self.xs, self.arena
+        cs, A = torch.cuda.current_stream(), self.arena
+        xs = self.xs if self.overlap else cs
         st_x = xs.cuda_stream
         chunks = (T + CHUNK - 1) // CHUNK
         xs.wait_stream(cs)
