@@ -380,7 +380,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
       // 64-column segment s of this warp: TMEM column and output column (within the 256-wide tile)
       auto tcol = [&](int s) { return half ? s * 64 : ch2 * 128 + s * 64; };
       auto ocol = [&](int s) { return half ? s * 128 + (q >> 1) * 64 : ch2 * 128 + s * 64; };
-      const bool valid = (kW || warp_row0 < gg.rows) && !(half && ch2);  // 128-row padded groups
+      // tail tiles: the two warps of a lane quarter split the two 64-column segments (store and
+      // dSwiGLU epilogues); the SwiGLU epilogue needs gate and up of a feature in one warp, so
+      // there the ch2 = 1 warps idle
+      const bool valid = (kW || warp_row0 < gg.rows) && !(half && ch2 && kEpi == EPI_SWIGLU);
       const int32_t out_row0 = kW ? gg.slot * p.M + warp_row0 : gg.a0 + warp_row0;
 
       if (p.debug & 1) {
@@ -391,16 +394,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
       } else if (valid) {
         if constexpr (kEpi == EPI_STORE_BF16) {
           uint32_t a0[32], a1[32], b0[32], b1[32], w[32];
-          tmem_ld_32x32b_x32(t_acc + tcol(0), a0);
-          tmem_ld_32x32b_x32(t_acc + tcol(0) + 32, a1);
-          tmem_ld_32x32b_x32(t_acc + tcol(1), b0);
-          tmem_ld_32x32b_x32(t_acc + tcol(1) + 32, b1);
-          tmem_ld_wait();
-          release();
-          pack_bf16_words(a0, a1, w);
-          st.put<false>(w, &p.tmC, tc.nb * TN + ocol(0), out_row0);
-          pack_bf16_words(b0, b1, w);
-          st.put<false>(w, &p.tmC, tc.nb * TN + ocol(1), out_row0);
+          if (half) {  // this warp's one segment
+            tmem_ld_32x32b_x32(t_acc + tcol(ch2), a0);
+            tmem_ld_32x32b_x32(t_acc + tcol(ch2) + 32, a1);
+            tmem_ld_wait();
+            release();
+            pack_bf16_words(a0, a1, w);
+            st.put<false>(w, &p.tmC, tc.nb * TN + ocol(ch2), out_row0);
+          } else {
+            tmem_ld_32x32b_x32(t_acc + tcol(0), a0);
+            tmem_ld_32x32b_x32(t_acc + tcol(0) + 32, a1);
+            tmem_ld_32x32b_x32(t_acc + tcol(1), b0);
+            tmem_ld_32x32b_x32(t_acc + tcol(1) + 32, b1);
+            tmem_ld_wait();
+            release();
+            pack_bf16_words(a0, a1, w);
+            st.put<false>(w, &p.tmC, tc.nb * TN + ocol(0), out_row0);
+            pack_bf16_words(b0, b1, w);
+            st.put<false>(w, &p.tmC, tc.nb * TN + ocol(1), out_row0);
+          }
         } else if constexpr (kEpi == EPI_SWIGLU) {
           // gate columns [0,128), up columns [128,256); this warp owns gate/up features [f0, +64)
           // (tail tile: gate block at TMEM [0,64), up block at [64,128))
@@ -450,7 +462,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
           uint4* rowB = reinterpret_cast<uint4*>(bufB + lane * 128);
           const int sw = lane & 7;
 #pragma unroll 1
-          for (int hh = 0; hh < 2; ++hh) {
+          for (int hh = half ? ch2 : 0; hh < (half ? ch2 + 1 : 2); ++hh) {
             const int blk = tc.nb * 2 + ocol(hh) / 128;
             const int fo = ocol(hh) % 128;
             float part = 0.0f;
