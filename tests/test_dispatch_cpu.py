@@ -57,6 +57,19 @@ def test_dispatch_tables_match_oracle(name, world, policy, zipf):
             want = np.array([[b, real, padded, e] for e, c, b, real, padded in slots[d]], dtype=np.int32).reshape(-1, 4)
             assert np.array_equal(got, want)
         assert np.array_equal(mbp.flow, moe_ref.executed_flow(r.mats[m], plan.home, reps, counts))
+        # pin the oracle's executed flow to the reference's flow_matrix semantics (costmodel.py:91-108):
+        # the planner-level flow_matrix (bit-exact with the reference, tests/test_planners_golden.py)
+        # with the split fractions count / x gives the same integer flow
+        x = r.mats[m].astype(np.float64)
+        splits = {}
+        for e, c in counts.items():
+            col = x[:, e][:, None]
+            frac = np.divide(c, col, out=np.zeros(c.shape), where=col > 0)
+            frac[x[:, e] == 0, 0] = 1.0
+            splits[e] = (np.array(mbp.placement.copies(e)), frac)
+        ref_flow = mb.flow_matrix(x, plan.home, topo, splits)
+        assert np.array_equal(np.rint(ref_flow).astype(np.int64), mbp.flow)
+        assert np.abs(ref_flow - mbp.flow).max() < 1e-6
         # executed GEMM rows per GPU equal the reference cost model's comp loads (integer splits)
         assert np.array_equal(mbp.flow.sum(axis=0), plan.executed_loads()[m])
         # canonical permutation from the route table (the kernel's rule) == oracle definition
