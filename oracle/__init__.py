@@ -10,15 +10,16 @@ Contents:
                  (costmodel.flow_matrix, costmodel.py:91-108 with replicate.round_split,
                  replicate.py:501-525), the canonical permutation, and the SwiGLU expert FFN
                  forward/backward with gate-weighted combine.
-  planners_np.py numpy restatement of the reference planners (reorder.py, replicate.py,
-                 lp.py, sim.py) used as the CPU reference arm of bench.py.
-  gen_golden.py  regenerates tests/golden/ by importing the reference package from
-                 /root/reference (this container only; the fixtures travel, the reference
-                 does not).
+  gen_golden.py  regenerates tests/golden/planners.json (planner golden vectors and KATs) by
+                 importing the reference package from /root/reference (this container only;
+                 the fixtures travel, the reference does not).
+  gen_golden_io.py  regenerates tests/golden/io/: trace directories and plan files written by the
+                 reference's own `gen` / `solve`, and its acceptance study (criteria 6/7).
 
 Parity pinning: the planners are pinned against golden vectors produced by the reference
-itself (tests/golden/planners_*.npz) plus the reference's own KATs; the histogram and the
-permutation are integer work checked bit-exactly; the layer math has no reference
+itself (tests/golden/planners.json, tests/golden/io/) plus the reference's own KATs; the
+oracle's executed flow is checked against the reference's flow_matrix semantics; the histogram
+and the permutation are integer work checked bit-exactly; the layer math has no reference
 implementation (the reference models it analytically), so its parity is against this fp32
 restatement at the north_star tolerance rel 2e-2 ("parity unpinned" for the layer math in
 the sense of the task statement: no reference numbers exist for it).
