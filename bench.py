@@ -117,9 +117,11 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- CPU reference arm
 
 def cpu_reference_sample(cfg_name: str, tokens: int, world: int, zipf: float, budget_s: float, threads: int):
-    """The reference's CPU path on a bounded sample: the planner pipeline of moebalance on the
-    full step's routing (oracle restatement) + np.bincount histogram + the fp32 layer fwd+bwd on a
-    token sample.  Returns (tokens/s extrapolated per step-token, sample description)."""
+    """The CPU path on a bounded sample (oracle port): np.bincount histogram + the fp32 layer
+    fwd+bwd (SwiGLU experts, gate-weighted combine) on a token sample, all host threads.  The
+    reference's planners are not in this arm (they cannot travel to the GPU box); their cost is
+    measured beside the native planners in profiles/r01_planner_timing.json.
+    Returns (tokens/s, sample description)."""
     import torch
     from oracle import moe_ref
     from paper_2605_08639_b200.workload import SHAPES, make_activations, make_routing, make_weights
@@ -133,8 +135,7 @@ def cpu_reference_sample(cfg_name: str, tokens: int, world: int, zipf: float, bu
         r = make_routing(shape, n, 1, 1, 0, zipf_s=zipf, shift=cfg["shift"])
         x, dout = make_activations(shape, n, 1, 0)
         t0 = time.perf_counter()
-        for j in range(1):
-            moe_ref.histogram(r.idx[0], shape.num_experts)
+        moe_ref.histogram(r.idx[0], shape.num_experts)
         moe_ref.moe_layer_fp32(x[0], torch.from_numpy(r.idx[0]), torch.from_numpy(r.gates[0]), wg, wu, wd, dout[0])
         dt = time.perf_counter() - t0
         elapsed += dt
