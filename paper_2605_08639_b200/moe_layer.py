@@ -458,11 +458,6 @@ class MoEDataPlane:
         wtab = np.zeros((len(wg), K.GROUP_FIELDS), dtype=np.int32)
         for i, row in enumerate(wg):
             wtab[i] = row
-        self.wgroups = torch.from_numpy(wtab).to(dev)
-        # the same table with plain stores for the home groups (first step after zero_grads)
-        wtab_store = wtab.copy()
-        wtab_store[:, 3] &= ~K.FLAG_ACCUMULATE
-        self.wgroups_store = torch.from_numpy(wtab_store).to(dev)
         self.idle_home = [loc for loc, row in enumerate(wg[:len(self.home_experts)]) if row[0] == 0]
         self.wsegs = torch.from_numpy(np.asarray(segs if segs else [(0, 0)], dtype=np.int32).reshape(-1, 2)).to(dev)
         # ---- replica gradient reduce lists (this rank as owner): only replicas that served rows
@@ -484,6 +479,24 @@ class MoEDataPlane:
                 p2 = [self.arena.peer_ptr(p, self.off_w["gw2"]) + (self.M + q) * (mn1 // 2) * 4 for p, q in srcs]
                 self.reduce.append((loc, torch.tensor(p1, dtype=torch.int64, device=dev),
                                     torch.tensor(p2, dtype=torch.int64, device=dev), len(srcs)))
+        # wgrad launch split: (A) replica groups + home experts that receive replica gradients,
+        # (B) every other home expert.  The owners' replica-gradient reduce waits only for A, so it
+        # runs beside B instead of after the whole weight-gradient phase.
+        red = {loc for loc, *_ in self.reduce}
+        nh = len(self.home_experts)
+        part_a = [i for i in range(len(wg)) if i >= nh or i in red]
+        part_b = [i for i in range(nh) if i not in red]
+        self.wparts = []
+        for rows_idx in ((part_a, part_b) if self.reduce else (list(range(len(wg))),)):
+            if not rows_idx:
+                self.wparts.append(None)
+                continue
+            tab = wtab[rows_idx]
+            tab_store = tab.copy()
+            tab_store[:, 3] &= ~K.FLAG_ACCUMULATE
+            share = float(tab[:, 0].sum()) / max(1.0, float(wtab[:, 0].sum()))
+            self.wparts.append((torch.from_numpy(np.ascontiguousarray(tab)).to(dev),
+                                torch.from_numpy(np.ascontiguousarray(tab_store)).to(dev), share))
 
     # ------------------------------------------------------------------ weights
     def _bind_bank(self) -> None:
@@ -709,12 +722,17 @@ class MoEDataPlane:
             ev_comp[(op, m)] = torch.cuda.Event()
             ev_comp[(op, m)].record(cs)
             pi += 1
-        # ---- weight gradients (compute stream), K over every micro-batch of the step
-        self._wgrad()
+        # ---- weight gradients (compute stream), K over every micro-batch of the step; the replica
+        # gradient reduce (comm stream) starts once part A (replica groups + their owners'
+        # experts) is done and overlaps part B
+        fresh = self._wgrad_prepare()
+        self._wgrad(self.wparts[0], fresh)
         ev = torch.cuda.Event()
         ev.record(cs)
+        if len(self.wparts) > 1:
+            self._wgrad(self.wparts[1], fresh)
         xs.wait_event(ev)
-        if self.world > 1:
+        if self.world > 1 and self.reduce:
             mn1, mn2 = 2 * hp * h, h * hp
             with self._timed(sum(n for _, _, _, n in self.reduce) * (mn1 + mn2) * 4, "comm_replica_grad_reduce", xs):
                 A.barrier(xs)  # every rank's replica gradients are complete
@@ -724,19 +742,24 @@ class MoEDataPlane:
                 A.barrier(xs)  # peers finished reading our replica gradients (next step may overwrite)
         cs.wait_stream(xs)
 
-    def _wgrad(self):
-        h, hp = self.shape.hidden, self.shape.ffn
-        R, MB = self.R, self.MB
-        if not self.wgroups.shape[0]:
-            return
-        rows = sum(self.real_rows(m) for m in range(MB))
+    def _wgrad_prepare(self) -> bool:
+        """Lazy zero_grads: zero the home slots no wgrad tile will write, report store mode."""
         fresh = getattr(self, "grads_pending_zero", False)
-        wgroups = self.wgroups_store if fresh else self.wgroups
         if fresh:
             for loc in self.idle_home:  # home experts without rows this step get no wgrad tile
                 self.gW1[loc].zero_()
                 self.gW2[loc].zero_()
             self.grads_pending_zero = False
+        return fresh
+
+    def _wgrad(self, part, fresh: bool):
+        h, hp = self.shape.hidden, self.shape.ffn
+        R, MB = self.R, self.MB
+        if part is None:
+            return
+        tab, tab_store, share = part
+        rows = share * sum(self.real_rows(m) for m in range(MB))
+        wgroups = tab_store if fresh else tab
         with self._timed(2.0 * rows * h * hp, "wgrad_down"):
             K.grouped_gemm(K.GEMM_WGRAD, self.dYr.view(MB * R, h), self.Act.view(MB * R, hp), wgroups, M=h, N=hp,
                            C=self.gW2, c_slot_stride=h * hp, segs=self.wsegs)
