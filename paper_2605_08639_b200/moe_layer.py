@@ -600,20 +600,25 @@ class MoEDataPlane:
         chunks = (T + CHUNK - 1) // CHUNK
         xs.wait_stream(cs)
         # K5: replica weights of every micro-batch into the peers' slots (copy engine)
+        push_ev = {}
         if self.pushes:
+            # in micro-batch order; D(m) waits for micro-batch m's pushes before its final barrier,
+            # so the first GEMMs need not wait for the whole step's replica weights
             self.cps.wait_stream(cs)
             lib = nat.kernels()
             push_t = self._timed(len(self.pushes) * (self.w1_bytes + self.w2_bytes), "comm_replica_push", self.cps)
             push_t.__enter__()
-            for dst, m, slot, loc in self.pushes:
+            for i, (dst, m, slot, loc) in enumerate(self.pushes):
                 d1 = A.peer_ptr(dst, self.off["w1r"]) + (m * self.slots + slot) * self.w1_bytes
                 d2 = A.peer_ptr(dst, self.off["w2r"]) + (m * self.slots + slot) * self.w2_bytes
                 nat.check(lib.mb_memcpy_async(d1, self.W1[loc].data_ptr(), self.w1_bytes, self.cps.cuda_stream),
                           lib, "replica push")
                 nat.check(lib.mb_memcpy_async(d2, self.W2[loc].data_ptr(), self.w2_bytes, self.cps.cuda_stream),
                           lib, "replica push")
+                if i + 1 == len(self.pushes) or self.pushes[i + 1][1] != m:
+                    push_ev[m] = torch.cuda.Event()
+                    push_ev[m].record(self.cps)
             push_t.__exit__(None, None, None)
-            xs.wait_stream(self.cps)
         ev_comm, ev_comp = {}, {}
 
         row_b = 2 * h
@@ -639,13 +644,15 @@ class MoEDataPlane:
                     st_x)
             self._k("mb_zero_pad_rows", self.Xr[m].data_ptr(), self.slot_tab[m].data_ptr(), self.nslots[m], h, st_x)
             if m == 0:
-                A.barrier(xs)  # all ranks: previous step drained, replica pushes landed
+                A.barrier(xs)  # all ranks: previous step drained
             self._k("mb_permute_rank", idx[m].data_ptr(), T, k, gates[m].data_ptr(), E,
                     self.chunk_base[m].data_ptr(), CHUNK, self.route_tab[m].data_ptr(), self.ncopies[m].data_ptr(),
                     self.plan.maxc, self.ptr_gate[m].data_ptr(), self.perm[m].data_ptr(), st_x)
             self._k("mb_scatter_rows", x[m].data_ptr(), T, k, h, self.perm[m].data_ptr(), self.ptr_xr[m].data_ptr(),
                     st_x)
-            A.barrier(xs)  # rows of micro-batch m have landed everywhere
+            if m in push_ev:
+                xs.wait_event(push_ev[m])  # this rank's replica pushes for micro-batch m
+            A.barrier(xs)  # rows and replica weights of micro-batch m have landed everywhere
 
         def _combine(m):  # C(m): K6 gate-weighted combine of Y, then the raw dout rows out (K3)
             A.barrier(xs)  # Y of micro-batch m complete on every rank
@@ -732,7 +739,7 @@ class MoEDataPlane:
         if len(self.wparts) > 1:
             self._wgrad(self.wparts[1], fresh)
         xs.wait_event(ev)
-        if self.world > 1 and self.reduce:
+        if self.world > 1:  # collective: every rank runs both barriers, with or without replicas
             mn1, mn2 = 2 * hp * h, h * hp
             with self._timed(sum(n for _, _, _, n in self.reduce) * (mn1 + mn2) * 4, "comm_replica_grad_reduce", xs):
                 A.barrier(xs)  # every rank's replica gradients are complete
