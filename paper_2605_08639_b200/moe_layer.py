@@ -590,121 +590,19 @@ class MoEDataPlane:
         """One training step of the layer over MB micro-batches (inputs [MB, T, ...] on device).
         Writes out / dx / dgate and accumulates fp32 expert gradients.  Asynchronous with respect
         to the host; the current stream is ordered after all of it on return.  `hooks` (optional)
-        gets inputs_ready(m, stream), after_forward(m, stream), after_backward(m, stream)."""
-        MB = self.MB
-        h, hp, k, T = self.shape.hidden, self.shape.ffn, self.shape.top_k, self.T
-        E = self.shape.num_experts
-        cs, A = torch.cuda.current_stream(), self.arena
-        xs = self.xs if self.overlap else cs
-        st_x = xs.cuda_stream
-        chunks = (T + CHUNK - 1) // CHUNK
-        xs.wait_stream(cs)
-        # K5: replica weights of every micro-batch into the peers' slots (copy engine)
-        push_ev = {}
-        if self.pushes:
-            # in micro-batch order; D(m) waits for micro-batch m's pushes before its final barrier,
-            # so the first GEMMs need not wait for the whole step's replica weights
-            self.cps.wait_stream(cs)
-            lib = nat.kernels()
-            push_t = self._timed(len(self.pushes) * (self.w1_bytes + self.w2_bytes), "comm_replica_push", self.cps)
-            push_t.__enter__()
-            for i, (dst, m, slot, loc) in enumerate(self.pushes):
-                d1 = A.peer_ptr(dst, self.off["w1r"]) + (m * self.slots + slot) * self.w1_bytes
-                d2 = A.peer_ptr(dst, self.off["w2r"]) + (m * self.slots + slot) * self.w2_bytes
-                nat.check(lib.mb_memcpy_async(d1, self.W1[loc].data_ptr(), self.w1_bytes, self.cps.cuda_stream),
-                          lib, "replica push")
-                nat.check(lib.mb_memcpy_async(d2, self.W2[loc].data_ptr(), self.w2_bytes, self.cps.cuda_stream),
-                          lib, "replica push")
-                if i + 1 == len(self.pushes) or self.pushes[i + 1][1] != m:
-                    push_ev[m] = torch.cuda.Event()
-                    push_ev[m].record(self.cps)
-            push_t.__exit__(None, None, None)
-        ev_comm, ev_comp = {}, {}
-
-        row_b = 2 * h
-
-        def dispatch(m):  # D(m): K1 histogram, K2 ranks, K3 scatter into every rank's receive rows
-            with self._timed(self.remote_rows(m)[0] * row_b, "comm_dispatch", xs):
-                _dispatch(m)
-
-        def combine(m):
-            with self._timed(sum(self.remote_rows(m)) * row_b, "comm_combine_dout", xs):
-                _combine(m)
-
-        def unpermute(m):
-            with self._timed(self.remote_rows(m)[0] * row_b, "comm_unpermute", xs):
-                _unpermute(m)
-
-        def _dispatch(m):
-            if hooks:
-                hooks.inputs_ready(m, xs)
-            self._k("mb_expert_histogram", idx[m].data_ptr(), 1, T, k, E, self.counts[m].data_ptr(),
-                    self.chunk_counts[m].data_ptr(), CHUNK, st_x)
-            self._k("mb_chunk_scan", self.chunk_counts[m].data_ptr(), self.chunk_base[m].data_ptr(), 1, chunks, E,
-                    st_x)
-            self._k("mb_zero_pad_rows", self.Xr[m].data_ptr(), self.slot_tab[m].data_ptr(), self.nslots[m], h, st_x)
-            if m == 0:
-                A.barrier(xs)  # all ranks: previous step drained
-            self._k("mb_permute_rank", idx[m].data_ptr(), T, k, gates[m].data_ptr(), E,
-                    self.chunk_base[m].data_ptr(), CHUNK, self.route_tab[m].data_ptr(), self.ncopies[m].data_ptr(),
-                    self.plan.maxc, self.ptr_gate[m].data_ptr(), self.perm[m].data_ptr(), st_x)
-            self._k("mb_scatter_rows", x[m].data_ptr(), T, k, h, self.perm[m].data_ptr(), self.ptr_xr[m].data_ptr(),
-                    st_x)
-            if m in push_ev:
-                xs.wait_event(push_ev[m])  # this rank's replica pushes for micro-batch m
-            A.barrier(xs)  # rows and replica weights of micro-batch m have landed everywhere
-
-        def _combine(m):  # C(m): K6 gate-weighted combine of Y, then the raw dout rows out (K3)
-            A.barrier(xs)  # Y of micro-batch m complete on every rank
-            self._k("mb_combine_rows", self.ptr_y[m].data_ptr(), self.perm[m].data_ptr(), gates[m].data_ptr(),
-                    T, k, h, out[m].data_ptr(), None, None, 1, st_x)
-            if hooks:
-                hooks.after_forward(m, xs)
-            self._k("mb_scatter_rows", dout[m].data_ptr(), T, k, h, self.perm[m].data_ptr(),
-                    self.ptr_dyr[m].data_ptr(), st_x)
-            A.barrier(xs)  # dout rows of micro-batch m have landed everywhere
-
-        def _unpermute(m):  # X(m): dX un-permute + dgate gather
-            A.barrier(xs)  # dX rows / dgate partials of micro-batch m complete everywhere
-            self._k("mb_combine_rows", self.ptr_dxp[m].data_ptr(), self.perm[m].data_ptr(), None, T, k, h,
-                    dx[m].data_ptr(), self.ptr_dgate[m].data_ptr(), dgate[m].data_ptr(), self.npart, st_x)
-            if hooks:
-                hooks.after_backward(m, xs)
-
-        def forward(m):  # F(m): gate/up GEMM + SwiGLU, down GEMM
-            ng = self.nslots[m]
-            if ng:
-                g = self.groups[m][:ng]
-                rows = self.real_rows(m)
-                with self._timed(4.0 * rows * h * hp, "fwd_swiglu"):
-                    K.grouped_gemm(K.GEMM_FWD_SWIGLU, self.Xr[m], self.W1, g, N=2 * hp, K=h, C=self.H[m],
-                                   C2=self.Act[m], B1=self.W1r[m])
-                with self._timed(2.0 * rows * h * hp, "fwd_down"):
-                    K.grouped_gemm(K.GEMM_FWD_STORE, self.Act[m], self.W2, g, N=h, K=hp, C=self.Y[m],
-                                   B1=self.W2r[m])
-                self.launches += 2
-
-        def backward(m):  # B(m): dAct (combine backward + dSwiGLU fused in the epilogue), dX
-            ng = self.nslots[m]
-            if ng:
-                g = self.groups[m][:ng]
-                rows = self.real_rows(m)
-                # dAct = dout.W2 with the combine backward fused in the epilogue: gate applied per row,
-                # dgate partials <dout.W2, act> = <dout, Y>, gate*act written over Act for dW2
-                with self._timed(2.0 * rows * h * hp, "dgrad_act_gated"):
-                    K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU_GATED, self.dYr[m], self.W2, g, N=hp, K=h, C=self.dH[m],
-                                   C2=self.Act[m], aux=self.H[m], B1=self.W2r[m], row_scale=self.gate_r[m],
-                                   row_partial=self.dgate_r[m])
-                with self._timed(4.0 * rows * h * hp, "dgrad_x"):
-                    K.grouped_gemm(K.GEMM_DGRAD_STORE, self.dH[m], self.W1, g, N=h, K=2 * hp, C=self.dXp[m],
-                                   B1=self.W1r[m])
-                self.launches += 2
-
-        comm_fn = {"D": dispatch, "C": combine, "X": unpermute}
-        comp_fn = {"F": forward, "B": backward}
+        gets inputs_ready(m, stream), after_forward(m, stream), after_backward(m, stream).
+        Runs the two-micro-batch-overlap schedule (schedule()); the same phases are available one
+        micro-batch at a time through begin_step / forward_mb / backward_mb / end_step."""
+        ops = _StepOps(self, hooks)
+        comm_fn = {"D": lambda m: ops.dispatch(m, x[m], idx[m], gates[m]),
+                   "C": lambda m: (ops.combine(m, gates[m], out[m]), ops.dout_dispatch(m, dout[m])),
+                   "X": lambda m: ops.unpermute(m, dx[m], dgate[m])}
+        comp_fn = {"F": ops.fwd_gemms, "B": ops.bwd_gemms}
         comm_needs = {"C": "F", "X": "B"}   # comm op waits for this compute op of the same micro-batch
         comp_needs = {"F": "D", "B": "C"}
-        comm_ops, comp_ops = schedule(MB)
+        comm_ops, comp_ops = schedule(self.MB)
+        ev_comm, ev_comp = {}, {}
+        cs, xs = ops.cs, ops.xs
         ci = pi = 0
         # host issue order only has to respect the cross-stream event dependencies; each stream
         # then runs its own sequence in order on the device
@@ -729,25 +627,52 @@ class MoEDataPlane:
             ev_comp[(op, m)] = torch.cuda.Event()
             ev_comp[(op, m)].record(cs)
             pi += 1
-        # ---- weight gradients (compute stream), K over every micro-batch of the step; the replica
-        # gradient reduce (comm stream) starts once part A (replica groups + their owners'
-        # experts) is done and overlaps part B
-        fresh = self._wgrad_prepare()
-        self._wgrad(self.wparts[0], fresh)
-        ev = torch.cuda.Event()
-        ev.record(cs)
-        if len(self.wparts) > 1:
-            self._wgrad(self.wparts[1], fresh)
-        xs.wait_event(ev)
-        if self.world > 1:  # collective: every rank runs both barriers, with or without replicas
-            mn1, mn2 = 2 * hp * h, h * hp
-            with self._timed(sum(n for _, _, _, n in self.reduce) * (mn1 + mn2) * 4, "comm_replica_grad_reduce", xs):
-                A.barrier(xs)  # every rank's replica gradients are complete
-                for loc, p1, p2, n in self.reduce:
-                    self._k("mb_accumulate_f32", self.gW1[loc].data_ptr(), p1.data_ptr(), n, mn1, st_x)
-                    self._k("mb_accumulate_f32", self.gW2[loc].data_ptr(), p2.data_ptr(), n, mn2, st_x)
-                A.barrier(xs)  # peers finished reading our replica gradients (next step may overwrite)
-        cs.wait_stream(xs)
+        ops.finish()
+
+    # ------------------------------------------------------------------ per-micro-batch API
+    def begin_step(self) -> None:
+        """Open a step for the per-micro-batch API: replica pushes of every micro-batch start."""
+        if getattr(self, "_ops", None) is not None:
+            raise RuntimeError("begin_step called twice without end_step")
+        self._ops = _StepOps(self, None)
+
+    def forward_mb(self, m: int, x: torch.Tensor, idx: torch.Tensor, gates: torch.Tensor,
+                   out: torch.Tensor) -> None:
+        """Forward of micro-batch m: dispatch, expert FFN, gate-weighted combine into out [T, h].
+        Ordered after the current stream's work; the current stream waits for out."""
+        ops = self._require_step()
+        ops.xs.wait_stream(ops.cs)
+        ops.dispatch(m, x, idx, gates)
+        ops.cs.wait_stream(ops.xs)
+        ops.fwd_gemms(m)
+        ops.xs.wait_stream(ops.cs)
+        ops.combine(m, gates, out)
+        ops.cs.wait_stream(ops.xs)
+
+    def backward_mb(self, m: int, dout: torch.Tensor, dx: torch.Tensor, dgate: torch.Tensor) -> None:
+        """Backward of micro-batch m (after its forward_mb): dout dispatch, dAct with the fused
+        combine backward, dX, un-permute into dx [T, h] and dgate [T, k].  Weight gradients are
+        contracted over every micro-batch in end_step."""
+        ops = self._require_step()
+        ops.xs.wait_stream(ops.cs)
+        ops.dout_dispatch(m, dout)
+        ops.cs.wait_stream(ops.xs)
+        ops.bwd_gemms(m)
+        ops.xs.wait_stream(ops.cs)
+        ops.unpermute(m, dx, dgate)
+        ops.cs.wait_stream(ops.xs)
+
+    def end_step(self) -> None:
+        """Weight gradients over the step's micro-batches and the replica-gradient reduce."""
+        ops = self._require_step()
+        ops.finish()
+        self._ops = None
+
+    def _require_step(self):
+        ops = getattr(self, "_ops", None)
+        if ops is None:
+            raise RuntimeError("call begin_step() first")
+        return ops
 
     def _wgrad_prepare(self) -> bool:
         """Lazy zero_grads: zero the home slots no wgrad tile will write, report store mode."""
@@ -821,3 +746,177 @@ class MoEDataPlane:
     def close(self) -> None:
         torch.cuda.synchronize(self.device)
         self.arena.close()
+
+
+class _StepOps:
+    """The phases of one step of a MoEDataPlane on its two streams (compute: K4 GEMMs; comm:
+    histogram / permutation / scatter / combine and every device barrier).  Every rank must call
+    the phases in the same order: each comm phase contains collective device barriers."""
+
+    def __init__(self, dp: "MoEDataPlane", hooks=None):
+        self.dp, self.hooks = dp, hooks
+        self.cs = torch.cuda.current_stream()
+        self.xs = dp.xs if dp.overlap else self.cs
+        self.st_x = self.xs.cuda_stream
+        self.xs.wait_stream(self.cs)
+        self.push_ev = {}
+        A, cps = dp.arena, dp.cps
+        if dp.pushes:
+            # K5, in micro-batch order; dispatch(m) waits for micro-batch m's pushes before its
+            # final barrier, so the first GEMMs need not wait for the whole step's replica weights
+            cps.wait_stream(self.cs)
+            lib = nat.kernels()
+            with dp._timed(len(dp.pushes) * (dp.w1_bytes + dp.w2_bytes), "comm_replica_push", cps):
+                for i, (dst, m, slot, loc) in enumerate(dp.pushes):
+                    d1 = A.peer_ptr(dst, dp.off["w1r"]) + (m * dp.slots + slot) * dp.w1_bytes
+                    d2 = A.peer_ptr(dst, dp.off["w2r"]) + (m * dp.slots + slot) * dp.w2_bytes
+                    nat.check(lib.mb_memcpy_async(d1, dp.W1[loc].data_ptr(), dp.w1_bytes, cps.cuda_stream),
+                              lib, "replica push")
+                    nat.check(lib.mb_memcpy_async(d2, dp.W2[loc].data_ptr(), dp.w2_bytes, cps.cuda_stream),
+                              lib, "replica push")
+                    if i + 1 == len(dp.pushes) or dp.pushes[i + 1][1] != m:
+                        self.push_ev[m] = torch.cuda.Event()
+                        self.push_ev[m].record(cps)
+        self.first = True
+
+    # -------------------------------------------------------------- comm stream
+    def dispatch(self, m, x, idx, gates):
+        """D(m): K1 histogram, K2 ranks, K3 scatter into every rank's receive rows."""
+        dp, xs, st = self.dp, self.xs, self.st_x
+        sh = dp.shape
+        T, k, h, E = dp.T, sh.top_k, sh.hidden, sh.num_experts
+        with dp._timed(dp.remote_rows(m)[0] * 2 * h, "comm_dispatch", xs):
+            if self.hooks:
+                self.hooks.inputs_ready(m, xs)
+            dp._k("mb_expert_histogram", idx.data_ptr(), 1, T, k, E, dp.counts[m].data_ptr(),
+                  dp.chunk_counts[m].data_ptr(), CHUNK, st)
+            dp._k("mb_chunk_scan", dp.chunk_counts[m].data_ptr(), dp.chunk_base[m].data_ptr(), 1,
+                  (T + CHUNK - 1) // CHUNK, E, st)
+            dp._k("mb_zero_pad_rows", dp.Xr[m].data_ptr(), dp.slot_tab[m].data_ptr(), dp.nslots[m], h, st)
+            if self.first:
+                dp.arena.barrier(xs)  # all ranks: previous step drained
+                self.first = False
+            dp._k("mb_permute_rank", idx.data_ptr(), T, k, gates.data_ptr(), E, dp.chunk_base[m].data_ptr(), CHUNK,
+                  dp.route_tab[m].data_ptr(), dp.ncopies[m].data_ptr(), dp.plan.maxc, dp.ptr_gate[m].data_ptr(),
+                  dp.perm[m].data_ptr(), st)
+            dp._k("mb_scatter_rows", x.data_ptr(), T, k, h, dp.perm[m].data_ptr(), dp.ptr_xr[m].data_ptr(), st)
+            if m in self.push_ev:
+                xs.wait_event(self.push_ev[m])  # this rank's replica pushes for micro-batch m
+            dp.arena.barrier(xs)  # rows and replica weights of micro-batch m have landed everywhere
+
+    def combine(self, m, gates, out):
+        """K6: out[t] = sum_i gate * Y[perm(t, i)] over peer loads."""
+        dp, xs = self.dp, self.xs
+        h = dp.shape.hidden
+        with dp._timed(dp.remote_rows(m)[0] * 2 * h, "comm_combine", xs):
+            dp.arena.barrier(xs)  # Y of micro-batch m complete on every rank
+            dp._k("mb_combine_rows", dp.ptr_y[m].data_ptr(), dp.perm[m].data_ptr(), gates.data_ptr(), dp.T,
+                  dp.shape.top_k, h, out.data_ptr(), None, None, 1, self.st_x)
+            if self.hooks:
+                self.hooks.after_forward(m, xs)
+
+    def dout_dispatch(self, m, dout):
+        """Backward K3: the raw dout rows follow the forward permutation."""
+        dp, xs = self.dp, self.xs
+        h = dp.shape.hidden
+        with dp._timed(dp.remote_rows(m)[0] * 2 * h, "comm_dout_dispatch", xs):
+            dp._k("mb_scatter_rows", dout.data_ptr(), dp.T, dp.shape.top_k, h, dp.perm[m].data_ptr(),
+                  dp.ptr_dyr[m].data_ptr(), self.st_x)
+            dp.arena.barrier(xs)  # dout rows of micro-batch m have landed everywhere
+
+    def unpermute(self, m, dx, dgate):
+        """X(m): dX un-permute (sum over the k copies) + dgate gather."""
+        dp, xs = self.dp, self.xs
+        h = dp.shape.hidden
+        with dp._timed(dp.remote_rows(m)[0] * 2 * h, "comm_unpermute", xs):
+            dp.arena.barrier(xs)  # dX rows / dgate partials of micro-batch m complete everywhere
+            dp._k("mb_combine_rows", dp.ptr_dxp[m].data_ptr(), dp.perm[m].data_ptr(), None, dp.T, dp.shape.top_k, h,
+                  dx.data_ptr(), dp.ptr_dgate[m].data_ptr(), dgate.data_ptr(), dp.npart, self.st_x)
+            if self.hooks:
+                self.hooks.after_backward(m, xs)
+
+    # -------------------------------------------------------------- compute stream
+    def fwd_gemms(self, m):
+        """F(m): gate/up GEMM + SwiGLU, down GEMM."""
+        dp = self.dp
+        h, hp = dp.shape.hidden, dp.shape.ffn
+        ng = dp.nslots[m]
+        if ng:
+            g = dp.groups[m][:ng]
+            rows = dp.real_rows(m)
+            with dp._timed(4.0 * rows * h * hp, "fwd_swiglu"):
+                K.grouped_gemm(K.GEMM_FWD_SWIGLU, dp.Xr[m], dp.W1, g, N=2 * hp, K=h, C=dp.H[m], C2=dp.Act[m],
+                               B1=dp.W1r[m])
+            with dp._timed(2.0 * rows * h * hp, "fwd_down"):
+                K.grouped_gemm(K.GEMM_FWD_STORE, dp.Act[m], dp.W2, g, N=h, K=hp, C=dp.Y[m], B1=dp.W2r[m])
+            dp.launches += 2
+
+    def bwd_gemms(self, m):
+        """B(m): dAct with the combine backward + dSwiGLU fused in its epilogue, then dX."""
+        dp = self.dp
+        h, hp = dp.shape.hidden, dp.shape.ffn
+        ng = dp.nslots[m]
+        if ng:
+            g = dp.groups[m][:ng]
+            rows = dp.real_rows(m)
+            # dAct = dout.W2 with the combine backward fused in the epilogue: gate applied per row,
+            # dgate partials <dout.W2, act> = <dout, Y>, gate*act written over Act for dW2
+            with dp._timed(2.0 * rows * h * hp, "dgrad_act_gated"):
+                K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU_GATED, dp.dYr[m], dp.W2, g, N=hp, K=h, C=dp.dH[m],
+                               C2=dp.Act[m], aux=dp.H[m], B1=dp.W2r[m], row_scale=dp.gate_r[m],
+                               row_partial=dp.dgate_r[m])
+            with dp._timed(4.0 * rows * h * hp, "dgrad_x"):
+                K.grouped_gemm(K.GEMM_DGRAD_STORE, dp.dH[m], dp.W1, g, N=h, K=2 * hp, C=dp.dXp[m], B1=dp.W1r[m])
+            dp.launches += 2
+
+    def finish(self):
+        """Weight gradients over every micro-batch (compute stream) in two parts; the replica
+        gradient reduce (comm stream) starts once part A (replica groups + their owners'
+        experts) is done and overlaps part B; then both streams join the current stream."""
+        dp, cs, xs = self.dp, self.cs, self.xs
+        h, hp = dp.shape.hidden, dp.shape.ffn
+        fresh = dp._wgrad_prepare()
+        dp._wgrad(dp.wparts[0], fresh)
+        ev = torch.cuda.Event()
+        ev.record(cs)
+        if len(dp.wparts) > 1:
+            dp._wgrad(dp.wparts[1], fresh)
+        xs.wait_event(ev)
+        if dp.world > 1:  # collective: every rank runs both barriers, with or without replicas
+            mn1, mn2 = 2 * hp * h, h * hp
+            with dp._timed(sum(n for _, _, _, n in dp.reduce) * (mn1 + mn2) * 4, "comm_replica_grad_reduce", xs):
+                dp.arena.barrier(xs)  # every rank's replica gradients are complete
+                for loc, p1, p2, n in dp.reduce:
+                    dp._k("mb_accumulate_f32", dp.gW1[loc].data_ptr(), p1.data_ptr(), n, mn1, self.st_x)
+                    dp._k("mb_accumulate_f32", dp.gW2[loc].data_ptr(), p2.data_ptr(), n, mn2, self.st_x)
+                dp.arena.barrier(xs)  # peers finished reading our replica gradients
+        cs.wait_stream(xs)
+
+
+class MoELayerFunction(torch.autograd.Function):
+    """torch.autograd entry for one micro-batch of a MoEDataPlane step:
+
+        dp.begin_step()
+        outs = [MoELayerFunction.apply(x[m], gates[m], dp, idx[m], m) for m in range(MB)]
+        ... loss.backward()        # runs backward_mb for every micro-batch
+        dp.end_step()              # weight gradients + replica-gradient reduce into dp.gW1 / gW2
+
+    Differentiable in x ([T, h] bf16) and gates ([T, k] fp32); the expert weight gradients
+    accumulate inside the data plane (fp32, all micro-batches of the step in one contraction).
+    Every rank must run the same micro-batches in the same order (collective barriers)."""
+
+    @staticmethod
+    def forward(ctx, x, gates, dp, idx, m):
+        out = torch.empty_like(x)
+        dp.forward_mb(m, x.contiguous(), idx.contiguous(), gates.contiguous(), out)
+        ctx.dp, ctx.m = dp, m
+        ctx.k = idx.shape[-1]
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        dp, m = ctx.dp, ctx.m
+        dx = torch.empty_like(dout)
+        dgate = torch.empty(dout.shape[0], ctx.k, dtype=torch.float32, device=dout.device)
+        dp.backward_mb(m, dout.contiguous(), dx, dgate)
+        return dx, dgate, None, None, None
