@@ -590,7 +590,8 @@ class MoEDataPlane:
         """One training step of the layer over MB micro-batches (inputs [MB, T, ...] on device).
         Writes out / dx / dgate and accumulates fp32 expert gradients.  Asynchronous with respect
         to the host; the current stream is ordered after all of it on return.  `hooks` (optional)
-        gets inputs_ready(m, stream), after_forward(m, stream), after_backward(m, stream).
+        gets inputs_ready(m, stream) (x, idx, gates of micro-batch m), optional dout_ready(m, stream),
+        after_forward(m, stream), after_backward(m, stream).
         Runs the two-micro-batch-overlap schedule (schedule()); the same phases are available one
         micro-batch at a time through begin_step / forward_mb / backward_mb / end_step."""
         ops = _StepOps(self, hooks)
@@ -712,19 +713,30 @@ class MoEDataPlane:
             self._h2d = torch.cuda.Stream(device=self.device)
             self._d2h = torch.cuda.Stream(device=self.device)
         h2d, d2h = self._h2d, self._d2h
-        ready = []
+        ready, dready = {}, {}
         h2d.wait_stream(cur)
+        # copy order follows the schedule's needs: the forward inputs of micro-batch m + 1 go
+        # before the dout of micro-batch m (D(m+1) is issued before C(m))
+        order = []
+        for m in range(self.MB):
+            order.append(("f", m))
+            if m >= 1:
+                order.append(("b", m - 1))
+        order.append(("b", self.MB - 1))
         with torch.cuda.stream(h2d):
-            for m in range(self.MB):
-                for key in ("x", "idx", "gates", "dout"):
+            for kind, m in order:
+                for key in (("x", "idx", "gates") if kind == "f" else ("dout",)):
                     dev[key][m].copy_(host[key][m], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(h2d)
-                ready.append(ev)
+                (ready if kind == "f" else dready)[m] = ev
 
         class _Hooks:
             def inputs_ready(self, m, stream):
                 stream.wait_event(ready[m])
+
+            def dout_ready(self, m, stream):
+                stream.wait_event(dready[m])
 
             def after_forward(self, m, stream):
                 d2h.wait_stream(stream)
@@ -820,6 +832,8 @@ class _StepOps:
         dp, xs = self.dp, self.xs
         h = dp.shape.hidden
         with dp._timed(dp.remote_rows(m)[0] * 2 * h, "comm_dout_dispatch", xs):
+            if self.hooks and hasattr(self.hooks, "dout_ready"):
+                self.hooks.dout_ready(m, xs)
             dp._k("mb_scatter_rows", dout.data_ptr(), dp.T, dp.shape.top_k, h, dp.perm[m].data_ptr(),
                   dp.ptr_dyr[m].data_ptr(), self.st_x)
             dp.arena.barrier(xs)  # dout rows of micro-batch m have landed everywhere
