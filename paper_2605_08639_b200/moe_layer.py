@@ -18,9 +18,10 @@ One process per GPU; every rank runs, per step of MB micro-batches:
 Two streams: the compute stream runs the GEMMs, the comm stream runs dispatch / combine and
 every device barrier (totally ordered per rank), linked by per-micro-batch events, so the
 NVLink all-to-all of one micro-batch overlaps the tensor-core work of another (two micro-batches
-in flight, see schedule()).  Routing is
-replayed, so every count, row offset and replica is known before the step: the host planners
-run once per step (StepPlan) and the kernels never exchange sizes.
+in flight, see schedule()).  Routing is replayed, so every count, row offset and replica is known
+before the step: the host planners run once per step (StepPlan) and the kernels never exchange
+sizes.  The same phases run one micro-batch at a time through begin_step / forward_mb /
+backward_mb / end_step and the MoELayerFunction autograd entry.
 """
 
 from __future__ import annotations
@@ -40,6 +41,8 @@ from .cluster import ClusterTopology, HardwareProfile
 from .comm import Comm, SymmetricArena
 
 PAD = 128       # receive-slot row padding = GEMM M tile
+# profiling only: skip the row movers (the GEMMs then run on stale / zero rows, which also draws
+# less power -- do not read the result as the movers' cost)
 _SKIP_ROWS = os.environ.get("MB_PROFILE_SKIP_ROWS", "0") == "1"
 # SMs left to the comm stream while the persistent GEMM runs (measured on B200, qwen3 shape:
 # N=4 step 24.1 ms with all 148 SMs in the GEMM, 19.7 ms with 28 left free)
