@@ -331,9 +331,17 @@ def run_ours(args, comm):
         topo, group = trace.topo, trace.topo.gpus_per_node
         model = ModelProfile(1, shape.num_experts, shape.top_k, shape.hidden, shape.ffn)
         cfg = {"shape": shape, "shift": 0, "slots": slots, "group": group}
-        args.tokens, args.micro_batches = trace.tokens_per_gpu, trace.num_micro_batches
+        args.micro_batches = trace.num_micro_batches
+        trace_mats = trace.matrices.astype(np.int64)
         if args.plans:
             bundle = planio.load_plan_bundle(args.plans, trace)
+            if bundle.sample_placement is not None:
+                # data-locality placement: samples (and their tokens) start on their new GPUs
+                from paper_2605_08639_b200.reordering import rewrite_trace_matrices
+                trace_mats = rewrite_trace_matrices(trace, bundle.sample_placement).astype(np.int64)
+        # token buffers hold the largest (micro-batch, GPU) row; shorter rows are padded with
+        # dropped tokens (idx -1: no histogram count, no dispatch, zero output)
+        args.tokens = int(trace_mats[:, args.trace_layer].sum(axis=-1).max()) // shape.top_k
     T, MB = args.tokens, args.micro_batches
 
     def routing_for(balanced):
@@ -342,16 +350,18 @@ def run_ours(args, comm):
         if trace is not None and not balanced:
             from paper_2605_08639_b200.traces import realize_tokens
             from paper_2605_08639_b200.workload import Routing
-            rows = [realize_tokens(trace.matrices[m, args.trace_layer, rank], shape.top_k, seed=m * world + rank)
-                    for m in range(MB)]
-            r = Routing(idx=np.stack([a for a, _ in rows]), gates=np.stack([b for _, b in rows]), mats=None)
+            idx = np.full((MB, T, shape.top_k), -1, dtype=np.int32)
+            gts = np.zeros((MB, T, shape.top_k), dtype=np.float32)
+            for m in range(MB):
+                i_m, g_m = realize_tokens(trace_mats[m, args.trace_layer, rank], shape.top_k, seed=m * world + rank)
+                idx[m, :len(i_m)], gts[m, :len(g_m)] = i_m, g_m
+            r = Routing(idx=idx, gates=gts, mats=None)
         else:
             r = make_routing(shape, T, MB, world, rank, zipf_s=args.zipf, shift=cfg["shift"], balanced=balanced,
                              all_ranks=False)
         counts, _ = expert_histogram(torch.from_numpy(r.idx).cuda(), shape.num_experts)
         r.mats = gather_routing(comm, counts.cpu().numpy().astype(np.int64))
-        if trace is not None and not balanced and not np.array_equal(
-                r.mats, trace.matrices[:, args.trace_layer].astype(np.int64)):
+        if trace is not None and not balanced and not np.array_equal(r.mats, trace_mats[:, args.trace_layer]):
             raise RuntimeError("device histogram of the realised tokens differs from the trace counts")
         return r
 

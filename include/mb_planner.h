@@ -47,6 +47,17 @@ int mbp_anneal_reorder(const double* x, int32_t nodes, int32_t gpn, int32_t E, i
                        double cooling, double eps_frac, double term_eps, double beta, const int64_t* extra,
                        int32_t nextra, int32_t threads, int64_t* assignment, int64_t* iterations);
 
+/* Data-locality sample placement (reorder.py:365-568): greedy_sample_initial (greedy_only != 0)
+ * or anneal_sample_placement (greedy start, one swap-SA chain per seed over samples inside each
+ * micro-batch's +/-band token window, best exact summed T_MoE).  counts [S][L][E] (float64 of
+ * the u32 sample counts), micro_batch[S], source_gpu[S], tokens[S], plans [L][E]; out placement[S]. */
+int mbp_sample_placement(int32_t nodes, int32_t gpn, int32_t E, int32_t L, int32_t MB, int32_t S, const double* counts,
+                         const int32_t* micro_batch, const int64_t* source_gpu, const double* tokens,
+                         const int64_t* plans, int64_t hidden, int64_t inter, double flops, double bw_nv,
+                         double bw_rd, double bpt, const uint64_t* seeds, int32_t nseeds, double cooling,
+                         double eps_frac, double term_eps, double beta, double band, int32_t greedy_only,
+                         int32_t threads, int64_t* placement);
+
 /* costmodel.compute_loads (costmodel.py:127-158) -> loads[5][G] = comp, nvlink_tx, nvlink_rx,
  * rdma_tx, rdma_rx; optional flow[G][G] (costmodel.flow_matrix, costmodel.py:91-108).
  * Splits: nsplit experts split_expert[], copies CSR split_ptr/split_gpus, fractions concatenated. */

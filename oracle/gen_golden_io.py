@@ -25,6 +25,7 @@ CASES = {
     #        samples_per_gpu, seed, solve seeds, replica slots)
     "small": (2, 2, 16, 2, 3, 2, 256, 3, 0.5, 0.0, 0, 5, 4, 2),
     "samples": (2, 2, 8, 1, 2, 2, 64, 2, 0.3, 0.4, 4, 11, 2, 1),
+    "samples2": (2, 2, 16, 2, 3, 2, 128, 3, 0.5, 0.3, 6, 21, 3, 2),
 }
 
 
@@ -48,6 +49,10 @@ def main():
         rc = cli.main(["solve", "--trace", str(tdir), "--out", str(pdir), "--seeds", str(seeds),
                        "--replica-slots", str(slots), "--threads", "1"])
         assert rc == 0
+        if spg > 0:  # data-locality sample placement (reorder.py:365-568) as well
+            rc = cli.main(["solve", "--trace", str(tdir), "--out", str(OUT / name / "plans_sl"), "--seeds",
+                           str(seeds), "--replica-slots", str(slots), "--threads", "1", "--sample-locality"])
+            assert rc == 0
         trace = rt.load_trace(tdir)
         meta[name] = {"trace_id": trace.trace_id(), "seeds": seeds, "replica_slots": slots,
                       "shape": list(trace.matrices.shape)}

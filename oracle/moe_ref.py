@@ -13,8 +13,11 @@ import torch
 # ----------------------------------------------------------------------------- integer path
 
 def histogram(idx: np.ndarray, num_experts: int) -> np.ndarray:
-    """x[e] = #{(t,i): idx[t,i] == e}: one row of RoutingTrace.matrices (routing.py:151-168)."""
-    return np.bincount(np.asarray(idx, dtype=np.int64).ravel(), minlength=num_experts).astype(np.int64)
+    """x[e] = #{(t,i): idx[t,i] == e}: one row of RoutingTrace.matrices (routing.py:151-168).
+    Entries outside [0, E) (dropped choices, idx = -1) are not counted."""
+    v = np.asarray(idx, dtype=np.int64).ravel()
+    v = v[(v >= 0) & (v < num_experts)]
+    return np.bincount(v, minlength=num_experts).astype(np.int64)
 
 
 def copies_of(e: int, home, replicas: dict) -> list:
@@ -76,13 +79,17 @@ def executed_flow(x: np.ndarray, home, replicas: dict, counts: dict) -> np.ndarr
 def canonical_permutation(idx: np.ndarray, j: int, x: np.ndarray, home, replicas: dict, counts: dict,
                           row_base: dict) -> np.ndarray:
     """perm[t, i] = (dst GPU, dst row) for source GPU j, (t, i) enumerated row-major; the
-    stable rank r of (t, i) among j's entries of expert e picks copy c = min{c: r < cum[c]}."""
+    stable rank r of (t, i) among j's entries of expert e picks copy c = min{c: r < cum[c]}.
+    Dropped choices (idx outside [0, E)) map to (-1, -1)."""
     t_n, k = idx.shape
+    num_experts = len(home)
     perm = np.full((t_n, k, 2), -1, dtype=np.int32)
     seen = {}
     for t in range(t_n):
         for i in range(k):
             e = int(idx[t, i])
+            if not 0 <= e < num_experts:
+                continue
             r = seen.get(e, 0)
             seen[e] = r + 1
             cnt = split_counts(x, home, replicas, counts, j, e)
@@ -106,6 +113,8 @@ def canonical_permutation_fast(idx: np.ndarray, j: int, x, home, replicas, count
     rank[order] = np.arange(flat.size) - starts
     out = np.full((flat.size, 2), -1, dtype=np.int64)
     for e in np.unique(flat):
+        if not 0 <= e < len(home):
+            continue  # dropped choice
         sel = flat == e
         r = rank[sel]
         cnt = np.asarray(split_counts(x, home, replicas, counts, j, int(e)))

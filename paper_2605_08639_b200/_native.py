@@ -71,6 +71,9 @@ _PLANNER_SIGS: dict = {
     "mbp_anneal_reorder": (c_int, [c_vp, c_i32, c_i32, c_i32, c_i64, c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_vp,
                                    c_i32, c_dbl, c_dbl, c_dbl, c_dbl, c_vp, c_i32, c_i32, c_vp, c_vp]),
     "mbp_compute_loads": (c_int, [c_vp, c_i32, c_i32, c_i32, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "mbp_sample_placement": (c_int, [c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64,
+                                     c_i64, c_dbl, c_dbl, c_dbl, c_dbl, c_vp, c_i32, c_dbl, c_dbl, c_dbl, c_dbl,
+                                     c_dbl, c_i32, c_i32, c_vp]),
     "mbp_greedy_replicate": (c_int, [c_vp, c_i32, c_i32, c_i32, c_vp, c_i64, c_i64, c_dbl, c_dbl, c_dbl, c_dbl,
                                      c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "mbp_solve_token_split": (c_int, [c_vp, c_i32, c_i32, c_i32, c_vp, c_i64, c_i64, c_dbl, c_dbl, c_dbl, c_dbl,

@@ -89,6 +89,20 @@ extern "C" int mbp_anneal_reorder(const double* x, int32_t nodes, int32_t gpn, i
                               nextra, threads, assignment, iterations);)
 }
 
+extern "C" int mbp_sample_placement(int32_t nodes, int32_t gpn, int32_t E, int32_t L, int32_t MB, int32_t S,
+                                    const double* counts, const int32_t* micro_batch, const int64_t* source_gpu,
+                                    const double* tokens, const int64_t* plans, int64_t hidden, int64_t inter,
+                                    double flops, double bw_nv, double bw_rd, double bpt, const uint64_t* seeds,
+                                    int32_t nseeds, double cooling, double eps_frac, double term_eps, double beta,
+                                    double band, int32_t greedy_only, int32_t threads, int64_t* placement) {
+  if (int rc = check_topo(nodes, gpn)) return rc;
+  if (S < 0 || L < 1 || MB < 1 || E < 1) return fail(kInvalid, "bad sample-placement dimensions");
+  if (!greedy_only && nseeds < 1) return fail(kInvalid, "need at least one annealing seed");
+  GUARD(Topo t(nodes, gpn); Hw hw{flops, bw_nv, bw_rd, bpt};
+        return anneal_samples(t, E, L, MB, S, counts, micro_batch, source_gpu, tokens, plans, hidden, inter, hw, seeds,
+                              nseeds, cooling, eps_frac, term_eps, beta, band, greedy_only, threads, placement);)
+}
+
 extern "C" int mbp_compute_loads(const double* x, int32_t nodes, int32_t gpn, int32_t E, const int64_t* placement,
                                  int32_t nsplit, const int32_t* split_expert, const int32_t* split_ptr,
                                  const int32_t* split_gpus, const double* split_frac, double* loads, double* flow) {

@@ -62,6 +62,10 @@ struct SplitFr {
 
 void static_plan(int E, int G, int64_t* out);
 void lpt_initial(const double* x, int G, int E, int64_t* out);
+int anneal_samples(const Topo& t, int E, int L, int MB, int S, const double* counts, const int32_t* mb_of,
+                   const int64_t* source, const double* tokens, const int64_t* plans, int64_t h, int64_t hp,
+                   const Hw& hw, const uint64_t* seeds, int nseeds, double cooling, double eps_frac, double term_eps,
+                   double beta, double band, int greedy_only, int threads, int64_t* out);
 int anneal_reorder(const double* x, const Topo& t, int E, int64_t h, int64_t hp, const Hw& hw, const uint64_t* seeds,
                    int nseeds, double cooling, double eps_frac, double term_eps, double beta, const int64_t* extra,
                    int nextra, int threads, int64_t* out, int64_t* iters_total);

@@ -6,9 +6,9 @@ replication.json  per (micro_batch, layer): replica list, split rows (source_gpu
                   serving_gpu, fraction) and the objective (replicate.py:539-578)
 
 `solve` is the reference CLI's `solve` command (cli.py:124-185) on this package's native
-planners: the files it writes are byte-identical to the reference's for the same trace and
-options (tests/test_io_golden.py).  Sample-locality placement (reorder.py:365-627) is out of scope
-(SURVEY.md section 8f.3).
+planners, including the data-locality sample placement (--sample-locality, reorder.py:365-568):
+the files it writes are byte-identical to the reference's for the same trace and options
+(tests/test_io_golden.py).
 """
 
 from __future__ import annotations
@@ -140,9 +140,10 @@ def load_plan_bundle(plans_dir, trace: rt.RoutingTrace) -> sim.PlanBundle:
 
 def solve(trace: rt.RoutingTrace, out_dir, seeds: int = 16, cooling: float = 0.9995, eps_frac: float = 1e-3,
           eps: float | None = None, beta: float = 20.0, replica_slots: int = 2, seed: int = 0,
-          threads: int = 0) -> sim.PlanBundle:
-    """Inter-batch reorder per layer, then intra-batch replication per (micro-batch, layer), and
-    write reorder.json / replication.json (cli.py:124-185, without --sample-locality)."""
+          threads: int = 0, sample_locality: bool = False) -> sim.PlanBundle:
+    """Inter-batch reorder per layer, optional data-locality sample placement, then intra-batch
+    replication per (micro-batch, layer) on the (rewritten) matrices; writes reorder.json /
+    replication.json (cli.py:124-185)."""
     topo, model, hw = trace.topo, trace.model, trace.topo.profile
     cfg = ro.AnnealConfig(seeds=chain_seeds(seed, seeds), cooling_rate=cooling, termination_eps=eps,
                           eps_frac=eps_frac, beta=beta)
@@ -158,7 +159,13 @@ def solve(trace: rt.RoutingTrace, out_dir, seeds: int = 16, cooling: float = 0.9
         est = cm.moe_time(cm.compute_loads(agg, plan.assignment, topo), model, hw, smoothing=smoothing)
         plans.append(plan)
         objectives.append({"exact": est.t_moe, "smoothed": est.t_moe_smoothed})
-    matrices = trace.matrices.astype(np.float64)
+    placement = None
+    if sample_locality:
+        if trace.samples is None:
+            raise ValueError("--sample-locality needs a trace with a sample table")
+        placement = ro.anneal_sample_placement(trace, plans, topo, model, hw, cfg, threads=nthreads)
+    matrices = (ro.rewrite_trace_matrices(trace, placement) if placement is not None
+                else trace.matrices.astype(np.float64))
     replica_cfg = rep.ReplicaConfig(slots_per_gpu=replica_slots)
     replication = rep.ReplicationPlan()
     tasks = []
@@ -173,8 +180,8 @@ def solve(trace: rt.RoutingTrace, out_dir, seeds: int = 16, cooling: float = 0.9
                                                 splits=split.to_split_map(pl)), model, hw).t_moe
         replication.entries[(mb, layer)] = rep.ReplicationEntry(pl, split, achieved)
     config_echo = {"seeds": seeds, "cooling": cooling, "eps_frac": eps_frac, "eps": eps, "beta": beta,
-                   "replica_slots": replica_slots, "seed": seed, "sample_locality": False}
+                   "replica_slots": replica_slots, "seed": seed, "sample_locality": bool(sample_locality)}
     tid = trace.trace_id()
-    save_reorder_plan(out / "reorder.json", tid, plans, objectives, None, config_echo)
+    save_reorder_plan(out / "reorder.json", tid, plans, objectives, placement, config_echo)
     save_replication_plan(out / "replication.json", tid, replication)
-    return sim.PlanBundle(reorder=plans, sample_placement=None, replication=replication)
+    return sim.PlanBundle(reorder=plans, sample_placement=placement, replication=replication)

@@ -121,13 +121,84 @@ def anneal_reorder(x_batch, topo: ClusterTopology, model, hw: HardwareProfile, c
     return ReorderPlan(out)
 
 
+def _sample_call(trace, plans, topo, model, hw, cfg, band, greedy_only, beta, threads):
+    if trace.samples is None:
+        raise ValueError("trace has no sample table")
+    s = trace.samples
+    L, E = trace.model.num_layers, trace.model.num_experts
+    if len(plans) != L:
+        raise ValueError(f"need one expert plan per layer ({L}), got {len(plans)}")
+    counts = nat.f64(np.asarray(s.counts, dtype=np.float64).reshape(s.num_samples, L, E))
+    mb = nat.i32(s.micro_batch)
+    src = nat.i64(s.source_gpu)
+    tok = nat.f64(np.asarray(s.tokens, dtype=np.float64))
+    pl = nat.i64(np.stack([np.asarray(p.assignment) for p in plans]))
+    seeds = np.ascontiguousarray([int(x) for x in (cfg.seeds if cfg else (0,))], dtype=np.uint64)
+    out = np.zeros(s.num_samples, dtype=np.int64)
+    lib = nat.planner()
+    nat.check(lib.mbp_sample_placement(
+        topo.num_nodes, topo.gpus_per_node, E, L, trace.num_micro_batches, s.num_samples, nat.ptr(counts),
+        nat.ptr(mb), nat.ptr(src), nat.ptr(tok), nat.ptr(pl), model.hidden_size, model.intermediate_size,
+        hw.flops_per_gpu, hw.bw_nvlink, hw.bw_rdma, hw.bytes_per_token, nat.ptr(seeds), len(seeds),
+        cfg.cooling_rate if cfg else 0.5, cfg.eps_frac if cfg else 1e-3,
+        (cfg.termination_eps if cfg and cfg.termination_eps is not None else -1.0), beta, band,
+        1 if greedy_only else 0, threads if threads is not None else (os.cpu_count() or 1), nat.ptr(out)),
+        lib, "sample_placement")
+    return SamplePlacement(source_gpu=out)
+
+
+def greedy_sample_initial(trace, plans: Sequence[ReorderPlan], topo: ClusterTopology, model, hw: HardwareProfile,
+                          beta: float = 20.0, band: float = 0.10) -> SamplePlacement:
+    """Longest-first greedy sample placement within the token band (reorder.py:457-487)."""
+    return _sample_call(trace, plans, topo, model, hw, None, band, True, beta, 1)
+
+
+def anneal_sample_placement(trace, plans: Sequence[ReorderPlan], topo: ClusterTopology, model, hw: HardwareProfile,
+                            cfg: AnnealConfig, band: float = 0.10, threads: int | None = None) -> SamplePlacement:
+    """Second annealing round: swap sample source GPUs under fixed expert plans; never worse
+    than the greedy start in summed exact time (reorder.py:537-568).  `threads` (extension):
+    chain parallelism, default all cores."""
+    return _sample_call(trace, plans, topo, model, hw, cfg, band, False, cfg.beta, threads)
+
+
 def apply_plan(x, plan: ReorderPlan, placement: SamplePlacement | None = None, trace=None,
                micro_batch: int | None = None, layer: int | None = None) -> np.ndarray:
-    """Expert relocation never changes matrix values (reorder.py:575-607); sample relocation
-    (data-locality placement) is out of scope for this build."""
+    """One routing matrix under an expert plan and sample placement (reorder.py:575-607): expert
+    relocation never changes matrix values; relocated samples move their counts between sources."""
     x = np.asarray(x, dtype=np.float64)
     if x.shape[1] != len(plan.assignment):
         raise ValueError(f"matrix has {x.shape[1]} experts, plan covers {len(plan.assignment)}")
-    if placement is not None:
-        raise NotImplementedError("sample relocation (reorder.py:365-627) is outside the data-plane scope")
-    return x.copy()
+    out = x.copy()
+    if placement is None:
+        return out
+    if trace is None or trace.samples is None or micro_batch is None or layer is None:
+        raise ValueError("sample relocation requires the trace with samples plus micro_batch and layer")
+    s = trace.samples
+    for i in np.flatnonzero(s.micro_batch == micro_batch):
+        src, dst = int(s.source_gpu[i]), int(placement.source_gpu[i])
+        if src == dst:
+            continue
+        counts = s.counts[i, layer].astype(np.float64)
+        out[src] -= counts
+        out[dst] += counts
+    if out.min() < 0:
+        raise ValueError("sample relocation produced negative counts; matrix does not match the trace")
+    return out
+
+
+def rewrite_trace_matrices(trace, placement: SamplePlacement) -> np.ndarray:
+    """All (MB, L, G, E) matrices with sample rows moved to their new sources (reorder.py:610-627)."""
+    s = trace.samples
+    if s is None:
+        raise ValueError("trace has no sample table")
+    out = trace.matrices.astype(np.float64).copy()
+    for i in range(s.num_samples):
+        src, dst = int(s.source_gpu[i]), int(placement.source_gpu[i])
+        if src == dst:
+            continue
+        counts = s.counts[i].astype(np.float64)  # (L, E)
+        out[int(s.micro_batch[i]), :, src, :] -= counts
+        out[int(s.micro_batch[i]), :, dst, :] += counts
+    if out.min() < 0:
+        raise ValueError("sample relocation produced negative counts")
+    return out

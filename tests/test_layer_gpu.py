@@ -132,3 +132,51 @@ def test_per_micro_batch_api_and_autograd_match_fused_step():
         assert torch.equal(xs[m].grad, dx[m]) and torch.equal(gs[m].grad, dgate[m])
     assert torch.equal(dp.gW1[:dp.M], g1) and torch.equal(dp.gW2[:dp.M], g2)
     dp.close()
+
+
+def test_dropped_token_choices():
+    """Choices with idx = -1 (capacity-dropped, or padding of a short micro-batch) are not
+    counted, not dispatched and contribute nothing; the rest of the layer matches the oracle."""
+    cfg = SHAPES["qwen3-30b-a3b"]
+    shape = cfg["shape"]
+    T, MB = 384, 1
+    routing = make_routing(shape, T, MB, 1, 0, zipf_s=1.0, shift=cfg["shift"])
+    rng = np.random.default_rng(3)
+    drop = rng.random(routing.idx.shape) < 0.1
+    drop[:, -32:, :] = True          # a fully dropped tail (padding tokens)
+    routing.idx[drop] = -1
+    routing.gates[drop] = 0.0
+    routing.mats = np.stack([moe_ref.histogram(routing.idx[m], shape.num_experts) for m in range(MB)])[:, None]
+    topo = build_topology(1, 1, b200_profile(shape.hidden))
+    model = ModelProfile(1, shape.num_experts, shape.top_k, shape.hidden, shape.ffn)
+    # the planners' trace format needs row sums divisible by k: plan on the kept choices only
+    plan = build_step_plan("static", routing.mats, topo, model, topo.profile, SimConfigs(replica=ReplicaConfig(0)),
+                           shape) if routing.mats.sum() % shape.top_k == 0 else None
+    if plan is None:
+        keep = int(routing.mats.sum() % shape.top_k)
+        flat = routing.idx.reshape(-1)
+        nz = np.flatnonzero(flat >= 0)[-keep:]
+        flat[nz] = -1
+        routing.mats = np.stack([moe_ref.histogram(routing.idx[m], shape.num_experts) for m in range(MB)])[:, None]
+        plan = build_step_plan("static", routing.mats, topo, model, topo.profile,
+                               SimConfigs(replica=ReplicaConfig(0)), shape)
+    dp = MoEDataPlane(Comm(), shape, T, MB, plan)
+    wg, wu, wd = make_weights(shape)
+    dp.set_weights(wg.cuda(), wu.cuda(), wd.cuda())
+    dp.zero_grads()
+    x, dout = make_activations(shape, T, MB, 0)
+    x, dout = x.cuda(), dout.cuda()
+    idx = torch.from_numpy(routing.idx).cuda()
+    gates = torch.from_numpy(routing.gates).cuda()
+    out, dx = torch.empty_like(x), torch.empty_like(x)
+    dgate = torch.empty(MB, T, shape.top_k, dtype=torch.float32, device="cuda")
+    dp.step(x, idx, gates, dout, out, dx, dgate)
+    torch.cuda.synchronize()
+    assert np.array_equal(dp.counts[0].cpu().numpy(), moe_ref.histogram(routing.idx[0], shape.num_experts))
+    assert bool((dp.perm[0].cpu().numpy()[routing.idx[0] < 0] == -1).all())
+    ref = moe_ref.moe_layer_fp32(x[0], idx[0], gates[0], wg.cuda(), wu.cuda(), wd.cuda(), dout[0])
+    assert moe_ref.rel_err(out[0], ref["out"]) < TOL
+    assert moe_ref.rel_err(dx[0], ref["dx"]) < TOL
+    assert moe_ref.rel_err(dgate[0], ref["dgate"]) < TOL
+    assert torch.all(out[0, -32:] == 0) and torch.all(dx[0, -32:] == 0)
+    dp.close()
