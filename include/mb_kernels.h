@@ -38,9 +38,9 @@ int mb_set_gemm_sms(int sms);
  * tcgen05/TMEM/TMA persistent grouped GEMM (bf16 in, fp32 accumulate).
  * Replaces: costmodel.comp_time (costmodel.py:161-163), the modelled 6*h*h' FLOP/token expert
  * FFN ("three GEMMs").  groups: device array of
- * struct {int32 rows, a0, slot, flags, seg_begin, seg_count, pad, pad}; segs (W mode only, may be
- * NULL): device array of struct {int32 a0, rows} K-segments, so one wgrad launch can contract
- * over every micro-batch of the step.                                                         */
+ * struct {int32 rows, a0, slot, flags, seg_begin, seg_count, rows_real, kblocks}; segs (W mode
+ * only, may be NULL): device array of struct {int32 a0, rows} K-segments (rows a multiple of 16,
+ * kblocks = sum of ceil(rows / 64)), so one wgrad launch can contract over every micro-batch.                                                         */
 enum {
   MB_GEMM_FWD_STORE = 0,     /* C[rows_g,N] = A[rows_g,K] . B_slot[N,K]^T           (Y = Act W2^T) */
   MB_GEMM_FWD_SWIGLU = 1,    /* as above, epilogue C=H, C2=silu(gate)*up             (H = X W1^T)   */
@@ -48,7 +48,7 @@ enum {
   MB_GEMM_DGRAD_DSWIGLU = 3, /* as above, epilogue SwiGLU backward with aux=H -> C=dH (dAct = dY W2) */
   MB_GEMM_WGRAD = 4,         /* C_slot[M,N] (+)= A[K_g,M]^T . B[K_g,N]               (dW)           */
   MB_GEMM_DGRAD_DSWIGLU_GATED = 5 /* A = raw dout rows; epilogue applies row_scale (gate): C = dH,
-                                     C2 = gate*act, row_partial[row][N/128] = partial <dout.W2, act>
+                                     C2 = gate*act, row_partial[row][N/64] = partial <dout.W2, act>
                                      whose sum is dgate = <dout, Y> (replaces the combine backward) */
 };
 /* mode | 0x100 forces the 1-CTA kernel (default: CTA-pair 256x256 tiles when the shape allows). */
