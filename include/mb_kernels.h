@@ -40,7 +40,7 @@ int mb_set_gemm_sms(int sms);
  * FFN ("three GEMMs").  groups: device array of
  * struct {int32 rows, a0, slot, flags, seg_begin, seg_count, rows_real, kblocks}; segs (W mode
  * only, may be NULL): device array of struct {int32 a0, rows} K-segments (rows a multiple of 16,
- * kblocks = sum of ceil(rows / 64)), so one wgrad launch can contract over every micro-batch.                                                         */
+ * kblocks = sum of ceil(rows / 64)), so one wgrad launch can contract over every micro-batch. */
 enum {
   MB_GEMM_FWD_STORE = 0,     /* C[rows_g,N] = A[rows_g,K] . B_slot[N,K]^T           (Y = Act W2^T) */
   MB_GEMM_FWD_SWIGLU = 1,    /* as above, epilogue C=H, C2=silu(gate)*up             (H = X W1^T)   */
