@@ -187,6 +187,7 @@ def run_reference(args, rank, world):
 
 def measure_policy(args, comm, policy, shape, cfg, routing, topo, model, cfgs, want_detail, bundle=None):
     import torch
+    from paper_2605_08639_b200.comm import local_device
     from paper_2605_08639_b200.moe_layer import MoEDataPlane, build_step_plan, plan_digest
     from paper_2605_08639_b200.workload import make_activations, make_weights_for
     rank, world = comm.rank, comm.world
@@ -224,7 +225,7 @@ def measure_policy(args, comm, policy, shape, cfg, routing, topo, model, cfgs, w
         step()
     torch.cuda.synchronize()
     comm.host_barrier()
-    sampler = ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) if want_detail else None
+    sampler = ClockSampler(local_device()) if want_detail else None
     if sampler:
         sampler.start()
         time.sleep(0.15)
@@ -244,11 +245,7 @@ def measure_policy(args, comm, policy, shape, cfg, routing, topo, model, cfgs, w
     ms = s.elapsed_time(e) / args.steps
     launches = (dp.launches - launches0) // args.steps
     dp.timing = False
-    ms_max = ms
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms_max = float(t.item())
+    ms_max = comm.max_over_ranks(ms)
     res = {"ms": ms_max, "plan_ms": plan_ms, "skew": plan.skew(), "launches": launches,
            "predicted_ms": plan.predicted_ms(topo, model, topo.profile),
            "rows": [dp.real_rows(m) for m in range(MB)], "rows_cap": plan.rows_cap}
@@ -283,10 +280,7 @@ def measure_policy(args, comm, policy, shape, cfg, routing, topo, model, cfgs, w
             dp.step_host(host, dev)
         comm.host_barrier()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / n_e2e
-        if world > 1:
-            t = torch.tensor([e2e_ms], device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+        e2e_ms = comm.max_over_ranks(e2e_ms)
         res["e2e_ms"] = e2e_ms
         res["h2d"] = sum(host[k].numel() * host[k].element_size() for k in ("x", "idx", "gates", "dout"))
         res["d2h"] = sum(host[k].numel() * host[k].element_size() for k in ("out", "dx", "dgate"))

@@ -79,6 +79,11 @@ int mb_permute_rank(const int32_t* idx, int64_t T, int32_t k, const float* gate,
 int mb_scatter_rows(const void* x, int64_t T, int32_t k, int32_t h, const int32_t* perm, void* const* dst_rows,
                     void* stream);
 
+/* Row-mover engine for mb_scatter_rows / mb_combine_rows: blocks > 0 selects the TMA bulk-copy
+ * kernels (cp.async.bulk rows through shared memory; one block per SM, ~190 KB of rows in flight,
+ * never co-resident with a GEMM CTA) on that many blocks; 0 = the register-copy kernels. */
+int mb_set_comm_blocks(int32_t blocks);
+
 /* ---------------------------------------------------------------- K6 combine
  * out[t] = sum_i w[t,i] * src_rows[perm.gpu][perm.row] in fp32 (w = gate, or 1 when gate == NULL),
  * rows read from peers; optionally scalar_out[t,i] = sum of the npart per-row partials at

@@ -57,9 +57,22 @@ class Comm:
     def all_gather_tensor(self, t: torch.Tensor) -> torch.Tensor:
         if self.world == 1:
             return t.unsqueeze(0)
+        if self.dist.get_backend() == "gloo":  # oversubscribed test mode: host-side gather
+            parts = [torch.empty_like(t, device="cpu") for _ in range(self.world)]
+            self.dist.all_gather(parts, t.contiguous().cpu())
+            return torch.stack(parts).to(t.device)
         out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
         self.dist.all_gather_into_tensor(out, t.contiguous())
         return out
+
+    def max_over_ranks(self, value: float) -> float:
+        """Max of a per-rank scalar (device-timed milliseconds) over all ranks."""
+        if self.world == 1:
+            return float(value)
+        dev = "cpu" if self.dist.get_backend() == "gloo" else "cuda"
+        t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
 
     def host_barrier(self) -> None:
         if self.world > 1:
@@ -136,13 +149,27 @@ class SymmetricArena:
             self.base = 0
 
 
+def local_device() -> int:
+    """CUDA device of this rank: LOCAL_RANK, folded onto the visible GPUs when more ranks than
+    GPUs run (MB_OVERSUBSCRIBE=1: a correctness test of an EP=8 job on a 2- or 4-GPU box; the
+    ranks sharing a GPU time-slice, so timings from that mode mean nothing)."""
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("MB_OVERSUBSCRIBE") == "1":
+        return local % max(1, torch.cuda.device_count())
+    return local
+
+
 def init_distributed() -> Comm:
-    """torchrun-style env (RANK/WORLD_SIZE/LOCAL_RANK/MASTER_*): NCCL process group, one GPU per rank."""
+    """torchrun-style env (RANK/WORLD_SIZE/LOCAL_RANK/MASTER_*): NCCL process group, one GPU per
+    rank (gloo under MB_OVERSUBSCRIBE=1: NCCL refuses two ranks on one GPU)."""
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1 and not dist.is_initialized():
-        local = int(os.environ.get("LOCAL_RANK", "0"))
-        torch.cuda.set_device(local)
+        dev = local_device()
+        torch.cuda.set_device(dev)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("MB_OVERSUBSCRIBE") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     return Comm()

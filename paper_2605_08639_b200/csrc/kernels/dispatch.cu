@@ -14,6 +14,7 @@
 //   row_base is fixed by the receive layout of the destination GPU: slots (home experts
 //   ascending, then replicated experts ascending) x source GPU ascending x rank, each slot padded
 //   to a multiple of 128 rows (the GEMM M tile).
+#include <algorithm>
 #include <cstdlib>
 
 #include "capi_common.cuh"
@@ -197,6 +198,192 @@ __global__ void __launch_bounds__(256) combine_rows_kernel(const void* const* __
   }
 }
 
+// ------------------------------------------------------------------ TMA row movers
+// The same two operations with the copy engine of each SM (cp.async.bulk) instead of register
+// copies.  A block owns most of an SM's shared memory, so it never co-resides with a GEMM CTA
+// (the row movers stay on the SMs the persistent GEMM leaves free), and each SM keeps ~190 KB of
+// rows in flight -- what a remote (NVLink) copy needs to cover its latency.
+constexpr int kTmaBarBytes = 1024;  // mbarriers at the start of dynamic shared memory
+
+// K3: warp w streams tokens t = gw, gw + nwarps, ...: token j is bulk-loaded into buffer j % nbuf
+// (one 128-bit-aligned row), then lanes 0..k-1 each bulk-store it to one (gpu, row) of the token's
+// choices.  Loads run nbuf - 1 tokens ahead; a buffer is refilled once the stores that read it
+// (the warp's previous bulk group) have drained it.
+__global__ void __launch_bounds__(256, 1) scatter_rows_tma_kernel(const uint8_t* __restrict__ x, int64_t T, int k,
+                                                                  int row_bytes, const int2* __restrict__ perm,
+                                                                  void* const* __restrict__ dst_rows, int nbuf) {
+  extern __shared__ __align__(1024) uint8_t smem_t[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_t) + warp * nbuf;
+  uint8_t* buf = smem_t + kTmaBarBytes + static_cast<int64_t>(warp) * nbuf * row_bytes;
+  if (lane == 0) {
+    for (int b = 0; b < nbuf; ++b) mbar_init(&bar[b], 1);
+    fence_proxy_async_smem();
+  }
+  __syncwarp();
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * nw + warp;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * nw;
+  if (gw >= T) return;
+  const int64_t n = (T - gw + nwarps - 1) / nwarps;
+  auto load = [&](int64_t j) {
+    const int b = static_cast<int>(j % nbuf);
+    mbar_arrive_expect_tx(&bar[b], row_bytes);
+    bulk_load_1d(buf + static_cast<int64_t>(b) * row_bytes, x + (gw + j * nwarps) * row_bytes, row_bytes, &bar[b]);
+  };
+  if (lane == 0)
+    for (int64_t j = 0; j < nbuf - 1 && j < n; ++j) load(j);
+  int2 pr = make_int2(-1, -1);
+  if (lane < k) pr = perm[gw * k + lane];
+  for (int64_t j = 0; j < n; ++j) {
+    const int b = static_cast<int>(j % nbuf);
+    const int64_t t = gw + j * nwarps;
+    // next token's choices while this one's row lands
+    int2 pr_next = make_int2(-1, -1);
+    if (lane < k && j + 1 < n) pr_next = perm[(t + nwarps) * k + lane];
+    mbar_wait(&bar[b], static_cast<uint32_t>((j / nbuf) & 1));
+    for (int i = lane; i < k; i += 32) {
+      const int2 p = i < 32 ? pr : perm[t * k + i];
+      if (p.x >= 0)
+        bulk_store_1d(reinterpret_cast<uint8_t*>(dst_rows[p.x]) + static_cast<int64_t>(p.y) * row_bytes,
+                      buf + static_cast<int64_t>(b) * row_bytes, row_bytes);
+    }
+    bulk_commit();
+    pr = pr_next;
+    const int64_t jn = j + nbuf - 1;
+    if (jn < n) {
+      bulk_wait_read<1>();  // token j-1's stores have read the buffer token jn lands in
+      __syncwarp();
+      if (lane == 0) load(jn);
+    }
+  }
+  bulk_wait<0>();
+}
+
+// K6: block-cooperative.  A producer warp keeps a ring of nslot token slots in flight: for each
+// token its lanes 0..k-1 bulk-load the k full rows (local or peer, one cp.async.bulk of 2h bytes
+// each -- the TMA unit's cost is per operation, so whole rows move ~4x the bytes per op of 1 KB
+// pieces) plus, for the dX un-permute, the rows' dgate partials; the (gpu, row, weight) triples
+// go into the slot beside them.  kConsumers warps reduce a landed slot together (warp w owns
+// columns w*32 + lane + 256*r) in fp32 with the fixed i order and arithmetic of
+// combine_rows_kernel (bit-identical results) and release the slot on its empty barrier.
+constexpr int kConsumers = 8;
+template <int KMAX>
+__global__ void __launch_bounds__(32 * (kConsumers + 1), 1)
+    combine_rows_tma_kernel(const void* const* __restrict__ src_rows, const int2* __restrict__ perm,
+                            const float* __restrict__ gate, int64_t T, int k, int h, uint4* __restrict__ out,
+                            const float* const* __restrict__ src_scalar, float* __restrict__ scalar_out, int npart,
+                            int nslot) {
+  extern __shared__ __align__(1024) uint8_t smem_t[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row_bytes = h * 2, vrow = h >> 3;
+  const bool scal = scalar_out != nullptr;
+  const int side_bytes = KMAX * 16 + (scal ? KMAX * npart * 4 : 0);  // npart % 4 == 0 (host check)
+  const int64_t slot_bytes = static_cast<int64_t>(KMAX) * row_bytes + side_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_t);
+  uint64_t* empty = full + nslot;
+  auto rows_of = [&](int s) { return smem_t + kTmaBarBytes + s * slot_bytes; };
+  auto meta = [&](int s) { return reinterpret_cast<int4*>(rows_of(s) + static_cast<int64_t>(KMAX) * row_bytes); };
+  auto scl = [&](int s) { return reinterpret_cast<float*>(rows_of(s) + static_cast<int64_t>(KMAX) * row_bytes + KMAX * 16); };
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < nslot; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], kConsumers);
+    }
+    fence_proxy_async_smem();
+  }
+  __syncthreads();
+  const int64_t n = (T - blockIdx.x + gridDim.x - 1) / gridDim.x;  // tokens of this block
+  if (static_cast<int64_t>(blockIdx.x) >= T) return;
+  if (warp == kConsumers) {
+    // ------------------------------------------------ producer
+    // permutation entries are loaded a batch of kTB tokens at a time (lane = token-in-batch *
+    // KMAX + choice), one batch ahead, so their global-load latency overlaps the slot waits
+    constexpr int kTB = 32 / KMAX;
+    const int ub = lane / KMAX, ci = lane % KMAX;
+    auto fetch = [&](int64_t b, int2& p, float& w) {
+      p = make_int2(-1, -1);
+      w = 0.0f;
+      const int64_t j = b * kTB + ub;
+      if (ci < k && j < n) {
+        const int64_t t = blockIdx.x + j * gridDim.x;
+        p = perm[t * k + ci];
+        w = gate ? gate[t * k + ci] : 1.0f;
+      }
+    };
+    int2 pc, pn;
+    float wc, wn;
+    fetch(0, pc, wc);
+    for (int64_t b = 0; b * kTB < n; ++b) {
+      fetch(b + 1, pn, wn);
+      for (int u = 0; u < kTB; ++u) {
+        const int64_t j = b * kTB + u;
+        if (j >= n) break;
+        const int s = static_cast<int>(j % nslot);
+        mbar_wait(&empty[s], static_cast<uint32_t>(((j / nslot) & 1) ^ 1));
+        const bool mine = ub == u;
+        if (mine) meta(s)[ci] = make_int4(pc.x, pc.y, __float_as_int(wc), 0);
+        const unsigned valid = __ballot_sync(0xffffffffu, mine && pc.x >= 0);
+        if (lane == 0) mbar_arrive_expect_tx(&full[s], __popc(valid) * (row_bytes + (scal ? npart * 4 : 0)));
+        __syncwarp();
+        if (mine && pc.x >= 0) {
+          bulk_load_1d(rows_of(s) + static_cast<int64_t>(ci) * row_bytes,
+                       reinterpret_cast<const uint8_t*>(src_rows[pc.x]) + static_cast<int64_t>(pc.y) * row_bytes,
+                       row_bytes, &full[s]);
+          if (scal)
+            bulk_load_1d(scl(s) + ci * npart, src_scalar[pc.x] + static_cast<int64_t>(pc.y) * npart, npart * 4,
+                         &full[s]);
+        }
+      }
+      pc = pn;
+      wc = wn;
+    }
+    return;
+  }
+  // -------------------------------------------------- consumers
+  for (int64_t j = 0; j < n; ++j) {
+    const int s = static_cast<int>(j % nslot);
+    const int64_t t = blockIdx.x + j * gridDim.x;
+    mbar_wait(&full[s], static_cast<uint32_t>((j / nslot) & 1));
+    const int4* m = meta(s);
+    if (scal && warp == 0 && lane < k) {
+      float sc = 0.0f;
+      if (m[lane].x >= 0) {
+        const float* src = scl(s) + lane * npart;
+        for (int qq = 0; qq < npart; ++qq) sc += src[qq];
+      }
+      scalar_out[t * k + lane] = sc;
+    }
+    const uint4* rows = reinterpret_cast<const uint4*>(rows_of(s));
+    for (int col = warp * 32 + lane; col < vrow; col += 32 * kConsumers) {
+      float acc[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
+      uint4 u4[KMAX];
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i)
+        if (i < k && m[i].x >= 0) u4[i] = rows[static_cast<int64_t>(i) * vrow + col];
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i) {
+        if (i >= k) break;
+        const int4 mi = m[i];
+        if (mi.x < 0) continue;
+        const float wi = __int_as_float(mi.z);
+        const uint32_t u[4] = {u4[i].x, u4[i].y, u4[i].z, u4[i].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          acc[2 * e] += wi * bf16lo(u[e]);
+          acc[2 * e + 1] += wi * bf16hi(u[e]);
+        }
+      }
+      out[t * vrow + col] = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
+                                       pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
 // ------------------------------------------------------------------ slot-table helpers
 // slot_tab: [nslots][4] int32 {row_begin, rows_real, rows_pad, expert}; slots tile [0, total) in order.
 __device__ __forceinline__ int find_slot(const int4* __restrict__ slots, int nslots, int64_t row) {
@@ -298,6 +485,15 @@ inline int64_t comm_grid() {
   return v;
 }
 
+// TMA row movers (scatter_rows_tma_kernel / combine_rows_tma_kernel): number of blocks, one per
+// SM; 0 = the register-copy kernels (mb_set_comm_blocks, env MB_COMM_BLOCKS overrides).
+static int g_comm_blocks = 0;
+inline int comm_blocks() {
+  if (const char* e = std::getenv("MB_COMM_BLOCKS")) return std::atoi(e);
+  return g_comm_blocks;
+}
+constexpr int kTmaSmemBudget = 192 * 1024;
+
 inline int grid_for(int64_t work_items, int per_block) {
   int64_t g = (work_items + per_block - 1) / per_block;
   const int64_t cap = comm_grid() > 0 ? comm_grid() : static_cast<int64_t>(device_sm_count()) * 8;
@@ -339,10 +535,31 @@ extern "C" int mb_permute_rank(const int32_t* idx, int64_t T, int32_t k, const f
 }
 
 
+extern "C" int mb_set_comm_blocks(int32_t blocks) {
+  MB_CHECK_ARG(blocks >= 0, "blocks must be >= 0 (0 = register-copy row movers)");
+  g_comm_blocks = blocks;
+  return MB_OK;
+}
+
 extern "C" int mb_scatter_rows(const void* x, int64_t T, int32_t k, int32_t h, const int32_t* perm,
                                void* const* dst_rows, void* stream) {
   MB_CHECK_ARG(x && perm && dst_rows && T >= 0 && k >= 1 && h >= 8 && h % 8 == 0, "bad scatter args");
   if (T == 0) return MB_OK;
+  if (const int nb = comm_blocks(); nb > 0) {
+    const int row_bytes = 2 * h;
+    int warps = 8, nbuf = 0;
+    while (warps > 1 && (nbuf = (kTmaSmemBudget - kTmaBarBytes) / (warps * row_bytes)) < 3) warps >>= 1;
+    nbuf = (kTmaSmemBudget - kTmaBarBytes) / (warps * row_bytes);
+    if (nbuf > 128 / warps) nbuf = 128 / warps;
+    if (nbuf >= 2) {
+      const int smem = kTmaBarBytes + warps * nbuf * row_bytes;
+      MB_CUDA_TRY(cudaFuncSetAttribute(scatter_rows_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      scatter_rows_tma_kernel<<<nb, 32 * warps, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+          reinterpret_cast<const uint8_t*>(x), T, k, row_bytes, reinterpret_cast<const int2*>(perm), dst_rows, nbuf);
+      MB_CUDA_TRY(cudaGetLastError());
+      return MB_OK;
+    }
+  }
   const int grid = grid_for(T, 8);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int vrow = h / 8;
@@ -363,11 +580,31 @@ extern "C" int mb_combine_rows(const void* const* src_rows, const int32_t* perm,
   MB_CHECK_ARG((scalar_out == nullptr) == (src_scalar == nullptr), "src_scalar and scalar_out go together");
   MB_CHECK_ARG(npart >= 1, "npart must be >= 1");
   if (T == 0) return MB_OK;
-  const int grid = grid_for(T, 8);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int vrow = h / 8;
   const int2* pr = reinterpret_cast<const int2*>(perm);
   uint4* o = reinterpret_cast<uint4*>(out);
+  if (const int nb = comm_blocks(); nb > 0 && k <= 16 && (!scalar_out || (npart % 4 == 0 && npart <= 64))) {
+    const int kmax = k <= 2 ? 2 : k <= 4 ? 4 : k <= 8 ? 8 : 16;
+    const int64_t slot_bytes = static_cast<int64_t>(kmax) * 2 * h + kmax * 16 + (scalar_out ? kmax * npart * 4 : 0);
+    int nslot = static_cast<int>((kTmaSmemBudget - kTmaBarBytes) / slot_bytes);
+    if (nslot > 64) nslot = 64;
+    if (nslot >= 2) {
+      const int smem = kTmaBarBytes + static_cast<int>(nslot * slot_bytes);
+      auto launch = [&](auto kern) -> int {
+        MB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        kern<<<nb, 32 * (kConsumers + 1), smem, s>>>(src_rows, pr, gate, T, k, h, o, src_scalar, scalar_out, npart,
+                                                     nslot);
+        MB_CUDA_TRY(cudaGetLastError());
+        return MB_OK;
+      };
+      if (kmax == 2) return launch(combine_rows_tma_kernel<2>);
+      if (kmax == 4) return launch(combine_rows_tma_kernel<4>);
+      if (kmax == 8) return launch(combine_rows_tma_kernel<8>);
+      return launch(combine_rows_tma_kernel<16>);
+    }
+  }
+  const int grid = grid_for(T, 8);
   if (vrow <= 64)
     combine_rows_kernel<2><<<grid, 256, comm_smem(), s>>>(src_rows, pr, gate, T, k, h, o, src_scalar, scalar_out, npart);
   else if (vrow <= 128)

@@ -180,3 +180,24 @@ def test_dropped_token_choices():
     assert moe_ref.rel_err(dgate[0], ref["dgate"]) < TOL
     assert torch.all(out[0, -32:] == 0) and torch.all(dx[0, -32:] == 0)
     dp.close()
+
+
+@pytest.mark.parametrize("name,T,MB", [("qwen3-30b-a3b", 512, 3), ("mixtral-8x7b", 256, 1), ("tiny", 256, 2)])
+def test_tma_row_movers_bit_identical(name, T, MB):
+    """The TMA bulk-copy row movers (mb_set_comm_blocks > 0: scatter, combine, dX un-permute with
+    the dgate gather) give bit-identical step results to the register-copy kernels."""
+    from paper_2605_08639_b200 import _native as nat
+    lib = nat.kernels()
+    shape, routing, plan, dp, _, (x, dout, idx, gates), (out, dx, dgate) = _run(name, T, MB)
+    g1, g2 = dp.gW1.clone(), dp.gW2.clone()
+    try:
+        nat.check(lib.mb_set_comm_blocks(12), lib, "mb_set_comm_blocks")
+        dp.zero_grads()
+        o2, dx2, dg2 = torch.empty_like(out), torch.empty_like(dx), torch.empty_like(dgate)
+        dp.step(x, idx, gates, dout, o2, dx2, dg2)
+        torch.cuda.synchronize()
+    finally:
+        nat.check(lib.mb_set_comm_blocks(0), lib, "mb_set_comm_blocks")
+    assert torch.equal(o2, out) and torch.equal(dx2, dx) and torch.equal(dg2, dgate)
+    assert torch.equal(dp.gW1, g1) and torch.equal(dp.gW2, g2)
+    dp.close()

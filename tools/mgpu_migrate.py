@@ -23,7 +23,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from oracle import moe_ref  # noqa: E402
 from paper_2605_08639_b200 import AnnealConfig, ModelProfile, ReplicaConfig, SimConfigs  # noqa: E402
 from paper_2605_08639_b200.cluster import b200_box_topology, b200_profile  # noqa: E402
-from paper_2605_08639_b200.comm import init_distributed  # noqa: E402
+from paper_2605_08639_b200.comm import init_distributed, local_device  # noqa: E402
 from paper_2605_08639_b200.moe_layer import MoEDataPlane, build_step_plan, interleave_w1  # noqa: E402
 from paper_2605_08639_b200.workload import SHAPES, make_activations, make_routing, make_weights  # noqa: E402
 
@@ -37,7 +37,7 @@ def main():
     args = ap.parse_args()
     comm = init_distributed()
     rank, world = comm.rank, comm.world
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    torch.cuda.set_device(local_device())
     cfg = SHAPES[args.config]
     shape = cfg["shape"]
     E, T, MB = shape.num_experts, args.tokens, args.micro_batches
