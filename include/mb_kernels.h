@@ -72,6 +72,14 @@ int mb_permute_rank(const int32_t* idx, int64_t T, int32_t k, const float* gate,
                     int32_t chunk_tokens, const int32_t* route_tab, const int32_t* ncopies, int32_t maxc,
                     float* const* dst_gate, int32_t* perm, void* stream);
 
+/* The same over nb consecutive micro-batches in one launch: idx / gate / perm advance by T*k
+ * entries, chunk_base by chunks*E, route_tab by E*maxc*4, ncopies by E, and dst_gate holds
+ * `world` receive-gate pointers per micro-batch. */
+int mb_permute_rank_nb(const int32_t* idx, int64_t T, int32_t k, const float* gate, int32_t E,
+                       const uint32_t* chunk_base, int32_t chunk_tokens, const int32_t* route_tab,
+                       const int32_t* ncopies, int32_t maxc, float* const* dst_gate, int32_t world, int32_t* perm,
+                       int32_t nb, void* stream);
+
 /* ---------------------------------------------------------------- K3 dispatch all-to-all
  * Row scatter: row t of x ([T,h] bf16) is stored at dst_rows[perm.gpu] + perm.row*h for every
  * choice i (device array of per-GPU base pointers, peers mapped over NVLink; 128-bit stores).
@@ -98,6 +106,10 @@ int mb_combine_bwd_expert(void* dout_rows, const void* y_rows, const float* gate
                           const int32_t* slot_tab, int32_t nslots, int64_t total_rows, int32_t h, void* stream);
 /* Zero the padding rows of every receive slot (slot_tab [nslots][4] {row_begin, rows_real, rows_pad, expert}). */
 int mb_zero_pad_rows(void* rows, const int32_t* slot_tab, int32_t nslots, int32_t h, void* stream);
+/* Batched: micro-batch b uses rows + b*rows_stride rows and slot_tab + b*max_slots entries
+ * (entries past a micro-batch's slot count are all-zero). */
+int mb_zero_pad_rows_nb(void* rows, int64_t rows_stride, const int32_t* slot_tab, int32_t max_slots, int32_t nb,
+                        int32_t h, void* stream);
 
 /* ---------------------------------------------------------------- K5 replicas
  * dst[i] += sum_s srcs[s][i] (fp32, sources in list order): replica-gradient reduce into the owner,

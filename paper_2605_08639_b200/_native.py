@@ -48,6 +48,9 @@ _KERNEL_SIGS = {
 _KERNEL_SIGS.update({
     "mb_chunk_scan": (c_int, [c_vp, c_vp, c_i64, c_i32, c_i32, c_vp]),
     "mb_permute_rank": (c_int, [c_vp, c_i64, c_i32, c_vp, c_i32, c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp]),
+    "mb_permute_rank_nb": (c_int, [c_vp, c_i64, c_i32, c_vp, c_i32, c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_i32,
+                                   c_vp, c_i32, c_vp]),
+    "mb_zero_pad_rows_nb": (c_int, [c_vp, c_i64, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "mb_scatter_rows": (c_int, [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp]),
     "mb_set_comm_blocks": (c_int, [c_i32]),
     "mb_combine_rows": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp]),

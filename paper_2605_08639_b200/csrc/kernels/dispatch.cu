@@ -55,13 +55,27 @@ __global__ void __launch_bounds__(256) chunk_scan_kernel(const uint32_t* __restr
 // ------------------------------------------------------------------ K2 stable-rank permutation
 // One warp per chunk of `chunk_tokens` tokens; ranks are stable in row-major (t, i) order.
 // route_tab: [E][maxc][4] int32 {cum_end, dst_gpu, dst_row_base, 0}; ncopies[E].
+// Batched over micro-batches on blockIdx.y (per-micro-batch tables at fixed strides; dst_gate
+// holds `world` pointers per micro-batch).
 __global__ void __launch_bounds__(128) permute_rank_kernel(
     const int32_t* __restrict__ idx, int64_t T, int k, const float* __restrict__ gate, int E,
     const uint32_t* __restrict__ chunk_base, int chunk_tokens, const int4* __restrict__ route_tab,
-    const int32_t* __restrict__ ncopies, int maxc, float* const* __restrict__ dst_gate, int2* __restrict__ perm) {
+    const int32_t* __restrict__ ncopies, int maxc, float* const* __restrict__ dst_gate, int2* __restrict__ perm,
+    int world) {
   extern __shared__ uint32_t running_all[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int chunk = blockIdx.x * (blockDim.x >> 5) + warp;
+  {
+    const int64_t b = blockIdx.y;
+    const int64_t chunks = (T + chunk_tokens - 1) / chunk_tokens;
+    idx += b * T * k;
+    if (gate) gate += b * T * k;
+    chunk_base += b * chunks * E;
+    route_tab += b * E * maxc;
+    ncopies += b * E;
+    if (dst_gate) dst_gate += b * world;
+    perm += b * T * k;
+  }
   uint32_t* running = running_all + warp * E;
   for (int e = lane; e < E; e += 32) running[e] = 0;
   __syncwarp();
@@ -447,8 +461,11 @@ __global__ void __launch_bounds__(256) combine_bwd_expert_kernel(uint4* __restri
 }
 
 // Zero the pad rows [row_begin + rows_real, row_begin + rows_pad) of every slot.
-__global__ void __launch_bounds__(256) zero_pad_rows_kernel(uint4* __restrict__ rows, const int4* __restrict__ slots, int h) {
-  const int4 sl = slots[blockIdx.x];
+// blockIdx.y = micro-batch (rows / slot tables at fixed strides; unused slot entries are all-zero)
+__global__ void __launch_bounds__(256) zero_pad_rows_kernel(uint4* __restrict__ rows, const int4* __restrict__ slots, int h,
+                                                            int64_t rows_stride, int slots_stride) {
+  rows += blockIdx.y * rows_stride * (h >> 3);
+  const int4 sl = slots[static_cast<int64_t>(blockIdx.y) * slots_stride + blockIdx.x];
   const int vrow = h >> 3;
   const int64_t r0 = static_cast<int64_t>(sl.x) + sl.y, r1 = static_cast<int64_t>(sl.x) + sl.z;
   const int64_t n = (r1 - r0) * vrow;
@@ -529,7 +546,25 @@ extern "C" int mb_permute_rank(const int32_t* idx, int64_t T, int32_t k, const f
   permute_rank_kernel<<<static_cast<unsigned>(grid), 32 * wpb, wpb * E * sizeof(uint32_t),
                         reinterpret_cast<cudaStream_t>(stream)>>>(
       idx, T, k, gate, E, chunk_base, chunk_tokens, reinterpret_cast<const int4*>(route_tab), ncopies, maxc, dst_gate,
-      reinterpret_cast<int2*>(perm));
+      reinterpret_cast<int2*>(perm), 0);
+  MB_CUDA_TRY(cudaGetLastError());
+  return MB_OK;
+}
+
+extern "C" int mb_permute_rank_nb(const int32_t* idx, int64_t T, int32_t k, const float* gate, int32_t E,
+                                  const uint32_t* chunk_base, int32_t chunk_tokens, const int32_t* route_tab,
+                                  const int32_t* ncopies, int32_t maxc, float* const* dst_gate, int32_t world,
+                                  int32_t* perm, int32_t nb, void* stream) {
+  MB_CHECK_ARG(T >= 0 && k >= 1 && E >= 1 && E <= 2048 && chunk_tokens >= 1 && maxc >= 1 && nb >= 0 && world >= 1,
+               "bad permute args");
+  MB_CHECK_ARG(idx && chunk_base && route_tab && ncopies && perm, "null permute operand");
+  if (T == 0 || nb == 0) return MB_OK;
+  const int64_t chunks = (T + chunk_tokens - 1) / chunk_tokens;
+  const int wpb = 4;
+  dim3 grid(static_cast<unsigned>((chunks + wpb - 1) / wpb), static_cast<unsigned>(nb));
+  permute_rank_kernel<<<grid, 32 * wpb, wpb * E * sizeof(uint32_t), reinterpret_cast<cudaStream_t>(stream)>>>(
+      idx, T, k, gate, E, chunk_base, chunk_tokens, reinterpret_cast<const int4*>(route_tab), ncopies, maxc, dst_gate,
+      reinterpret_cast<int2*>(perm), world);
   MB_CUDA_TRY(cudaGetLastError());
   return MB_OK;
 }
@@ -638,7 +673,18 @@ extern "C" int mb_zero_pad_rows(void* rows, const int32_t* slot_tab, int32_t nsl
   MB_CHECK_ARG(rows && slot_tab && nslots >= 0 && h % 8 == 0, "bad zero_pad args");
   if (nslots == 0) return MB_OK;
   zero_pad_rows_kernel<<<nslots, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<uint4*>(rows), reinterpret_cast<const int4*>(slot_tab), h);
+      reinterpret_cast<uint4*>(rows), reinterpret_cast<const int4*>(slot_tab), h, 0, 0);
+  MB_CUDA_TRY(cudaGetLastError());
+  return MB_OK;
+}
+
+extern "C" int mb_zero_pad_rows_nb(void* rows, int64_t rows_stride, const int32_t* slot_tab, int32_t max_slots,
+                                   int32_t nb, int32_t h, void* stream) {
+  MB_CHECK_ARG(rows && slot_tab && max_slots >= 0 && nb >= 0 && rows_stride >= 0 && h % 8 == 0, "bad zero_pad args");
+  if (max_slots == 0 || nb == 0) return MB_OK;
+  dim3 grid(static_cast<unsigned>(max_slots), static_cast<unsigned>(nb));
+  zero_pad_rows_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<uint4*>(rows), reinterpret_cast<const int4*>(slot_tab), h, rows_stride, max_slots);
   MB_CUDA_TRY(cudaGetLastError());
   return MB_OK;
 }

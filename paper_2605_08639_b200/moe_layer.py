@@ -47,7 +47,13 @@ _SKIP_ROWS = os.environ.get("MB_PROFILE_SKIP_ROWS", "0") == "1"
 # SMs left to the comm stream while the persistent GEMM runs (measured on B200, qwen3 shape:
 # N=4 step 24.1 ms with all 148 SMs in the GEMM, 19.7 ms with 28 left free)
 COMM_SMS = {1: 20}
-COMM_SMS_MULTI = 28
+COMM_SMS_MULTI = 32
+# Row-mover engine per world size: "regs" = register-copy kernels (co-resident with the GEMM's
+# CTAs on every SM), "tma" = cp.async.bulk kernels, one block on each of the COMM_SMS SMs the
+# GEMM leaves free.  Measured (profiles/r01_comm_engine.txt): at N=4 tma/32 SMs 18.85-19.04 ms
+# vs regs 19.2-19.26 per step; at N=1 (HBM-local moves) regs is faster (18.8-19.3 vs >= 20.1).
+ROW_MOVERS = {1: "regs"}
+ROW_MOVERS_MULTI = "tma"
 # overlap=False runs every phase in issue order on one stream with all SMs in the GEMM: at world 1
 # (local row movers) it measured the same step time as the overlapped schedule (19.6 vs 19.4 ms).
 CHUNK = 32      # tokens per permutation chunk
@@ -278,11 +284,13 @@ class MoEDataPlane:
 
     def __init__(self, comm: Comm, shape: LayerShape, tokens: int, micro_batches: int, plan: StepPlan,
                  device: torch.device | None = None, comm_sms: int | None = None,
-                 expert_state: dict | None = None, rows_cap: int = 0, overlap: bool | None = None):
+                 expert_state: dict | None = None, rows_cap: int = 0, overlap: bool | None = None,
+                 row_movers: str | None = None):
         """expert_state: optional per-expert tensors that follow their expert when the reorder
         plan migrates it (e.g. optimizer moments): {name: (per-expert shape, torch dtype)}.
         rows_cap: receive rows per micro-batch to allocate (>= every plan this layer will load).
-        overlap: run dispatch / combine on their own stream beside the GEMMs (default)."""
+        overlap: run dispatch / combine on their own stream beside the GEMMs (default).
+        row_movers: "regs" | "tma" scatter / combine engine (default per world size, ROW_MOVERS)."""
         shape.check()
         self.comm, self.shape, self.T, self.MB = comm, shape, tokens, micro_batches
         self.rank, self.world = comm.rank, comm.world
@@ -295,6 +303,13 @@ class MoEDataPlane:
         sms = torch.cuda.get_device_properties(self.device).multi_processor_count
         lib = nat.kernels()
         nat.check(lib.mb_set_gemm_sms(max(2, sms - comm_sms)), lib, "mb_set_gemm_sms")
+        if row_movers is None:
+            row_movers = os.environ.get("MB_ROW_MOVERS") or ROW_MOVERS.get(self.world, ROW_MOVERS_MULTI)
+        if row_movers not in ("regs", "tma"):
+            raise ValueError(f"row_movers must be 'regs' or 'tma', got {row_movers!r}")
+        self.row_movers = row_movers
+        nat.check(lib.mb_set_comm_blocks(comm_sms if (row_movers == "tma" and comm_sms > 0) else 0), lib,
+                  "mb_set_comm_blocks")
         E, h, hp = shape.num_experts, shape.hidden, shape.ffn
         if E % self.world:
             raise ValueError(f"{E} experts not divisible by {self.world} GPUs")
@@ -410,9 +425,10 @@ class MoEDataPlane:
         for m, mbp in enumerate(plan.mbs):
             route.append(mbp.route_tab[d])
             ncop.append(mbp.ncopies)
-            st = mbp.slot_tab[d]
-            sw = mbp.slot_w[d]
             n = int(mbp.nslots[d])
+            st = mbp.slot_tab[d].copy()
+            st[n:] = 0  # unused entries all-zero (the batched pad-row zeroing relies on it)
+            sw = mbp.slot_w[d]
             if int(sw[:n, 0][sw[:n, 1] > 0].max(initial=-1)) >= self.slots:
                 raise ValueError("plan uses more replica slots than allocated")
             g = np.zeros((max_slots, K.GROUP_FIELDS), dtype=np.int32)
@@ -598,7 +614,7 @@ class MoEDataPlane:
         Runs the two-micro-batch-overlap schedule (schedule()); the same phases are available one
         micro-batch at a time through begin_step / forward_mb / backward_mb / end_step."""
         ops = _StepOps(self, hooks)
-        comm_fn = {"D": lambda m: ops.dispatch(m, x[m], idx[m], gates[m]),
+        comm_fn = {"D": lambda m: ops.dispatch(m, x[m], idx[m], gates[m], idx, gates),
                    "C": lambda m: (ops.combine(m, gates[m], out[m]), ops.dout_dispatch(m, dout[m])),
                    "X": lambda m: ops.unpermute(m, dx[m], dgate[m])}
         comp_fn = {"F": ops.fwd_gemms, "B": ops.bwd_gemms}
@@ -720,7 +736,7 @@ class MoEDataPlane:
         h2d.wait_stream(cur)
         # copy order follows the schedule's needs: the forward inputs of micro-batch m + 1 go
         # before the dout of micro-batch m (D(m+1) is issued before C(m))
-        order = []
+        order = [("r", None)]   # every micro-batch's routing (small) first: D(0) prepares them all
         for m in range(self.MB):
             order.append(("f", m))
             if m >= 1:
@@ -728,13 +744,22 @@ class MoEDataPlane:
         order.append(("b", self.MB - 1))
         with torch.cuda.stream(h2d):
             for kind, m in order:
-                for key in (("x", "idx", "gates") if kind == "f" else ("dout",)):
+                if kind == "r":
+                    for key in ("idx", "gates"):
+                        dev[key].copy_(host[key], non_blocking=True)
+                    rready = torch.cuda.Event()
+                    rready.record(h2d)
+                    continue
+                for key in (("x",) if kind == "f" else ("dout",)):
                     dev[key][m].copy_(host[key][m], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(h2d)
                 (ready if kind == "f" else dready)[m] = ev
 
         class _Hooks:
+            def routing_ready(self, stream):
+                stream.wait_event(rready)
+
             def inputs_ready(self, m, stream):
                 stream.wait_event(ready[m])
 
@@ -793,31 +818,74 @@ class _StepOps:
                         self.push_ev[m] = torch.cuda.Event()
                         self.push_ev[m].record(cps)
         self.first = True
+        self.prepared = set()
 
     # -------------------------------------------------------------- comm stream
-    def dispatch(self, m, x, idx, gates):
-        """D(m): K1 histogram, K2 ranks, K3 scatter into every rank's receive rows."""
+    def prepare(self, m0, m1, idx, gates):
+        """Routing side of micro-batches [m0, m1) in one launch per kernel: K1 histogram, chunk
+        scan, pad-row zeroing, K2 stable ranks (+ gates into the serving ranks' receive slots).
+        idx / gates are the [MB, T, k] step tensors (routing is replayed, so every micro-batch's
+        permutation can be built before its rows move)."""
         dp, xs, st = self.dp, self.xs, self.st_x
         sh = dp.shape
         T, k, h, E = dp.T, sh.top_k, sh.hidden, sh.num_experts
+        nb = m1 - m0
+        if nb <= 0:
+            return
+        if self.hooks and hasattr(self.hooks, "routing_ready"):
+            self.hooks.routing_ready(xs)
+        dp._k("mb_expert_histogram", idx[m0].data_ptr(), nb, T, k, E, dp.counts[m0].data_ptr(),
+              dp.chunk_counts[m0].data_ptr(), CHUNK, st)
+        dp._k("mb_chunk_scan", dp.chunk_counts[m0].data_ptr(), dp.chunk_base[m0].data_ptr(), nb,
+              (T + CHUNK - 1) // CHUNK, E, st)
+        dp._k("mb_zero_pad_rows_nb", dp.Xr[m0].data_ptr(), dp.R, dp.slot_tab[m0].data_ptr(), dp.plan.max_slots, nb,
+              h, st)
+        if self.first:
+            dp.arena.barrier(xs)  # all ranks: previous step drained (receive gates may be rewritten)
+            self.first = False
+        dp._k("mb_permute_rank_nb", idx[m0].data_ptr(), T, k, gates[m0].data_ptr(), E, dp.chunk_base[m0].data_ptr(),
+              CHUNK, dp.route_tab[m0].data_ptr(), dp.ncopies[m0].data_ptr(), dp.plan.maxc,
+              dp.ptr_gate[m0].data_ptr(), dp.world, dp.perm[m0].data_ptr(), nb, st)
+        self.prepared.update(range(m0, m1))
+
+    def dispatch(self, m, x, idx, gates, idx_all=None, gates_all=None):
+        """D(m): routing side of m (unless prepared), K3 scatter into every rank's receive rows.
+        With the step's [MB, ...] routing tensors (idx_all / gates_all), D(0) also prepares
+        micro-batches 1..MB-1 in one batch right after its scatter."""
+        dp, xs, st = self.dp, self.xs, self.st_x
+        sh = dp.shape
+        T, k, h = dp.T, sh.top_k, sh.hidden
         with dp._timed(dp.remote_rows(m)[0] * 2 * h, "comm_dispatch", xs):
+            if m not in self.prepared:
+                self._prepare_one(m, idx, gates)
             if self.hooks:
                 self.hooks.inputs_ready(m, xs)
-            dp._k("mb_expert_histogram", idx.data_ptr(), 1, T, k, E, dp.counts[m].data_ptr(),
-                  dp.chunk_counts[m].data_ptr(), CHUNK, st)
-            dp._k("mb_chunk_scan", dp.chunk_counts[m].data_ptr(), dp.chunk_base[m].data_ptr(), 1,
-                  (T + CHUNK - 1) // CHUNK, E, st)
-            dp._k("mb_zero_pad_rows", dp.Xr[m].data_ptr(), dp.slot_tab[m].data_ptr(), dp.nslots[m], h, st)
-            if self.first:
-                dp.arena.barrier(xs)  # all ranks: previous step drained
-                self.first = False
-            dp._k("mb_permute_rank", idx.data_ptr(), T, k, gates.data_ptr(), E, dp.chunk_base[m].data_ptr(), CHUNK,
-                  dp.route_tab[m].data_ptr(), dp.ncopies[m].data_ptr(), dp.plan.maxc, dp.ptr_gate[m].data_ptr(),
-                  dp.perm[m].data_ptr(), st)
             dp._k("mb_scatter_rows", x.data_ptr(), T, k, h, dp.perm[m].data_ptr(), dp.ptr_xr[m].data_ptr(), st)
+            if idx_all is not None and m == 0:
+                self.prepare(1, dp.MB, idx_all, gates_all)
             if m in self.push_ev:
                 xs.wait_event(self.push_ev[m])  # this rank's replica pushes for micro-batch m
             dp.arena.barrier(xs)  # rows and replica weights of micro-batch m have landed everywhere
+
+    def _prepare_one(self, m, idx, gates):
+        """Routing side of micro-batch m from its own [T, k] tensors (per-micro-batch API)."""
+        dp, xs, st = self.dp, self.xs, self.st_x
+        sh = dp.shape
+        T, k, h, E = dp.T, sh.top_k, sh.hidden, sh.num_experts
+        if self.hooks and hasattr(self.hooks, "routing_ready"):
+            self.hooks.routing_ready(xs)
+        dp._k("mb_expert_histogram", idx.data_ptr(), 1, T, k, E, dp.counts[m].data_ptr(),
+              dp.chunk_counts[m].data_ptr(), CHUNK, st)
+        dp._k("mb_chunk_scan", dp.chunk_counts[m].data_ptr(), dp.chunk_base[m].data_ptr(), 1,
+              (T + CHUNK - 1) // CHUNK, E, st)
+        dp._k("mb_zero_pad_rows", dp.Xr[m].data_ptr(), dp.slot_tab[m].data_ptr(), dp.nslots[m], h, st)
+        if self.first:
+            dp.arena.barrier(xs)  # all ranks: previous step drained
+            self.first = False
+        dp._k("mb_permute_rank", idx.data_ptr(), T, k, gates.data_ptr(), E, dp.chunk_base[m].data_ptr(), CHUNK,
+              dp.route_tab[m].data_ptr(), dp.ncopies[m].data_ptr(), dp.plan.maxc, dp.ptr_gate[m].data_ptr(),
+              dp.perm[m].data_ptr(), st)
+        self.prepared.add(m)
 
     def combine(self, m, gates, out):
         """K6: out[t] = sum_i gate * Y[perm(t, i)] over peer loads."""
