@@ -54,6 +54,10 @@ COMM_SMS_MULTI = 32
 # vs regs 19.2-19.26 per step; at N=1 (HBM-local moves) regs is faster (18.8-19.3 vs >= 20.1).
 ROW_MOVERS = {1: "regs"}
 ROW_MOVERS_MULTI = "tma"
+# the last weight-gradient launch of a step runs on every SM: by then the comm stream only has the
+# replica-gradient reduce (register kernel, co-resident) left -- or, at N=1, the last un-permute
+# (register movers, co-resident too).  MB_WGRAD_ALL_SMS=0 keeps the split (A/B).
+WGRAD_ALL_SMS = os.environ.get("MB_WGRAD_ALL_SMS", "1") == "1"
 # overlap=False runs every phase in issue order on one stream with all SMs in the GEMM: at world 1
 # (local row movers) it measured the same step time as the overlapped schedule (19.6 vs 19.4 ms).
 CHUNK = 32      # tokens per permutation chunk
@@ -302,7 +306,8 @@ class MoEDataPlane:
             comm_sms = COMM_SMS.get(self.world, COMM_SMS_MULTI) if self.overlap else 0
         sms = torch.cuda.get_device_properties(self.device).multi_processor_count
         lib = nat.kernels()
-        nat.check(lib.mb_set_gemm_sms(max(2, sms - comm_sms)), lib, "mb_set_gemm_sms")
+        self.gemm_sms, self.all_sms = max(2, sms - comm_sms), sms
+        nat.check(lib.mb_set_gemm_sms(self.gemm_sms), lib, "mb_set_gemm_sms")
         if row_movers is None:
             row_movers = os.environ.get("MB_ROW_MOVERS") or ROW_MOVERS.get(self.world, ROW_MOVERS_MULTI)
         if row_movers not in ("regs", "tma"):
@@ -961,11 +966,21 @@ class _StepOps:
         dp, cs, xs = self.dp, self.cs, self.xs
         h, hp = dp.shape.hidden, dp.shape.ffn
         fresh = dp._wgrad_prepare()
-        dp._wgrad(dp.wparts[0], fresh)
-        ev = torch.cuda.Event()
-        ev.record(cs)
-        if len(dp.wparts) > 1:
-            dp._wgrad(dp.wparts[1], fresh)
+        split = len(dp.wparts) > 1
+        widen = WGRAD_ALL_SMS and dp.overlap and (split or dp.row_movers == "regs")
+        lib = nat.kernels()
+        try:
+            if widen and not split:
+                nat.check(lib.mb_set_gemm_sms(dp.all_sms), lib, "mb_set_gemm_sms")
+            dp._wgrad(dp.wparts[0], fresh)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            if split:
+                if widen:
+                    nat.check(lib.mb_set_gemm_sms(dp.all_sms), lib, "mb_set_gemm_sms")
+                dp._wgrad(dp.wparts[1], fresh)
+        finally:
+            nat.check(lib.mb_set_gemm_sms(dp.gemm_sms), lib, "mb_set_gemm_sms")
         xs.wait_event(ev)
         if dp.world > 1:  # collective: every rank runs both barriers, with or without replicas
             mn1, mn2 = 2 * hp * h, h * hp

@@ -55,3 +55,33 @@ def test_world2_plans_identical(policy):
     mp.spawn(_worker, args=(world, _free_port(), policy, out), nprocs=world, join=True)
     d0, d1 = out[0][0], out[1][0]
     assert d0 == d1 and len(set(d0)) == 1
+
+
+def _comm_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank), MB_OVERSUBSCRIBE="1")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import torch
+        from paper_2605_08639_b200.comm import Comm, local_device
+        comm = Comm()
+        # max over ranks of the device-timed ms (the bench's max-over-ranks rule), gloo host path
+        m = comm.max_over_ranks(1.5 + rank)
+        g = comm.all_gather_tensor(torch.tensor([rank, 10 * rank], dtype=torch.int64))
+        out[rank] = (m, g.tolist(), local_device())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world4_oversubscribed_host_collectives():
+    """MB_OVERSUBSCRIBE host side: gloo max-over-ranks and tensor all-gather; LOCAL_RANK folds
+    onto the visible GPUs (none here: every rank maps to device 0)."""
+    world = 4
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_comm_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    for r in range(world):
+        m, g, dev = out[r]
+        assert m == 1.5 + world - 1
+        assert g == [[p, 10 * p] for p in range(world)]
+        assert dev == 0
