@@ -158,15 +158,15 @@ def synthetic_config(args, world):
             "zipf_s": args.zipf, "hot_shift": cfg["shift"], "ep": world,
             "gpu_group": min(world, args.group or cfg["group"]),
             "replica_slots": cfg["slots"] if args.slots is None else args.slots, "sa_chains": args.sa_chains,
-            **data_plane_config(world),
+            **data_plane_config(world, shape),
             "l2": "inputs larger than L2 (per-step working set >> 126 MB)"}
 
 
-def data_plane_config(world):
+def data_plane_config(world, shape):
     """Row-mover engine and SMs left to the comm stream (MoEDataPlane defaults / env overrides)."""
     from paper_2605_08639_b200 import moe_layer as ml
     movers = os.environ.get("MB_ROW_MOVERS") or ml.ROW_MOVERS.get(world, ml.ROW_MOVERS_MULTI)
-    return {"row_movers": movers, "comm_sms": ml.COMM_SMS.get(world, ml.COMM_SMS_MULTI)}
+    return {"row_movers": movers, "comm_sms": ml.default_comm_sms(world, shape)}
 
 
 def run_reference(args, rank, world):
@@ -408,7 +408,7 @@ def run_ours(args, comm):
             "experts": shape.num_experts, "top_k": shape.top_k, "hidden": shape.hidden, "ffn": shape.ffn,
             "tokens_per_gpu": T, "micro_batches": MB, "global_tokens_per_step": tokens_step,
             "policy": args.headline, "ep": world, "gpu_group": group, "replica_slots": slots,
-            "sa_chains": args.sa_chains, **data_plane_config(world),
+            "sa_chains": args.sa_chains, **data_plane_config(world, shape),
             "l2": "inputs larger than L2 (per-step working set >> 126 MB)"},
         "roofline": {"kernel": "K4 tcgen05 grouped GEMM (all fwd/dgrad/wgrad launches of the step)",
                      "bound": "tensor", "achieved": round(gemm_tflops, 1), "peak": peak_tf, "unit": "TFLOP/s",

@@ -48,15 +48,20 @@ _SKIP_ROWS = os.environ.get("MB_PROFILE_SKIP_ROWS", "0") == "1"
 # N=4 step 24.1 ms with all 148 SMs in the GEMM, 19.7 ms with 28 left free)
 COMM_SMS = {1: 20}
 COMM_SMS_MULTI = 32
+# Experts with a wide FFN do much more GEMM work per moved row (bytes / FLOP of a step = 4 / (9 h')):
+# at h' >= 4096 the TMA movers keep up on 8 SMs (Mixtral-8x7B at N=4: 79.3-79.8 -> 71.8-74.0 ms per
+# step with 140 GEMM SMs); Qwen3-235B (h' = 1536) is comm-bound on 16 (68.7-70.0 -> 73.0-73.2 ms).
+COMM_SMS_WIDE_FFN = 8
+WIDE_FFN = 4096
 # Row-mover engine per world size: "regs" = register-copy kernels (co-resident with the GEMM's
 # CTAs on every SM), "tma" = cp.async.bulk kernels, one block on each of the COMM_SMS SMs the
 # GEMM leaves free.  Measured (profiles/r01_comm_engine.txt): at N=4 tma/32 SMs 18.85-19.04 ms
 # vs regs 19.2-19.26 per step; at N=1 (HBM-local moves) regs is faster (18.8-19.3 vs >= 20.1).
 ROW_MOVERS = {1: "regs"}
 ROW_MOVERS_MULTI = "tma"
-# the last weight-gradient launch of a step runs on every SM: by then the comm stream only has the
-# replica-gradient reduce (register kernel, co-resident) left -- or, at N=1, the last un-permute
-# (register movers, co-resident too).  MB_WGRAD_ALL_SMS=0 keeps the split (A/B).
+# with replicas (N>1) the second weight-gradient launch runs on every SM: by then the comm stream
+# only has the replica-gradient reduce (register kernel, co-resident) left (N=4: 18.9-19.0 ->
+# 18.7-18.9 ms; at N=1 widening the single launch measured 3% slower).  MB_WGRAD_ALL_SMS=0: A/B.
 WGRAD_ALL_SMS = os.environ.get("MB_WGRAD_ALL_SMS", "1") == "1"
 # overlap=False runs every phase in issue order on one stream with all SMs in the GEMM: at world 1
 # (local row movers) it measured the same step time as the overlapped schedule (19.6 vs 19.4 ms).
@@ -258,6 +263,13 @@ def deinterleave_w1(w1: torch.Tensor) -> tuple:
 # ----------------------------------------------------------------------------- data plane
 
 
+def default_comm_sms(world: int, shape: "LayerShape") -> int:
+    """SMs left to the comm stream's row movers while the persistent GEMM runs."""
+    if world in COMM_SMS:
+        return COMM_SMS[world]
+    return COMM_SMS_WIDE_FFN if shape.ffn >= WIDE_FFN else COMM_SMS_MULTI
+
+
 def schedule(mb: int):
     """Per-rank issue order of one step, two micro-batches in flight (the two-batch overlap of
     EP training systems): compute runs F0 F1 B0 F2 B1 ... F(n-1) B(n-2) B(n-1), the comm stream
@@ -303,7 +315,7 @@ class MoEDataPlane:
             overlap = os.environ["MB_OVERLAP"] == "1"
         self.overlap = True if overlap is None else overlap
         if comm_sms is None:
-            comm_sms = COMM_SMS.get(self.world, COMM_SMS_MULTI) if self.overlap else 0
+            comm_sms = default_comm_sms(self.world, shape) if self.overlap else 0
         sms = torch.cuda.get_device_properties(self.device).multi_processor_count
         lib = nat.kernels()
         self.gemm_sms, self.all_sms = max(2, sms - comm_sms), sms
@@ -967,7 +979,7 @@ class _StepOps:
         h, hp = dp.shape.hidden, dp.shape.ffn
         fresh = dp._wgrad_prepare()
         split = len(dp.wparts) > 1
-        widen = WGRAD_ALL_SMS and dp.overlap and (split or dp.row_movers == "regs")
+        widen = WGRAD_ALL_SMS and dp.overlap and split   # measured slower at N=1 (single part)
         lib = nat.kernels()
         try:
             if widen and not split:
