@@ -6,8 +6,8 @@ run() { P=$((P+1)); local out=$1; shift; timeout 900 "$@" > gpurun_out/fin_$out.
 run n1 python bench.py
 run n1_ref python bench.py --impl reference --steps 2 --warmup 1
 run n2 $TR2 --master-port $((P+50)) bench.py --gpus 2
-run n2_regs env MB_ROW_MOVERS=regs MB_COMM_BLOCKS=0 $TR2 --master-port $((P+60)) bench.py --gpus 2 --policies relibra --steps 8
-run n2_tma $TR2 --master-port $((P+70)) bench.py --gpus 2 --policies relibra --steps 8
+
+
 run n4 $TR --master-port $((P+100)) bench.py --gpus 4
 for z in 0.5 1.5 2.0; do run n4_z$z $TR --master-port $((P+200)) bench.py --gpus 4 --zipf $z --steps 6; P=$((P+1)); done
 run n4_g2 $TR --master-port $((P+300)) bench.py --gpus 4 --group 2 --steps 6
