@@ -42,7 +42,7 @@ def load_peaks():
         return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
 
 
-K4_TRAFFIC = os.path.join(ROOT, "profiles", "r01_launches_step_summary.json")
+K4_TRAFFIC = os.path.join(ROOT, "profiles", "r01_launches_step2_summary.json")
 
 
 def k4_traffic_per_step(config: str, world: int, tokens: int, mbs: int):
@@ -416,7 +416,7 @@ def run_ours(args, comm):
                      "traffic": (None if trace is not None else
                                  k4_traffic_per_step(args.config, world, args.tokens, args.micro_batches)),
                      "traffic_unit": "DRAM bytes per step over all K4 launches (ncu, profiles/"
-                                     "r01_launches_step_summary.json)",
+                                     "r01_launches_step2_summary.json)",
                      "peak_source": f"bf16_tflops_sustained, {peak_src}",
                      "flops_per_step": head["gemm_flop"], "gemm_ms_per_step": round(head["gemm_ms"], 4),
                      "gemm_share_of_step": round(head["gemm_ms"] / head["ms"], 4),
