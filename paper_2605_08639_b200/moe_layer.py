@@ -818,24 +818,41 @@ class _StepOps:
         self.xs.wait_stream(self.cs)
         self.push_ev = {}
         A, cps = dp.arena, dp.cps
+        # K5 replica pushes (copy engine), in micro-batch order; dispatch(m) waits for micro-batch
+        # m's pushes before its final barrier, so the first GEMMs need not wait for the whole
+        # step's replica weights.  Only micro-batch 0's are enqueued here; the rest go right after
+        # D(0) is enqueued, so the host does not delay the first dispatch.
+        self.push_groups = {}
+        for p in dp.pushes:
+            self.push_groups.setdefault(p[1], []).append(p)
+        self._push_order = sorted(self.push_groups)
+        self._push_timer = None
         if dp.pushes:
-            # K5, in micro-batch order; dispatch(m) waits for micro-batch m's pushes before its
-            # final barrier, so the first GEMMs need not wait for the whole step's replica weights
             cps.wait_stream(self.cs)
-            lib = nat.kernels()
-            with dp._timed(len(dp.pushes) * (dp.w1_bytes + dp.w2_bytes), "comm_replica_push", cps):
-                for i, (dst, m, slot, loc) in enumerate(dp.pushes):
-                    d1 = A.peer_ptr(dst, dp.off["w1r"]) + (m * dp.slots + slot) * dp.w1_bytes
-                    d2 = A.peer_ptr(dst, dp.off["w2r"]) + (m * dp.slots + slot) * dp.w2_bytes
-                    nat.check(lib.mb_memcpy_async(d1, dp.W1[loc].data_ptr(), dp.w1_bytes, cps.cuda_stream),
-                              lib, "replica push")
-                    nat.check(lib.mb_memcpy_async(d2, dp.W2[loc].data_ptr(), dp.w2_bytes, cps.cuda_stream),
-                              lib, "replica push")
-                    if i + 1 == len(dp.pushes) or dp.pushes[i + 1][1] != m:
-                        self.push_ev[m] = torch.cuda.Event()
-                        self.push_ev[m].record(cps)
+            self._push_timer = dp._timed(len(dp.pushes) * (dp.w1_bytes + dp.w2_bytes), "comm_replica_push", cps)
+            self._push_timer.__enter__()
+            self._issue_pushes(0)
         self.first = True
         self.prepared = set()
+
+    def _issue_pushes(self, upto=None):
+        """Enqueue the replica pushes of micro-batches <= upto (all when None) not issued yet."""
+        dp, A, cps = self.dp, self.dp.arena, self.dp.cps
+        lib = nat.kernels()
+        while self._push_order and (upto is None or self._push_order[0] <= upto):
+            m = self._push_order.pop(0)
+            for dst, _, slot, loc in self.push_groups[m]:
+                d1 = A.peer_ptr(dst, dp.off["w1r"]) + (m * dp.slots + slot) * dp.w1_bytes
+                d2 = A.peer_ptr(dst, dp.off["w2r"]) + (m * dp.slots + slot) * dp.w2_bytes
+                nat.check(lib.mb_memcpy_async(d1, dp.W1[loc].data_ptr(), dp.w1_bytes, cps.cuda_stream), lib,
+                          "replica push")
+                nat.check(lib.mb_memcpy_async(d2, dp.W2[loc].data_ptr(), dp.w2_bytes, cps.cuda_stream), lib,
+                          "replica push")
+            self.push_ev[m] = torch.cuda.Event()
+            self.push_ev[m].record(cps)
+        if not self._push_order and self._push_timer is not None:
+            self._push_timer.__exit__(None, None, None)
+            self._push_timer = None
 
     # -------------------------------------------------------------- comm stream
     def prepare(self, m0, m1, idx, gates):
@@ -868,7 +885,7 @@ class _StepOps:
     def dispatch(self, m, x, idx, gates, idx_all=None, gates_all=None):
         """D(m): routing side of m (unless prepared), K3 scatter into every rank's receive rows.
         With the step's [MB, ...] routing tensors (idx_all / gates_all), D(0) also prepares
-        micro-batches 1..MB-1 in one batch right after its scatter."""
+        micro-batches 1..MB-1 in one batch once its rows have landed."""
         dp, xs, st = self.dp, self.xs, self.st_x
         sh = dp.shape
         T, k, h = dp.T, sh.top_k, sh.hidden
@@ -878,11 +895,14 @@ class _StepOps:
             if self.hooks:
                 self.hooks.inputs_ready(m, xs)
             dp._k("mb_scatter_rows", x.data_ptr(), T, k, h, dp.perm[m].data_ptr(), dp.ptr_xr[m].data_ptr(), st)
-            if idx_all is not None and m == 0:
-                self.prepare(1, dp.MB, idx_all, gates_all)
+            self._issue_pushes(m if idx_all is None else None)
             if m in self.push_ev:
                 xs.wait_event(self.push_ev[m])  # this rank's replica pushes for micro-batch m
             dp.arena.barrier(xs)  # rows and replica weights of micro-batch m have landed everywhere
+        if idx_all is not None and m == 0:
+            # after D(0)'s barrier, beside F(0): only pad rows (disjoint from the real rows peers
+            # may already be storing) and this rank's own tables / receive gates are written
+            self.prepare(1, dp.MB, idx_all, gates_all)
 
     def _prepare_one(self, m, idx, gates):
         """Routing side of micro-batch m from its own [T, k] tensors (per-micro-batch API)."""
@@ -977,6 +997,7 @@ class _StepOps:
         experts) is done and overlaps part B; then both streams join the current stream."""
         dp, cs, xs = self.dp, self.cs, self.xs
         h, hp = dp.shape.hidden, dp.shape.ffn
+        self._issue_pushes()
         fresh = dp._wgrad_prepare()
         split = len(dp.wparts) > 1
         widen = WGRAD_ALL_SMS and dp.overlap and split   # measured slower at N=1 (single part)
