@@ -16,6 +16,7 @@
 //   to a multiple of 128 rows (the GEMM M tile).
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 
 #include "capi_common.cuh"
 #include "sm100_ptx.cuh"
@@ -282,23 +283,28 @@ __global__ void __launch_bounds__(256, 1) scatter_rows_tma_kernel(const uint8_t*
 // columns w*32 + lane + 256*r) in fp32 with the fixed i order and arithmetic of
 // combine_rows_kernel (bit-identical results) and release the slot on its empty barrier.
 constexpr int kConsumers = 8;
+// nsplit > 1: a slot holds one 1/nsplit column piece of the token's k rows (more, smaller slots in
+// flight for the same shared memory); work item = (token, piece).
 template <int KMAX>
 __global__ void __launch_bounds__(32 * (kConsumers + 1), 1)
     combine_rows_tma_kernel(const void* const* __restrict__ src_rows, const int2* __restrict__ perm,
                             const float* __restrict__ gate, int64_t T, int k, int h, uint4* __restrict__ out,
                             const float* const* __restrict__ src_scalar, float* __restrict__ scalar_out, int npart,
-                            int nslot) {
+                            int nslot, int nsplit) {
   extern __shared__ __align__(1024) uint8_t smem_t[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row_bytes = h * 2, vrow = h >> 3;
+  const int piece_bytes = row_bytes / nsplit, pvrow = vrow / nsplit;
   const bool scal = scalar_out != nullptr;
   const int side_bytes = KMAX * 16 + (scal ? KMAX * npart * 4 : 0);  // npart % 4 == 0 (host check)
-  const int64_t slot_bytes = static_cast<int64_t>(KMAX) * row_bytes + side_bytes;
+  const int64_t slot_bytes = static_cast<int64_t>(KMAX) * piece_bytes + side_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_t);
   uint64_t* empty = full + nslot;
   auto rows_of = [&](int s) { return smem_t + kTmaBarBytes + s * slot_bytes; };
-  auto meta = [&](int s) { return reinterpret_cast<int4*>(rows_of(s) + static_cast<int64_t>(KMAX) * row_bytes); };
-  auto scl = [&](int s) { return reinterpret_cast<float*>(rows_of(s) + static_cast<int64_t>(KMAX) * row_bytes + KMAX * 16); };
+  auto meta = [&](int s) { return reinterpret_cast<int4*>(rows_of(s) + static_cast<int64_t>(KMAX) * piece_bytes); };
+  auto scl = [&](int s) {
+    return reinterpret_cast<float*>(rows_of(s) + static_cast<int64_t>(KMAX) * piece_bytes + KMAX * 16);
+  };
   if (threadIdx.x == 0) {
     for (int b = 0; b < nslot; ++b) {
       mbar_init(&full[b], 1);
@@ -331,22 +337,28 @@ __global__ void __launch_bounds__(32 * (kConsumers + 1), 1)
     for (int64_t b = 0; b * kTB < n; ++b) {
       fetch(b + 1, pn, wn);
       for (int u = 0; u < kTB; ++u) {
-        const int64_t j = b * kTB + u;
-        if (j >= n) break;
-        const int s = static_cast<int>(j % nslot);
-        mbar_wait(&empty[s], static_cast<uint32_t>(((j / nslot) & 1) ^ 1));
+        const int64_t jt = b * kTB + u;
+        if (jt >= n) break;
         const bool mine = ub == u;
-        if (mine) meta(s)[ci] = make_int4(pc.x, pc.y, __float_as_int(wc), 0);
         const unsigned valid = __ballot_sync(0xffffffffu, mine && pc.x >= 0);
-        if (lane == 0) mbar_arrive_expect_tx(&full[s], __popc(valid) * (row_bytes + (scal ? npart * 4 : 0)));
-        __syncwarp();
-        if (mine && pc.x >= 0) {
-          bulk_load_1d(rows_of(s) + static_cast<int64_t>(ci) * row_bytes,
-                       reinterpret_cast<const uint8_t*>(src_rows[pc.x]) + static_cast<int64_t>(pc.y) * row_bytes,
-                       row_bytes, &full[s]);
-          if (scal)
-            bulk_load_1d(scl(s) + ci * npart, src_scalar[pc.x] + static_cast<int64_t>(pc.y) * npart, npart * 4,
-                         &full[s]);
+        for (int part = 0; part < nsplit; ++part) {
+          const int64_t j = jt * nsplit + part;
+          const int s = static_cast<int>(j % nslot);
+          mbar_wait(&empty[s], static_cast<uint32_t>(((j / nslot) & 1) ^ 1));
+          const bool with_scal = scal && part == 0;
+          if (mine) meta(s)[ci] = make_int4(pc.x, pc.y, __float_as_int(wc), 0);
+          if (lane == 0)
+            mbar_arrive_expect_tx(&full[s], __popc(valid) * (piece_bytes + (with_scal ? npart * 4 : 0)));
+          __syncwarp();
+          if (mine && pc.x >= 0) {
+            bulk_load_1d(rows_of(s) + static_cast<int64_t>(ci) * piece_bytes,
+                         reinterpret_cast<const uint8_t*>(src_rows[pc.x]) + static_cast<int64_t>(pc.y) * row_bytes +
+                             static_cast<int64_t>(part) * piece_bytes,
+                         piece_bytes, &full[s]);
+            if (with_scal)
+              bulk_load_1d(scl(s) + ci * npart, src_scalar[pc.x] + static_cast<int64_t>(pc.y) * npart, npart * 4,
+                           &full[s]);
+          }
         }
       }
       pc = pn;
@@ -355,12 +367,13 @@ __global__ void __launch_bounds__(32 * (kConsumers + 1), 1)
     return;
   }
   // -------------------------------------------------- consumers
-  for (int64_t j = 0; j < n; ++j) {
+  for (int64_t j = 0; j < n * nsplit; ++j) {
     const int s = static_cast<int>(j % nslot);
-    const int64_t t = blockIdx.x + j * gridDim.x;
+    const int64_t t = blockIdx.x + (j / nsplit) * gridDim.x;
+    const int part = static_cast<int>(j % nsplit);
     mbar_wait(&full[s], static_cast<uint32_t>((j / nslot) & 1));
     const int4* m = meta(s);
-    if (scal && warp == 0 && lane < k) {
+    if (scal && part == 0 && warp == 0 && lane < k) {
       float sc = 0.0f;
       if (m[lane].x >= 0) {
         const float* src = scl(s) + lane * npart;
@@ -369,14 +382,14 @@ __global__ void __launch_bounds__(32 * (kConsumers + 1), 1)
       scalar_out[t * k + lane] = sc;
     }
     const uint4* rows = reinterpret_cast<const uint4*>(rows_of(s));
-    for (int col = warp * 32 + lane; col < vrow; col += 32 * kConsumers) {
+    for (int col = warp * 32 + lane; col < pvrow; col += 32 * kConsumers) {
       float acc[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
       uint4 u4[KMAX];
 #pragma unroll
       for (int i = 0; i < KMAX; ++i)
-        if (i < k && m[i].x >= 0) u4[i] = rows[static_cast<int64_t>(i) * vrow + col];
+        if (i < k && m[i].x >= 0) u4[i] = rows[static_cast<int64_t>(i) * pvrow + col];
 #pragma unroll
       for (int i = 0; i < KMAX; ++i) {
         if (i >= k) break;
@@ -390,11 +403,89 @@ __global__ void __launch_bounds__(32 * (kConsumers + 1), 1)
           acc[2 * e + 1] += wi * bf16hi(u[e]);
         }
       }
-      out[t * vrow + col] = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
-                                       pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+      out[t * vrow + static_cast<int64_t>(part) * pvrow + col] =
+          make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]), pack_bf16x2(acc[4], acc[5]),
+                     pack_bf16x2(acc[6], acc[7]));
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
+// K6, confined register variant: warp per token, all k rows of a column chunk loaded before any
+// is accumulated (k * VPL 128-bit loads in flight per lane; the fixed-i fp32 accumulation of
+// combine_rows_kernel, so results are bit-identical).  Launched one 512-thread block per free SM
+// with a shared-memory reservation that keeps it off the GEMM's SMs.
+template <int KMAX, int VPL>
+__global__ void __launch_bounds__(512, 1) combine_rows_mlp_kernel(const void* const* __restrict__ src_rows,
+                                                                  const int2* __restrict__ perm,
+                                                                  const float* __restrict__ gate, int64_t T, int k,
+                                                                  int h, uint4* __restrict__ out,
+                                                                  const float* const* __restrict__ src_scalar,
+                                                                  float* __restrict__ scalar_out, int npart) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp_global = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int vrow = h >> 3;
+  for (int64_t t = warp_global; t < T; t += nwarps) {
+    int2 p = make_int2(-1, -1);
+    float w = 0.0f;
+    if (lane < k) {
+      p = perm[t * k + lane];
+      w = gate ? gate[t * k + lane] : 1.0f;
+    }
+    float sc = 0.0f;
+    if (scalar_out && lane < k && p.x >= 0) {
+      const float* src = src_scalar[p.x] + static_cast<int64_t>(p.y) * npart;
+      for (int q = 0; q < npart; ++q) sc += src[q];
+    }
+    const uint4* rowp[KMAX];
+    float wi[KMAX];
+#pragma unroll
+    for (int i = 0; i < KMAX; ++i) {
+      const int px = __shfl_sync(0xffffffffu, p.x, i);
+      const int py = __shfl_sync(0xffffffffu, p.y, i);
+      wi[i] = __shfl_sync(0xffffffffu, w, i);
+      rowp[i] = (i < k && px >= 0)
+                    ? reinterpret_cast<const uint4*>(src_rows[px]) + static_cast<int64_t>(py) * vrow
+                    : nullptr;
+    }
+    for (int col0 = 0; col0 < vrow; col0 += 32 * VPL) {
+      uint4 u[KMAX][VPL];
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i)
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+          const int col = col0 + j * 32 + lane;
+          if (rowp[i] && col < vrow) u[i][j] = rowp[i][col];
+        }
+      float acc[VPL][8];
+#pragma unroll
+      for (int j = 0; j < VPL; ++j)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[j][q] = 0.0f;
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i) {
+        if (!rowp[i]) continue;
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+          const uint32_t uu[4] = {u[i][j].x, u[i][j].y, u[i][j].z, u[i][j].w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            acc[j][2 * q] += wi[i] * bf16lo(uu[q]);
+            acc[j][2 * q + 1] += wi[i] * bf16hi(uu[q]);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) {
+        const int col = col0 + j * 32 + lane;
+        if (col < vrow)
+          out[t * vrow + col] = make_uint4(pack_bf16x2(acc[j][0], acc[j][1]), pack_bf16x2(acc[j][2], acc[j][3]),
+                                           pack_bf16x2(acc[j][4], acc[j][5]), pack_bf16x2(acc[j][6], acc[j][7]));
+      }
+    }
+    if (scalar_out && lane < k) scalar_out[t * k + lane] = sc;
   }
 }
 
@@ -619,17 +710,39 @@ extern "C" int mb_combine_rows(const void* const* src_rows, const int32_t* perm,
   const int vrow = h / 8;
   const int2* pr = reinterpret_cast<const int2*>(perm);
   uint4* o = reinterpret_cast<uint4*>(out);
+  const char* ce = std::getenv("MB_COMBINE_ENGINE");
+  if (const int nb = comm_blocks(); nb > 0 && k <= 8 && !(ce && std::string(ce) == "tma")) {
+    // confined register engine: the smem reservation keeps the blocks off the GEMM's SMs
+    constexpr int kReserve = 100 * 1024;
+    const int kmax = k <= 2 ? 2 : k <= 4 ? 4 : 8;
+    auto launch = [&](auto kern) -> int {
+      MB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kReserve));
+      kern<<<nb, 512, kReserve, s>>>(src_rows, pr, gate, T, k, h, o, src_scalar, scalar_out, npart);
+      MB_CUDA_TRY(cudaGetLastError());
+      return MB_OK;
+    };
+    if (kmax == 2) return launch(combine_rows_mlp_kernel<2, 4>);
+    if (kmax == 4) return launch(combine_rows_mlp_kernel<4, 2>);
+    return launch(combine_rows_mlp_kernel<8, 2>);
+  }
   if (const int nb = comm_blocks(); nb > 0 && k <= 16 && (!scalar_out || (npart % 4 == 0 && npart <= 64))) {
     const int kmax = k <= 2 ? 2 : k <= 4 ? 4 : k <= 8 ? 8 : 16;
-    const int64_t slot_bytes = static_cast<int64_t>(kmax) * 2 * h + kmax * 16 + (scalar_out ? kmax * npart * 4 : 0);
+    // whole rows per slot (MB_COMBINE_SPLIT=n: 1/n pieces -- measured n times slower: the cost is
+    // per bulk operation, not per byte)
+    int nsplit = 1;
+    if (const char* e = std::getenv("MB_COMBINE_SPLIT")) nsplit = std::max(1, std::atoi(e));
+    auto slot_of = [&](int ns) {
+      return static_cast<int64_t>(kmax) * (2 * h / ns) + kmax * 16 + (scalar_out ? kmax * npart * 4 : 0);
+    };
+    const int64_t slot_bytes = slot_of(nsplit);
     int nslot = static_cast<int>((kTmaSmemBudget - kTmaBarBytes) / slot_bytes);
     if (nslot > 64) nslot = 64;
-    if (nslot >= 2) {
+    if (nslot >= 2 && (2 * h) % (16 * nsplit) == 0) {
       const int smem = kTmaBarBytes + static_cast<int>(nslot * slot_bytes);
       auto launch = [&](auto kern) -> int {
         MB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         kern<<<nb, 32 * (kConsumers + 1), smem, s>>>(src_rows, pr, gate, T, k, h, o, src_scalar, scalar_out, npart,
-                                                     nslot);
+                                                     nslot, nsplit);
         MB_CUDA_TRY(cudaGetLastError());
         return MB_OK;
       };
