@@ -47,6 +47,21 @@ int mbp_anneal_reorder(const double* x, int32_t nodes, int32_t gpn, int32_t E, i
                        double cooling, double eps_frac, double term_eps, double beta, const int64_t* extra,
                        int32_t nextra, int32_t threads, int64_t* assignment, int64_t* iterations);
 
+/* Device annealing (GPU-side planning): the chains of anneal_reorder run on the GPU
+ * (mb_anneal_chains, include/mb_kernels.h), one thread per seed.  mbp_anneal_prepare computes what
+ * they share exactly as mbp_anneal_reorder does on the host -- the LPT start (base[E]), the
+ * contribution tensor contrib[E][G][5][G] (reorder.py:179-194), the time units consts[5] =
+ * {comp_unit, nv_tx, nv_rx, rd_tx, rd_rx seconds per row} -- and each seed's numpy PCG64 state
+ * rng[nseeds][4] = {state_hi, state_lo, inc_hi, inc_lo} (SeedSequence(seed), reorder.py:303).
+ * mbp_anneal_select returns the first minimum of the exact T_MoE over ncand candidate plans
+ * (LPT, extras, chains in seed order: reorder.py:352-362). */
+int mbp_anneal_prepare(const double* x, int32_t nodes, int32_t gpn, int32_t E, int64_t hidden, int64_t inter,
+                       double flops, double bw_nv, double bw_rd, double bpt, double beta, const uint64_t* seeds,
+                       int32_t nseeds, int64_t* base, double* contrib, double* consts, uint64_t* rng);
+int mbp_anneal_select(const double* x, int32_t nodes, int32_t gpn, int32_t E, int64_t hidden, int64_t inter,
+                      double flops, double bw_nv, double bw_rd, double bpt, double beta, const int64_t* cands,
+                      int32_t ncand, int64_t* assignment);
+
 /* Data-locality sample placement (reorder.py:365-568): greedy_sample_initial (greedy_only != 0)
  * or anneal_sample_placement (greedy start, one swap-SA chain per seed over samples inside each
  * micro-batch's +/-band token window, best exact summed T_MoE).  counts [S][L][E] (float64 of

@@ -16,7 +16,8 @@ from .loads import (CostEstimate, LoadVector, SmoothingConfig, comm_row_times, c
                     compute_loads, flow_matrix, lse, moe_time, smoothed_moe_time)
 from .policies import (POLICIES, PlanBundle, SimConfigs, SimReport, build_policy_bundle, compare_report,
                        evaluate_bundle, run_baseline, solve_tasks)
-from .reordering import (AnnealConfig, ReorderPlan, SamplePlacement, anneal_reorder, anneal_sample_placement,
+from .reordering import (AnnealConfig, ReorderPlan, SamplePlacement, anneal_reorder, anneal_reorder_device,
+                         anneal_sample_placement,
                          apply_plan, greedy_sample_initial, lpt_initial, rewrite_trace_matrices, static_plan)
 from .replication import (InstanceTooLargeError, ReplicaConfig, ReplicaPlacement, ReplicationEntry,
                           ReplicationPlan, SplitPlan, candidate_gpus, greedy_replicate, replica_memory, round_split,

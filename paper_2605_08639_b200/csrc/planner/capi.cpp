@@ -89,6 +89,24 @@ extern "C" int mbp_anneal_reorder(const double* x, int32_t nodes, int32_t gpn, i
                               nextra, threads, assignment, iterations);)
 }
 
+extern "C" int mbp_anneal_prepare(const double* x, int32_t nodes, int32_t gpn, int32_t E, int64_t hidden,
+                                  int64_t inter, double flops, double bw_nv, double bw_rd, double bpt, double beta,
+                                  const uint64_t* seeds, int32_t nseeds, int64_t* base, double* contrib,
+                                  double* consts, uint64_t* rng) {
+  if (int rc = check_topo(nodes, gpn)) return rc;
+  if (nseeds < 0) return fail(kInvalid, "bad seed count");
+  GUARD(Topo t(nodes, gpn); Hw hw{flops, bw_nv, bw_rd, bpt};
+        return anneal_prepare(x, t, E, hidden, inter, hw, beta, seeds, nseeds, base, contrib, consts, rng);)
+}
+
+extern "C" int mbp_anneal_select(const double* x, int32_t nodes, int32_t gpn, int32_t E, int64_t hidden,
+                                 int64_t inter, double flops, double bw_nv, double bw_rd, double bpt, double beta,
+                                 const int64_t* cands, int32_t ncand, int64_t* assignment) {
+  if (int rc = check_topo(nodes, gpn)) return rc;
+  GUARD(Topo t(nodes, gpn); Hw hw{flops, bw_nv, bw_rd, bpt};
+        return anneal_select(x, t, E, hidden, inter, hw, beta, cands, ncand, assignment);)
+}
+
 extern "C" int mbp_sample_placement(int32_t nodes, int32_t gpn, int32_t E, int32_t L, int32_t MB, int32_t S,
                                     const double* counts, const int32_t* micro_batch, const int64_t* source_gpu,
                                     const double* tokens, const int64_t* plans, int64_t hidden, int64_t inter,

@@ -84,6 +84,13 @@ class PCG64 {
     state_ += initstate;
     step();
   }
+  // raw generator state {state_hi, state_lo, inc_hi, inc_lo} (a fresh stream: no buffered half)
+  void raw(uint64_t* out4) const {
+    out4[0] = static_cast<uint64_t>(state_ >> 64);
+    out4[1] = static_cast<uint64_t>(state_);
+    out4[2] = static_cast<uint64_t>(inc_ >> 64);
+    out4[3] = static_cast<uint64_t>(inc_);
+  }
   uint64_t next64() {
     step();
     const uint64_t hi = static_cast<uint64_t>(state_ >> 64), lo = static_cast<uint64_t>(state_);

@@ -69,6 +69,11 @@ int anneal_samples(const Topo& t, int E, int L, int MB, int S, const double* cou
 int anneal_reorder(const double* x, const Topo& t, int E, int64_t h, int64_t hp, const Hw& hw, const uint64_t* seeds,
                    int nseeds, double cooling, double eps_frac, double term_eps, double beta, const int64_t* extra,
                    int nextra, int threads, int64_t* out, int64_t* iters_total);
+int anneal_prepare(const double* x, const Topo& t, int E, int64_t h, int64_t hp, const Hw& hw, double beta,
+                   const uint64_t* seeds, int nseeds, int64_t* base_out, double* contrib_out, double* consts_out,
+                   uint64_t* rng_out);
+int anneal_select(const double* x, const Topo& t, int E, int64_t h, int64_t hp, const Hw& hw, double beta,
+                  const int64_t* cands, int ncand, int64_t* out);
 
 std::vector<int> candidate_gpus(int e, const std::vector<int64_t>& home, const Topo& t);
 int greedy_replicate(const double* x, int E, const int64_t* home, const Topo& t, int64_t h, int64_t hp, const Hw& hw,

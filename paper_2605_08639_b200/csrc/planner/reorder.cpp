@@ -227,4 +227,41 @@ int anneal_reorder(const double* x, const Topo& t, int E, int64_t h, int64_t hp,
   return kOk;
 }
 
+// Device-chain support (mb_anneal_chains in the sm_100a library runs _run_chain, one GPU thread
+// per seed): the inputs every chain shares -- LPT start, contribution tensor, time units -- and
+// each seed's PCG64 state, computed exactly as anneal_reorder does on the host.
+int anneal_prepare(const double* x, const Topo& t, int E, int64_t h, int64_t hp, const Hw& hw, double beta,
+                   const uint64_t* seeds, int nseeds, int64_t* base_out, double* contrib_out, double* consts_out,
+                   uint64_t* rng_out) {
+  const int G = t.G;
+  if (E % G != 0) return fail(kInvalid, "%d experts not divisible by %d GPUs", E, G);
+  lpt_initial(x, G, E, base_out);
+  AnnealShared sh(x, E, t, h, hp, hw, beta);
+  std::copy(sh.contrib.begin(), sh.contrib.end(), contrib_out);
+  consts_out[0] = sh.comp_unit;
+  for (int r = 0; r < 4; ++r) consts_out[1 + r] = sh.row_units[r];
+  for (int s = 0; s < nseeds; ++s) PCG64{SeedSequence(seeds[s])}.raw(rng_out + size_t(4) * s);
+  return kOk;
+}
+
+// anneal_reorder's final choice: first minimum of the exact T_MoE over the candidate plans
+// (LPT, extra plans, chains in seed order; reorder.py:352-362).
+int anneal_select(const double* x, const Topo& t, int E, int64_t h, int64_t hp, const Hw& hw, double beta,
+                  const int64_t* cands, int ncand, int64_t* out) {
+  if (ncand < 1) return fail(kInvalid, "no candidate plans");
+  AnnealShared sh(x, E, t, h, hp, hw, beta);
+  int best = 0;
+  double best_t = std::numeric_limits<double>::infinity();
+  for (int c = 0; c < ncand; ++c) {
+    AnnealChainState st(sh, &cands[size_t(c) * E]);
+    const double tt = st.exact(st.loads5.data());
+    if (tt < best_t) {
+      best_t = tt;
+      best = c;
+    }
+  }
+  std::copy(&cands[size_t(best) * E], &cands[size_t(best + 1) * E], out);
+  return kOk;
+}
+
 }  // namespace mbp
