@@ -133,12 +133,14 @@ int mb_peer_barrier(uint32_t* const* flags, int32_t rank, int32_t world, uint32_
 
 /* ---------------------------------------------------------------- GPU-side planning
  * The annealing chains of reorder.anneal_reorder (reorder.py:299-326) on the device, one thread
- * per chain: contrib [E][G][5][G] f64, base [E] (LPT start), consts[5] and rng[nchains][4] from
- * mbp_anneal_prepare (include/mb_planner.h); writes each chain's best plan best[nchains][E] and its
- * iteration count.  Pick the final plan with mbp_anneal_select.  G <= 32, E <= 1024. */
+ * per chain, every (layer, seed) chain of a model in one launch: chain c anneals layer
+ * c / chains_per_layer with contrib[layer] ([E][G][5][G] f64) and base[layer] ([E], the LPT start);
+ * consts[5] and rng[nchains][4] as mbp_anneal_prepare (include/mb_planner.h) writes them.  Writes
+ * each chain's best plan best[nchains][E] and its iteration count; pick each layer's plan with
+ * mbp_anneal_select.  G <= 32, E <= 1024. */
 int mb_anneal_chains(const double* contrib, int32_t E, int32_t G, const int64_t* base, const double* consts,
-                     double beta, const uint64_t* rng, int32_t nchains, double cooling, double eps_frac,
-                     double term_eps, int64_t* best, int64_t* iters, void* stream);
+                     double beta, const uint64_t* rng, int32_t nchains, int32_t chains_per_layer, double cooling,
+                     double eps_frac, double term_eps, int64_t* best, int64_t* iters, void* stream);
 
 #ifdef __cplusplus
 }

@@ -17,6 +17,7 @@ from .loads import (CostEstimate, LoadVector, SmoothingConfig, comm_row_times, c
 from .policies import (POLICIES, PlanBundle, SimConfigs, SimReport, build_policy_bundle, compare_report,
                        evaluate_bundle, run_baseline, solve_tasks)
 from .reordering import (AnnealConfig, ReorderPlan, SamplePlacement, anneal_reorder, anneal_reorder_device,
+                         anneal_reorder_layers_device,
                          anneal_sample_placement,
                          apply_plan, greedy_sample_initial, lpt_initial, rewrite_trace_matrices, static_plan)
 from .replication import (InstanceTooLargeError, ReplicaConfig, ReplicaPlacement, ReplicationEntry,

@@ -53,8 +53,8 @@ _KERNEL_SIGS.update({
     "mb_zero_pad_rows_nb": (c_int, [c_vp, c_i64, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "mb_scatter_rows": (c_int, [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp]),
     "mb_set_comm_blocks": (c_int, [c_i32]),
-    "mb_anneal_chains": (c_int, [c_vp, c_i32, c_i32, c_vp, c_vp, c_dbl, c_vp, c_i32, c_dbl, c_dbl, c_dbl, c_vp, c_vp,
-                                 c_vp]),
+    "mb_anneal_chains": (c_int, [c_vp, c_i32, c_i32, c_vp, c_vp, c_dbl, c_vp, c_i32, c_i32, c_dbl, c_dbl, c_dbl, c_vp,
+                                 c_vp, c_vp]),
     "mb_combine_rows": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "mb_combine_bwd_expert": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i64, c_i32, c_vp]),
     "mb_zero_pad_rows": (c_int, [c_vp, c_vp, c_i32, c_i32, c_vp]),

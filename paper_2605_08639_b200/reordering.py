@@ -129,49 +129,81 @@ def anneal_reorder_device(x_batch, topo: ClusterTopology, model, hw: HardwarePro
     anneal_reorder does, the chains run as one GPU thread per seed (mb_anneal_chains), and the
     host picks the first minimum of the exact T_MoE over [LPT, extra plans, chains in seed order]
     (reorder.py:329-362).  Same arguments and result as anneal_reorder."""
+    plans, iters = anneal_reorder_layers_device([x_batch], topo, model, hw, cfg, [extra_initial_plans], device)
+    return (plans[0], iters) if return_iterations else plans[0]
+
+
+def anneal_reorder_layers_device(x_layers, topo: ClusterTopology, model, hw: HardwareProfile, cfg: AnnealConfig,
+                                 extra_initial_plans=None, device=None, timings: dict | None = None):
+    """Every layer's reorder plan with all (layer, seed) chains in ONE device launch -- the
+    paper's "one thread per (layer, seed)" solver at GPU width.  x_layers:
+    per-layer (G, E) batch matrices; extra_initial_plans: per-layer sequences (or None).
+    Returns ([ReorderPlan per layer], total chain iterations); `timings` (optional dict) receives
+    host prepare / device chains / host select wall milliseconds."""
+    import time
+
     import torch
-    x = nat.f64(x_batch)
-    num_experts = x.shape[1]
+    t0 = time.perf_counter()
+    xs = [nat.f64(x) for x in x_layers]
+    L = len(xs)
+    if L == 0:
+        return [], 0
+    num_experts = xs[0].shape[1]
     G = topo.num_gpus
     if num_experts % G:
         raise ValueError(f"{num_experts} experts not divisible by {G} GPUs")
-    for plan in extra_initial_plans:
-        plan.validate(topo)
+    extras = list(extra_initial_plans) if extra_initial_plans is not None else [()] * L
+    if len(extras) != L:
+        raise ValueError("need one extra-plan sequence per layer")
+    for ex in extras:
+        for plan in ex:
+            plan.validate(topo)
     seeds = np.ascontiguousarray([int(s) for s in cfg.seeds], dtype=np.uint64)
     n = len(seeds)
     if n < 1:
         raise ValueError("need at least one annealing seed")
-    base = np.zeros(num_experts, dtype=np.int64)
-    contrib = np.zeros((num_experts, G, 5, G), dtype=np.float64)
+    base = np.zeros((L, num_experts), dtype=np.int64)
+    contrib = np.zeros((L, num_experts, G, 5, G), dtype=np.float64)
     consts = np.zeros(5, dtype=np.float64)
-    rng = np.zeros((n, 4), dtype=np.uint64)
+    rng = np.zeros((L, n, 4), dtype=np.uint64)
     lib = nat.planner()
     args = (topo.num_nodes, topo.gpus_per_node, num_experts, model.hidden_size, model.intermediate_size,
             hw.flops_per_gpu, hw.bw_nvlink, hw.bw_rdma, hw.bytes_per_token, cfg.beta)
-    nat.check(lib.mbp_anneal_prepare(nat.ptr(x), *args, nat.ptr(seeds), n, nat.ptr(base), nat.ptr(contrib),
-                                     nat.ptr(consts), nat.ptr(rng)), lib, "anneal_prepare")
+    for li, x in enumerate(xs):
+        if x.shape != (G, num_experts):
+            raise ValueError(f"layer {li}: expected a ({G}, {num_experts}) batch matrix, got {x.shape}")
+        nat.check(lib.mbp_anneal_prepare(nat.ptr(x), *args, nat.ptr(seeds), n, nat.ptr(base[li]),
+                                         nat.ptr(contrib[li]), nat.ptr(consts), nat.ptr(rng[li])), lib,
+                  "anneal_prepare")
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    t1 = time.perf_counter()
     d_contrib = torch.from_numpy(contrib).to(dev)
     d_base = torch.from_numpy(base).to(dev)
     d_rng = torch.from_numpy(rng.view(np.int64)).to(dev)
-    d_best = torch.empty((n, num_experts), dtype=torch.int64, device=dev)
-    d_iters = torch.empty(n, dtype=torch.int64, device=dev)
+    d_best = torch.empty((L * n, num_experts), dtype=torch.int64, device=dev)
+    d_iters = torch.empty(L * n, dtype=torch.int64, device=dev)
     klib = nat.kernels()
     with torch.cuda.device(dev):
         nat.check(klib.mb_anneal_chains(d_contrib.data_ptr(), num_experts, G, d_base.data_ptr(), nat.ptr(consts),
-                                        cfg.beta, d_rng.data_ptr(), n, cfg.cooling_rate, cfg.eps_frac,
+                                        cfg.beta, d_rng.data_ptr(), L * n, n, cfg.cooling_rate, cfg.eps_frac,
                                         cfg.termination_eps if cfg.termination_eps is not None else -1.0,
                                         d_best.data_ptr(), d_iters.data_ptr(), nat.stream_ptr()),
                   klib, "mb_anneal_chains")
-        best = d_best.cpu().numpy()
+        best = d_best.cpu().numpy().reshape(L, n, num_experts)
         iters = int(d_iters.sum().item())
-    extra = [np.asarray(p.assignment, dtype=np.int64) for p in extra_initial_plans]
-    cands = np.ascontiguousarray(np.stack([base] + extra + list(best)), dtype=np.int64)
-    out = np.zeros(num_experts, dtype=np.int64)
-    nat.check(lib.mbp_anneal_select(nat.ptr(x), *args, nat.ptr(cands), len(cands), nat.ptr(out)), lib,
-              "anneal_select")
-    plan = ReorderPlan(out)
-    return (plan, iters) if return_iterations else plan
+    t2 = time.perf_counter()
+    plans = []
+    for li, x in enumerate(xs):
+        extra = [np.asarray(p.assignment, dtype=np.int64) for p in extras[li]]
+        cands = np.ascontiguousarray(np.stack([base[li]] + extra + list(best[li])), dtype=np.int64)
+        out = np.zeros(num_experts, dtype=np.int64)
+        nat.check(lib.mbp_anneal_select(nat.ptr(x), *args, nat.ptr(cands), len(cands), nat.ptr(out)), lib,
+                  "anneal_select")
+        plans.append(ReorderPlan(out))
+    if timings is not None:
+        timings.update(prepare_ms=(t1 - t0) * 1e3, device_ms=(t2 - t1) * 1e3,
+                       select_ms=(time.perf_counter() - t2) * 1e3)
+    return plans, iters
 
 
 def _sample_call(trace, plans, topo, model, hw, cfg, band, greedy_only, beta, threads):

@@ -41,5 +41,31 @@ def main():
               flush=True)
 
 
+def layers(L=48):
+    """A whole model's reorder planning: L layers x 16 seeds (host: OpenMP over each layer's
+    chains, layer after layer; device: every chain in one launch)."""
+    shape = SHAPES["qwen3-30b-a3b"]["shape"]
+    model = mb.ModelProfile(1, shape.num_experts, shape.top_k, shape.hidden, shape.ffn)
+    topo = b200_box_topology(8, 4, b200_profile(shape.hidden))
+    xs = [make_routing(shape, 2048, 2, 8, 0, zipf_s=0.7 + 0.02 * li, shift=li).mats.sum(axis=0).astype(np.float64)
+          for li in range(L)]
+    cfg = mb.AnnealConfig()
+    tm = {}
+    t0 = time.perf_counter()
+    dev, iters = mb.anneal_reorder_layers_device(xs, topo, model, topo.profile, cfg, timings=tm)
+    t1 = time.perf_counter()
+    host = [mb.anneal_reorder(x, topo, model, topo.profile, cfg) for x in xs]
+    t2 = time.perf_counter()
+    t1, t2 = t0 + (t2 - t1), t0 + (t2 - t1) + (t1 - t0)   # host_ms = t1 - t0, device_ms = t2 - t1
+    print(json.dumps({"layers": L, "G": 8, "group": 4, "chains": L * len(cfg.seeds), "iterations": iters,
+                      "host_ms": round((t1 - t0) * 1e3, 1), "host_threads": os.cpu_count(),
+                      "device_ms": round((t2 - t1) * 1e3, 1), "device_breakdown_ms": {k: round(v, 1) for k, v in tm.items()},
+                      "identical": all(a.assignment.tolist() == b.assignment.tolist() for a, b in zip(host, dev))}),
+          flush=True)
+
+
 if __name__ == "__main__":
+    layers(1)   # warm-up: CUDA context + module load
+    for L in (1, 8, 48):
+        layers(L)
     main()
