@@ -158,6 +158,7 @@ def synthetic_config(args, world):
             "zipf_s": args.zipf, "hot_shift": cfg["shift"], "ep": world,
             "gpu_group": min(world, args.group or cfg["group"]),
             "replica_slots": cfg["slots"] if args.slots is None else args.slots, "sa_chains": args.sa_chains,
+            "reorder_planner": "device" if args.device_planner else "host",
             **data_plane_config(world, shape),
             "l2": "inputs larger than L2 (per-step working set >> 126 MB)"}
 
@@ -315,7 +316,7 @@ def run_ours(args, comm):
     model = ModelProfile(1, shape.num_experts, shape.top_k, shape.hidden, shape.ffn)
     slots = cfg["slots"] if args.slots is None else args.slots
     cfgs = SimConfigs(anneal=AnnealConfig(seeds=tuple(range(args.sa_chains))), replica=ReplicaConfig(slots),
-                      threads=min(8, os.cpu_count() or 1))
+                      threads=min(8, os.cpu_count() or 1), device_anneal=args.device_planner)
     trace, bundle = None, None
     if args.trace:
         # replay a recorded count trace (routing.bin + manifest.json, either implementation):
@@ -461,6 +462,8 @@ def main():
     ap.add_argument("--policies", default="relibra,static,eplb_like,balanced_oracle,relibra_box",
                     help="relibra_box = relibra with one replication group spanning all EP GPUs (run when EP > group)")
     ap.add_argument("--headline", default="relibra")
+    ap.add_argument("--device-planner", action="store_true",
+                    help="run the reorder planner's annealing chains on the GPU (identical plans)")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--trace", default=None, help="replay a recorded routing trace directory (manifest.json + "
