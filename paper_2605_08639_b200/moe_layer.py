@@ -817,7 +817,7 @@ class _StepOps:
         self.st_x = self.xs.cuda_stream
         self.xs.wait_stream(self.cs)
         self.push_ev = {}
-        A, cps = dp.arena, dp.cps
+        cps = dp.cps
         # K5 replica pushes (copy engine), in micro-batch order; dispatch(m) waits for micro-batch
         # m's pushes before its final barrier, so the first GEMMs need not wait for the whole
         # step's replica weights.  Only micro-batch 0's are enqueued here; the rest go right after
