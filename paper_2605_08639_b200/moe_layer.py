@@ -759,6 +759,11 @@ class MoEDataPlane:
             if m >= 1:
                 order.append(("b", m - 1))
         order.append(("b", self.MB - 1))
+        # micro-batch 0's rows arrive in head_parts pieces and the last micro-batch's dx leaves in
+        # as many: the scatter of the first piece and the read-back of the first piece overlap the
+        # rest of the copy (only the step's head and tail copies are exposed)
+        head_parts = tail_parts = 2
+        last = self.MB - 1
         with torch.cuda.stream(h2d):
             for kind, m in order:
                 if kind == "r":
@@ -767,18 +772,30 @@ class MoEDataPlane:
                     rready = torch.cuda.Event()
                     rready.record(h2d)
                     continue
-                for key in (("x",) if kind == "f" else ("dout",)):
-                    dev[key][m].copy_(host[key][m], non_blocking=True)
+                if kind == "f":
+                    evs = []
+                    for t0, t1 in _token_parts(self.T, head_parts if m == 0 else 1):
+                        dev["x"][m][t0:t1].copy_(host["x"][m][t0:t1], non_blocking=True)
+                        ev = torch.cuda.Event()
+                        ev.record(h2d)
+                        evs.append(ev)
+                    ready[m] = evs
+                    continue
+                dev["dout"][m].copy_(host["dout"][m], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(h2d)
-                (ready if kind == "f" else dready)[m] = ev
+                dready[m] = ev
+        T = self.T
 
         class _Hooks:
             def routing_ready(self, stream):
                 stream.wait_event(rready)
 
-            def inputs_ready(self, m, stream):
-                stream.wait_event(ready[m])
+            def input_parts(self, m):
+                return len(ready[m])
+
+            def inputs_ready(self, m, stream, part=0):
+                stream.wait_event(ready[m][part])
 
             def dout_ready(self, m, stream):
                 stream.wait_event(dready[m])
@@ -788,11 +805,15 @@ class MoEDataPlane:
                 with torch.cuda.stream(d2h):
                     host["out"][m].copy_(dev["out"][m], non_blocking=True)
 
-            def after_backward(self, m, stream):
+            def output_parts(self, m):
+                return tail_parts if m == last else 1
+
+            def after_backward(self, m, stream, part=0):
+                t0, t1 = _token_parts(T, self.output_parts(m))[part]
                 d2h.wait_stream(stream)
                 with torch.cuda.stream(d2h):
-                    host["dx"][m].copy_(dev["dx"][m], non_blocking=True)
-                    host["dgate"][m].copy_(dev["dgate"][m], non_blocking=True)
+                    host["dx"][m][t0:t1].copy_(dev["dx"][m][t0:t1], non_blocking=True)
+                    host["dgate"][m][t0:t1].copy_(dev["dgate"][m][t0:t1], non_blocking=True)
 
         # the compute stream reads the dispatched rows only, so only the comm stream waits on inputs
         self.forward_backward(dev["x"], dev["idx"], dev["gates"], dev["dout"], dev["out"], dev["dx"], dev["dgate"],
@@ -803,6 +824,12 @@ class MoEDataPlane:
     def close(self) -> None:
         torch.cuda.synchronize(self.device)
         self.arena.close()
+
+
+def _token_parts(T: int, parts: int):
+    """[t0, t1) ranges splitting T tokens into `parts` near-equal pieces."""
+    b = [T * i // parts for i in range(parts + 1)]
+    return [(b[i], b[i + 1]) for i in range(parts) if b[i + 1] > b[i]]
 
 
 class _StepOps:
@@ -892,9 +919,13 @@ class _StepOps:
         with dp._timed(dp.remote_rows(m)[0] * 2 * h, "comm_dispatch", xs):
             if m not in self.prepared:
                 self._prepare_one(m, idx, gates)
-            if self.hooks:
-                self.hooks.inputs_ready(m, xs)
-            dp._k("mb_scatter_rows", x.data_ptr(), T, k, h, dp.perm[m].data_ptr(), dp.ptr_xr[m].data_ptr(), st)
+            # the host-buffer step lands micro-batch 0's rows in parts: scatter each as it arrives
+            parts = self.hooks.input_parts(m) if self.hooks and hasattr(self.hooks, "input_parts") else 1
+            for p, (t0, t1) in enumerate(_token_parts(T, parts)):
+                if self.hooks:
+                    self.hooks.inputs_ready(m, xs, p)
+                dp._k("mb_scatter_rows", x[t0:].data_ptr(), t1 - t0, k, h, dp.perm[m][t0:].data_ptr(),
+                      dp.ptr_xr[m].data_ptr(), st)
             self._issue_pushes(m if idx_all is None else None)
             if m in self.push_ev:
                 xs.wait_event(self.push_ev[m])  # this rank's replica pushes for micro-batch m
@@ -952,10 +983,14 @@ class _StepOps:
         h = dp.shape.hidden
         with dp._timed(dp.remote_rows(m)[0] * 2 * h, "comm_unpermute", xs):
             dp.arena.barrier(xs)  # dX rows / dgate partials of micro-batch m complete everywhere
-            dp._k("mb_combine_rows", dp.ptr_dxp[m].data_ptr(), dp.perm[m].data_ptr(), None, dp.T, dp.shape.top_k, h,
-                  dx.data_ptr(), dp.ptr_dgate[m].data_ptr(), dgate.data_ptr(), dp.npart, self.st_x)
-            if self.hooks:
-                self.hooks.after_backward(m, xs)
+            # the host-buffer step reads the last micro-batch's dx back in parts, each as it is done
+            parts = self.hooks.output_parts(m) if self.hooks and hasattr(self.hooks, "output_parts") else 1
+            for p, (t0, t1) in enumerate(_token_parts(dp.T, parts)):
+                dp._k("mb_combine_rows", dp.ptr_dxp[m].data_ptr(), dp.perm[m][t0:].data_ptr(), None, t1 - t0,
+                      dp.shape.top_k, h, dx[t0:].data_ptr(), dp.ptr_dgate[m].data_ptr(), dgate[t0:].data_ptr(),
+                      dp.npart, self.st_x)
+                if self.hooks:
+                    self.hooks.after_backward(m, xs, p)
 
     # -------------------------------------------------------------- compute stream
     def fwd_gemms(self, m):
