@@ -63,3 +63,23 @@ def test_migration_moves_cover_every_expert_once():
             assert old[e] == src and int(np.flatnonzero(old == src)[ss]) == e
             seen.append(e)
     assert sorted(seen) == list(range(E))
+
+
+@pytest.mark.parametrize("T,parts", [(8192, 1), (8192, 2), (7, 2), (5, 3), (1, 2), (0, 2)])
+def test_token_parts_cover_every_token_once(T, parts):
+    from paper_2605_08639_b200.moe_layer import _token_parts
+    ranges = _token_parts(T, parts)
+    covered = [t for a, b in ranges for t in range(a, b)]
+    assert covered == list(range(T))
+    assert all(b > a for a, b in ranges) and len(ranges) <= parts
+
+
+def test_comm_sm_defaults():
+    """Row movers: 20 SMs at N=1 (register engine), 32 at N>1, 8 for wide-FFN experts."""
+    from paper_2605_08639_b200 import moe_layer as ml
+    from paper_2605_08639_b200.workload import SHAPES
+    assert ml.default_comm_sms(1, SHAPES["qwen3-30b-a3b"]["shape"]) == 20
+    assert ml.default_comm_sms(8, SHAPES["qwen3-30b-a3b"]["shape"]) == 32
+    assert ml.default_comm_sms(4, SHAPES["qwen3-235b-a22b"]["shape"]) == 32
+    assert ml.default_comm_sms(4, SHAPES["mixtral-8x7b"]["shape"]) == 8
+    assert ml.ROW_MOVERS[1] == "regs" and ml.ROW_MOVERS_MULTI == "tma"
