@@ -400,7 +400,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
             tmem_ld_wait();
             release();
             pack_bf16_words(a0, a1, w);
-            st.put<false>(w, &p.tmC, tc.nb * TN + ocol(ch2), out_row0);
+            st.template put<false>(w, &p.tmC, tc.nb * TN + ocol(ch2), out_row0);
           } else {
             tmem_ld_32x32b_x32(t_acc + tcol(0), a0);
             tmem_ld_32x32b_x32(t_acc + tcol(0) + 32, a1);
@@ -409,9 +409,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
             tmem_ld_wait();
             release();
             pack_bf16_words(a0, a1, w);
-            st.put<false>(w, &p.tmC, tc.nb * TN + ocol(0), out_row0);
+            st.template put<false>(w, &p.tmC, tc.nb * TN + ocol(0), out_row0);
             pack_bf16_words(b0, b1, w);
-            st.put<false>(w, &p.tmC, tc.nb * TN + ocol(1), out_row0);
+            st.template put<false>(w, &p.tmC, tc.nb * TN + ocol(1), out_row0);
           }
         } else if constexpr (kEpi == EPI_SWIGLU) {
           // gate columns [0,128), up columns [128,256); this warp owns gate/up features [f0, +64)
@@ -437,8 +437,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
             g1[i] = pack_bf16x2(__uint_as_float(g1[2 * i]), __uint_as_float(g1[2 * i + 1]));
             u1[i] = pack_bf16x2(__uint_as_float(u1[2 * i]), __uint_as_float(u1[2 * i + 1]));
           }
-          st.put2<false>(g0, g1, &p.tmC, tc.nb * TN + f0, out_row0);
-          st.put2<false>(u0, u1, &p.tmC, tc.nb * TN + 128 + f0, out_row0);
+          st.template put2<false>(g0, g1, &p.tmC, tc.nb * TN + f0, out_row0);
+          st.template put2<false>(u0, u1, &p.tmC, tc.nb * TN + 128 + f0, out_row0);
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const uint32_t gw = i < 16 ? g0[i] : g1[i - 16];
@@ -446,7 +446,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
             const float a0 = bf16lo(gw), a1 = bf16hi(gw), b0 = bf16lo(uw), b1 = bf16hi(uw);
             w[i] = pack_bf16x2(__fdividef(a0, 1.0f + __expf(-a0)) * b0, __fdividef(a1, 1.0f + __expf(-a1)) * b1);
           }
-          st.put<false>(w, &p.tmC2, tc.nb * (TN / 2) + f0, out_row0);
+          st.template put<false>(w, &p.tmC2, tc.nb * (TN / 2) + f0, out_row0);
         } else if constexpr (kEpi == EPI_DSWIGLU || kEpi == EPI_DSWIGLU_GATED) {
           // dAct columns of 64-column segment hh = features [fo, +64) of interleave block blk:
           // gate|up 256 columns of H / dH.  H (gate|up) comes in through TMA into the warp's two
@@ -549,15 +549,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
           release();
           const int32_t c0 = tc.nb * TN + ch2 * 128;
           if (accumulate) {
-            st.put<true>(r0, &p.tmC, c0, out_row0);
-            st.put<true>(r1, &p.tmC, c0 + 32, out_row0);
-            st.put<true>(r2, &p.tmC, c0 + 64, out_row0);
-            st.put<true>(r3, &p.tmC, c0 + 96, out_row0);
+            st.template put<true>(r0, &p.tmC, c0, out_row0);
+            st.template put<true>(r1, &p.tmC, c0 + 32, out_row0);
+            st.template put<true>(r2, &p.tmC, c0 + 64, out_row0);
+            st.template put<true>(r3, &p.tmC, c0 + 96, out_row0);
           } else {
-            st.put<false>(r0, &p.tmC, c0, out_row0);
-            st.put<false>(r1, &p.tmC, c0 + 32, out_row0);
-            st.put<false>(r2, &p.tmC, c0 + 64, out_row0);
-            st.put<false>(r3, &p.tmC, c0 + 96, out_row0);
+            st.template put<false>(r0, &p.tmC, c0, out_row0);
+            st.template put<false>(r1, &p.tmC, c0 + 32, out_row0);
+            st.template put<false>(r2, &p.tmC, c0 + 64, out_row0);
+            st.template put<false>(r3, &p.tmC, c0 + 96, out_row0);
           }
         }
       }
