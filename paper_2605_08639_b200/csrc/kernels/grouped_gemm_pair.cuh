@@ -28,6 +28,9 @@ struct PairTile {
   static constexpr int kBoxBytes = 32 * 128;  // one 32-row x 128-byte TMA box
 };
 
+#ifndef MB_PAIR_HEAVY_EPI_WARPS
+#define MB_PAIR_HEAVY_EPI_WARPS 8   // 4 (two column passes, 5 operand stages): dAct-gated 918 -> 845 TF
+#endif
 #ifndef MB_PAIR_LIGHT_EPI_WARPS
 #define MB_PAIR_LIGHT_EPI_WARPS 8   // 4 (6 stages) measured equal alone, 3-25% slower beside the comm kernels
 #endif
@@ -38,10 +41,10 @@ struct PairTile {
 template <int kEpi>
 struct PairCfg : PairTile {
   static constexpr bool kHeavy = kEpi == EPI_DSWIGLU || kEpi == EPI_DSWIGLU_GATED;
-  static constexpr int kEpiWarps = kHeavy ? 8 : MB_PAIR_LIGHT_EPI_WARPS;
+  static constexpr int kEpiWarps = kHeavy ? MB_PAIR_HEAVY_EPI_WARPS : MB_PAIR_LIGHT_EPI_WARPS;
   static constexpr int kThreads = 64 + 32 * kEpiWarps;
   static constexpr int kBoxesPerWarp = kHeavy ? 2 : 1;
-  static constexpr int kStages = kHeavy ? 4 : (kEpiWarps == 4 ? 6 : 5);
+  static constexpr int kStages = kHeavy ? (kEpiWarps == 4 ? 5 : 4) : (kEpiWarps == 4 ? 6 : 5);
   static constexpr int kABytes = 128 * BK * 2;  // this CTA's 128 rows of A
   static constexpr int kBBytes = 128 * BK * 2;  // this CTA's 128 columns of B
   static constexpr int kStageBytes = kABytes + kBBytes;
