@@ -10,6 +10,7 @@ files from the same trace.
 Run in the build container (needs /root/reference):
     PYTHONDONTWRITEBYTECODE=1 python oracle/gen_golden_io.py
     PYTHONDONTWRITEBYTECODE=1 python oracle/gen_golden_io.py --acceptance   (criteria 6/7 study, ~5 min)
+    PYTHONDONTWRITEBYTECODE=1 python oracle/gen_golden_io.py --qwen3        (production-shape trace + plans)
 """
 
 import json
@@ -60,7 +61,7 @@ def main():
     print(f"wrote {OUT}")
 
 
-if __name__ == "__main__" and "--acceptance" not in sys.argv:
+if __name__ == "__main__" and "--acceptance" not in sys.argv and "--qwen3" not in sys.argv:
     main()
 
 
@@ -104,3 +105,29 @@ def acceptance_study():
 
 if __name__ == "__main__" and "--acceptance" in sys.argv:
     acceptance_study()
+
+
+def qwen3():
+    """A Qwen3-30B-A3B-shaped trace (E=128, k=8, h=2048, h'=768; one group of 4 GPUs, 8
+    micro-batches of 8192 tokens per GPU, domain-focused skew) written by the reference's `gen`
+    with B200-like cost-model units, and the plan files its `solve` writes for it.  The GPU bench
+    replays both through the kernels (bench.py --trace ... --plans ...)."""
+    sys.path.insert(0, REF)
+    from moebalance import cli  # noqa: E402
+    out = OUT / "qwen3_ep4"
+    if out.exists():
+        shutil.rmtree(out)
+    rc = cli.main(["gen", "--out", str(out / "trace"), "--nodes", "1", "--gpus-per-node", "4", "--experts", "128",
+                   "--layers", "1", "--micro-batches", "8", "--top-k", "8", "--tokens-per-gpu", "8192",
+                   "--domains", "4", "--alpha", "0.3", "--focus", "0.5", "--seed", "7", "--hidden", "2048",
+                   "--intermediate", "768", "--flops", "1.0e15", "--bw-nvlink", "6.5e11", "--bw-rdma", "6.5e11",
+                   "--bytes-per-token", "4096"])
+    assert rc == 0
+    rc = cli.main(["solve", "--trace", str(out / "trace"), "--out", str(out / "plans"), "--seeds", "8",
+                   "--replica-slots", "2", "--threads", "8"])
+    assert rc == 0
+    print(f"wrote {out}")
+
+
+if __name__ == "__main__" and "--qwen3" in sys.argv:
+    qwen3()
