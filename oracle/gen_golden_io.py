@@ -107,6 +107,12 @@ if __name__ == "__main__" and "--acceptance" in sys.argv:
     acceptance_study()
 
 
+QWEN3_CASES = {  # name: (nodes, gpus per node) -- EP=4 one group; EP=8 two groups of 4 (north-star config)
+    "qwen3_ep4": (1, 4),
+    "qwen3_ep8": (2, 4),
+}
+
+
 def qwen3():
     """A Qwen3-30B-A3B-shaped trace (E=128, k=8, h=2048, h'=768; one group of 4 GPUs, 8
     micro-batches of 8192 tokens per GPU, domain-focused skew) written by the reference's `gen`
@@ -114,19 +120,20 @@ def qwen3():
     replays both through the kernels (bench.py --trace ... --plans ...)."""
     sys.path.insert(0, REF)
     from moebalance import cli  # noqa: E402
-    out = OUT / "qwen3_ep4"
-    if out.exists():
-        shutil.rmtree(out)
-    rc = cli.main(["gen", "--out", str(out / "trace"), "--nodes", "1", "--gpus-per-node", "4", "--experts", "128",
-                   "--layers", "1", "--micro-batches", "8", "--top-k", "8", "--tokens-per-gpu", "8192",
-                   "--domains", "4", "--alpha", "0.3", "--focus", "0.5", "--seed", "7", "--hidden", "2048",
-                   "--intermediate", "768", "--flops", "1.0e15", "--bw-nvlink", "6.5e11", "--bw-rdma", "6.5e11",
-                   "--bytes-per-token", "4096"])
-    assert rc == 0
-    rc = cli.main(["solve", "--trace", str(out / "trace"), "--out", str(out / "plans"), "--seeds", "8",
-                   "--replica-slots", "2", "--threads", "8"])
-    assert rc == 0
-    print(f"wrote {out}")
+    for name, (nodes, gpn) in QWEN3_CASES.items():
+        out = OUT / name
+        if out.exists():
+            shutil.rmtree(out)
+        rc = cli.main(["gen", "--out", str(out / "trace"), "--nodes", str(nodes), "--gpus-per-node", str(gpn),
+                       "--experts", "128", "--layers", "1", "--micro-batches", "8", "--top-k", "8",
+                       "--tokens-per-gpu", "8192", "--domains", "4", "--alpha", "0.3", "--focus", "0.5", "--seed", "7",
+                       "--hidden", "2048", "--intermediate", "768", "--flops", "1.0e15", "--bw-nvlink", "6.5e11",
+                       "--bw-rdma", "6.5e11", "--bytes-per-token", "4096"])
+        assert rc == 0
+        rc = cli.main(["solve", "--trace", str(out / "trace"), "--out", str(out / "plans"), "--seeds", "8",
+                       "--replica-slots", "2", "--threads", "8"])
+        assert rc == 0
+        print(f"wrote {out}")
 
 
 if __name__ == "__main__" and "--qwen3" in sys.argv:
