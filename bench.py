@@ -146,6 +146,11 @@ def cpu_reference_sample(cfg_name: str, tokens: int, world: int, zipf: float, bu
     return tps, f"{done_tokens} tokens of {cfg_name} (1 GPU's share), fp32 torch CPU fwd+bwd + bincount, {elapsed:.1f}s"
 
 
+def hot_shift(args, cfg):
+    """Experts the hot set rotates by per micro-batch (config default unless --hot-shift)."""
+    return cfg["shift"] if args.hot_shift is None else args.hot_shift
+
+
 def synthetic_config(args, world):
     """The `config` object of a synthetic-routing run (both arms print the same one)."""
     from paper_2605_08639_b200.workload import SHAPES
@@ -155,7 +160,7 @@ def synthetic_config(args, world):
             "experts": shape.num_experts, "top_k": shape.top_k, "hidden": shape.hidden, "ffn": shape.ffn,
             "tokens_per_gpu": args.tokens, "micro_batches": args.micro_batches,
             "global_tokens_per_step": world * args.tokens * args.micro_batches, "policy": args.headline,
-            "zipf_s": args.zipf, "hot_shift": cfg["shift"], "ep": world,
+            "zipf_s": args.zipf, "hot_shift": hot_shift(args, cfg), "ep": world,
             "gpu_group": min(world, args.group or cfg["group"]),
             "replica_slots": cfg["slots"] if args.slots is None else args.slots, "sa_chains": args.sa_chains,
             "reorder_planner": "device" if args.device_planner else "host",
@@ -360,7 +365,7 @@ def run_ours(args, comm):
                 idx[m, :len(i_m)], gts[m, :len(g_m)] = i_m, g_m
             r = Routing(idx=idx, gates=gts, mats=None)
         else:
-            r = make_routing(shape, T, MB, world, rank, zipf_s=args.zipf, shift=cfg["shift"], balanced=balanced,
+            r = make_routing(shape, T, MB, world, rank, zipf_s=args.zipf, shift=hot_shift(args, cfg), balanced=balanced,
                              all_ranks=False)
         counts, _ = expert_histogram(torch.from_numpy(r.idx).cuda(), shape.num_experts)
         r.mats = gather_routing(comm, counts.cpu().numpy().astype(np.int64))
@@ -456,6 +461,8 @@ def main():
     ap.add_argument("--tokens", type=int, default=8192)
     ap.add_argument("--micro-batches", type=int, default=8)
     ap.add_argument("--zipf", type=float, default=1.0)
+    ap.add_argument("--hot-shift", type=int, default=None,
+                    help="experts the hot set rotates by per micro-batch (default: the config's)")
     ap.add_argument("--slots", type=int, default=None)
     ap.add_argument("--group", type=int, default=0)
     ap.add_argument("--sa-chains", type=int, default=8)
