@@ -46,8 +46,8 @@ PAD = 128       # receive-slot row padding = GEMM M tile
 _SKIP_ROWS = os.environ.get("MB_PROFILE_SKIP_ROWS", "0") == "1"
 # SMs left to the comm stream while the persistent GEMM runs (measured on B200, qwen3 shape:
 # N=4 step 24.1 ms with all 148 SMs in the GEMM, 19.7 ms with 28 left free)
-COMM_SMS = {1: 20}
-COMM_SMS_MULTI = 32
+COMM_SMS = {1: 20, 2: 28, 4: 28}   # N=4 A/B: 28 SMs 18.41-18.60 ms vs 32 SMs 18.75-18.85
+COMM_SMS_MULTI = 32                # N >= 8 (most NVLink rows per GPU) keeps the wider split
 # Experts with a wide FFN do much more GEMM work per moved row (bytes / FLOP of a step = 4 / (9 h')):
 # at h' >= 4096 the TMA movers keep up on 8 SMs (Mixtral-8x7B at N=4: 79.3-79.8 -> 71.8-74.0 ms per
 # step with 140 GEMM SMs); Qwen3-235B (h' = 1536) is comm-bound on 16 (68.7-70.0 -> 73.0-73.2 ms).
@@ -264,10 +264,15 @@ def deinterleave_w1(w1: torch.Tensor) -> tuple:
 
 
 def default_comm_sms(world: int, shape: "LayerShape") -> int:
-    """SMs left to the comm stream's row movers while the persistent GEMM runs."""
-    if world in COMM_SMS:
-        return COMM_SMS[world]
-    return COMM_SMS_WIDE_FFN if shape.ffn >= WIDE_FFN else COMM_SMS_MULTI
+    """SMs left to the comm stream's row movers while the persistent GEMM runs (env
+    MB_COMM_SMS overrides, for A/B runs)."""
+    if os.environ.get("MB_COMM_SMS"):
+        return int(os.environ["MB_COMM_SMS"])
+    if world == 1:
+        return COMM_SMS[1]
+    if shape.ffn >= WIDE_FFN:
+        return COMM_SMS_WIDE_FFN
+    return COMM_SMS.get(world, COMM_SMS_MULTI)
 
 
 def schedule(mb: int):

@@ -75,11 +75,12 @@ def test_token_parts_cover_every_token_once(T, parts):
 
 
 def test_comm_sm_defaults():
-    """Row movers: 20 SMs at N=1 (register engine), 32 at N>1, 8 for wide-FFN experts."""
+    """Row movers: 20 SMs at N=1 (register engine), 28 at N=2/4, 32 at N>=8, 8 for wide-FFN experts."""
     from paper_2605_08639_b200 import moe_layer as ml
     from paper_2605_08639_b200.workload import SHAPES
     assert ml.default_comm_sms(1, SHAPES["qwen3-30b-a3b"]["shape"]) == 20
     assert ml.default_comm_sms(8, SHAPES["qwen3-30b-a3b"]["shape"]) == 32
-    assert ml.default_comm_sms(4, SHAPES["qwen3-235b-a22b"]["shape"]) == 32
+    assert ml.default_comm_sms(4, SHAPES["qwen3-30b-a3b"]["shape"]) == 28
+    assert ml.default_comm_sms(4, SHAPES["qwen3-235b-a22b"]["shape"]) == 28
     assert ml.default_comm_sms(4, SHAPES["mixtral-8x7b"]["shape"]) == 8
     assert ml.ROW_MOVERS[1] == "regs" and ml.ROW_MOVERS_MULTI == "tma"
