@@ -55,7 +55,8 @@ COMM_SMS_WIDE_FFN = 8
 WIDE_FFN = 4096
 # Row-mover engine per world size: "regs" = register-copy kernels (co-resident with the GEMM's
 # CTAs on every SM), "tma" = cp.async.bulk kernels, one block on each of the COMM_SMS SMs the
-# GEMM leaves free.  Measured (profiles/r01_comm_engine.txt): at N=4 tma/32 SMs 18.85-19.04 ms
+# GEMM leaves free (bulk-copy scatter, register combine with a shared-memory reservation).
+# Measured (profiles/r01_comm_engine.txt): at N=4 confined/32 SMs 18.85-19.04 ms
 # vs regs 19.2-19.26 per step; at N=1 (HBM-local moves) regs is faster (18.8-19.3 vs >= 20.1).
 ROW_MOVERS = {1: "regs"}
 ROW_MOVERS_MULTI = "tma"
