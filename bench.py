@@ -116,34 +116,39 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- CPU reference arm
 
-def cpu_reference_sample(cfg_name: str, tokens: int, world: int, zipf: float, budget_s: float, threads: int):
-    """The CPU path on a bounded sample (oracle port): np.bincount histogram + the fp32 layer
-    fwd+bwd (SwiGLU experts, gate-weighted combine) on a token sample, all host threads.  The
-    reference's planners are not in this arm (they cannot travel to the GPU box); their cost is
-    measured beside the native planners in profiles/r01_planner_timing.json.
-    Returns (tokens/s, sample description)."""
-    import torch
-    from oracle import moe_ref
-    from paper_2605_08639_b200.workload import SHAPES, make_activations, make_routing, make_weights
-    torch.set_num_threads(threads)
-    cfg = SHAPES[cfg_name]
+def cpu_reference_step(args, world, threads: int, reps: int = 1) -> dict:
+    """One step of the CPU reference path on the host cores (oracle/ref_arm.py): the reference's
+    own planners (moebalance from oracle/_ref: build_policy_bundle("relibra") over the step's
+    routing, threads=1 and threads=nproc) plus the fp32 port of the layer fwd+bwd on a fixed
+    token sample, combined as tokens/s of the whole step (every GPU's tokens on this host)."""
+    from oracle import ref_arm
+    from paper_2605_08639_b200.workload import SHAPES, make_routing
+    cfg = SHAPES[args.config]
     shape = cfg["shape"]
-    n = 256
-    wg, wu, wd = make_weights(shape)
-    done_tokens, elapsed = 0, 0.0
-    while elapsed < budget_s:
-        r = make_routing(shape, n, 1, 1, 0, zipf_s=zipf, shift=cfg["shift"])
-        x, dout = make_activations(shape, n, 1, 0)
-        t0 = time.perf_counter()
-        moe_ref.histogram(r.idx[0], shape.num_experts)
-        moe_ref.moe_layer_fp32(x[0], torch.from_numpy(r.idx[0]), torch.from_numpy(r.gates[0]), wg, wu, wd, dout[0])
-        dt = time.perf_counter() - t0
-        elapsed += dt
-        done_tokens += n
-        if dt < budget_s / 8:
-            n *= 2
-    tps = done_tokens / elapsed
-    return tps, f"{done_tokens} tokens of {cfg_name} (1 GPU's share), fp32 torch CPU fwd+bwd + bincount, {elapsed:.1f}s"
+    slots = cfg["slots"] if args.slots is None else args.slots
+    group = min(world, args.group or cfg["group"])
+    tokens_step = world * args.tokens * args.micro_batches
+    layer_tps = ref_arm.port_layer_tokens_per_s(args.config, args.zipf, threads, reps=reps)
+    out = {"layer_port_tokens_per_s": layer_tps, "layer_sample_tokens": 2048}
+    mb = ref_arm.load_reference()
+    if mb is not None:
+        r = make_routing(shape, args.tokens, args.micro_batches, world, 0, zipf_s=args.zipf, shift=hot_shift(args, cfg))
+        out["planner_s_threads1"] = ref_arm.reference_planner_seconds(mb, r.mats, shape, world, group, args.sa_chains,
+                                                                      slots, 1, reps=reps)
+        out["planner_s_threadsN"] = ref_arm.reference_planner_seconds(mb, r.mats, shape, world, group,
+                                                                      args.sa_chains, slots, threads, reps=reps)
+        out["planner"] = "moebalance 0.1.0 (oracle/_ref) sim.build_policy_bundle('relibra')"
+        planner_s = min(out["planner_s_threads1"], out["planner_s_threadsN"])
+    else:
+        out["planner"] = "unavailable (oracle/_ref not built: run oracle/build_ref.sh)"
+        planner_s = 0.0
+    out["step_s"] = planner_s + tokens_step / layer_tps
+    out["value"] = tokens_step / out["step_s"]
+    out["kind"] = "reference" if mb is not None else "port"
+    out["sample"] = (f"per step: the reference's planners on the step's routing ({args.micro_batches} micro-batches x "
+                     f"{world} GPUs, {args.sa_chains} SA chains) + the fp32 layer port at the rate of a fixed "
+                     f"2048-token sample, scaled to the step's {tokens_step} tokens")
+    return out
 
 
 def hot_shift(args, cfg):
@@ -164,51 +169,102 @@ def synthetic_config(args, world):
             "gpu_group": min(world, args.group or cfg["group"]),
             "replica_slots": cfg["slots"] if args.slots is None else args.slots, "sa_chains": args.sa_chains,
             "reorder_planner": "device" if args.device_planner else "host",
-            **data_plane_config(world, shape),
+            **data_plane_config(world, shape, args),
             "l2": "inputs larger than L2 (per-step working set >> 126 MB)"}
 
 
-def data_plane_config(world, shape):
-    """Row-mover engine and SMs left to the comm stream (MoEDataPlane defaults / env overrides)."""
+def data_plane_config(world, shape, args=None):
+    """Row-mover engine, SMs left to the comm stream, weight-gradient mode and replica weight
+    sets (MoEDataPlane defaults / env overrides)."""
     from paper_2605_08639_b200 import moe_layer as ml
     movers = os.environ.get("MB_ROW_MOVERS") or ml.ROW_MOVERS.get(world, ml.ROW_MOVERS_MULTI)
-    return {"row_movers": movers, "comm_sms": ml.default_comm_sms(world, shape)}
+    out = {"row_movers": movers, "comm_sms": ml.default_comm_sms(world, shape)}
+    if args is not None:
+        out["wgrad_mode"] = args.wgrad_mode
+        out["replica_sets"] = args.replica_sets or int(os.environ.get("MB_REPLICA_SETS", ml.REPLICA_SETS))
+    return out
 
 
 def run_reference(args, rank, world):
-    import torch
+    """--impl reference: the reference's own CPU implementation of the path (oracle/_ref
+    planners + the fp32 layer port) on this host's cores, rank 0 only."""
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    vals = []
+    steps = []
     for i in range(args.warmup + args.steps):
-        tps, sample = cpu_reference_sample(args.config, args.tokens, world, args.zipf,
-                                           budget_s=2.0 if i < args.warmup else 4.0, threads=threads)
+        r = cpu_reference_step(args, world, threads)
         if i >= args.warmup:
-            vals.append(tps)
-    # whole-job throughput: every GPU's share is independent CPU work on the same host
-    value = float(np.mean(vals))
+            steps.append(r)
+    value = statistics.median(r["value"] for r in steps)
+    last = steps[-1]
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.median(r["step_s"] for r in steps) * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": synthetic_config(args, world),
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": last["kind"],
+                             "sample": last["sample"], "planner": last["planner"],
+                             "planner_s_threads1": statistics.median(r.get("planner_s_threads1", 0.0) for r in steps),
+                             "planner_s_threadsN": statistics.median(r.get("planner_s_threadsN", 0.0) for r in steps),
+                             "layer_port_tokens_per_s": statistics.median(r["layer_port_tokens_per_s"] for r in steps),
+                             "spread": (max(r["value"] for r in steps) - min(r["value"] for r in steps)) / value},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------------------- B200 arm
 
-def measure_policy(args, comm, policy, shape, cfg, routing, topo, model, cfgs, want_detail, bundle=None):
+def _device_inputs(shape, T, MB, rank, routing):
     import torch
-    from paper_2605_08639_b200.comm import local_device
-    from paper_2605_08639_b200.moe_layer import MoEDataPlane, build_step_plan, plan_digest
-    from paper_2605_08639_b200.workload import make_activations, make_weights_for
-    rank, world = comm.rank, comm.world
-    T, MB = args.tokens, args.micro_batches
+    from paper_2605_08639_b200.workload import make_activations
+    xh, douth = make_activations(shape, T, MB, rank)
+    dev = {"x": xh.cuda(), "dout": douth.cuda(), "idx": torch.from_numpy(routing.idx).cuda(),
+           "gates": torch.from_numpy(routing.gates).cuda()}
+    dev["out"] = torch.empty_like(dev["x"])
+    dev["dx"] = torch.empty_like(dev["x"])
+    dev["dgate"] = torch.empty(MB, T, shape.top_k, dtype=torch.float32, device="cuda")
+    return dev
+
+
+def _make_plane(comm, shape, T, MB, plan, **kw):
+    from paper_2605_08639_b200.moe_layer import MoEDataPlane
+    from paper_2605_08639_b200.workload import make_weights_for
+    dp = MoEDataPlane(comm, shape, T, MB, plan, **kw)
+    experts = np.flatnonzero(plan.home == comm.rank)
+    wg, wu, wd = make_weights_for(shape, experts)
+    dp.set_weights(wg, wu, wd)
+    del wg, wu, wd
+    dp.zero_grads()
+    return dp
+
+
+def _step(dp, dev):
+    # one training step of the layer: optimizer.zero_grad() semantics (lazy: the first gradient
+    # contribution stores instead of accumulating), then fwd + bwd over every micro-batch
+    dp.zero_grads()
+    dp.step(dev["x"], dev["idx"], dev["gates"], dev["dout"], dev["out"], dev["dx"], dev["dgate"])
+
+
+def _timed_steps(comm, fn, steps):
+    """Device time of `steps` calls of fn (CUDA events on the current stream, barrier + sync on
+    both sides), max over ranks, per step."""
+    import torch
+    torch.cuda.synchronize()
+    comm.host_barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    comm.host_barrier()
+    return comm.max_over_ranks(s.elapsed_time(e) / steps)
+
+
+def _plan(args, comm, policy, shape, routing, topo, model, cfgs, bundle=None):
+    from paper_2605_08639_b200.moe_layer import build_step_plan, plan_digest, step_plan_from_bundle
     t0 = time.perf_counter()
     if bundle is not None:  # plan files (planio.solve / the reference's `solve`)
-        from paper_2605_08639_b200.moe_layer import step_plan_from_bundle
         plan = step_plan_from_bundle(policy, bundle, routing.mats, shape, layer=args.trace_layer)
     else:
         plan = build_step_plan(policy, routing.mats, topo, model, topo.profile, cfgs, shape)
@@ -216,94 +272,191 @@ def measure_policy(args, comm, policy, shape, cfg, routing, topo, model, cfgs, w
     digests = comm.all_gather_object(plan_digest(plan))
     if len(set(digests)) != 1:
         raise RuntimeError(f"ranks disagree on the step plan: {digests}")
-    dp = MoEDataPlane(comm, shape, T, MB, plan)
-    experts = np.flatnonzero(plan.home == rank)
-    wg, wu, wd = make_weights_for(shape, experts)
-    dp.set_weights(wg, wu, wd)
-    del wg, wu, wd
-    dp.zero_grads()
-    xh, douth = make_activations(shape, T, MB, rank)
-    dev = {"x": xh.cuda(), "dout": douth.cuda(), "idx": torch.from_numpy(routing.idx).cuda(),
-           "gates": torch.from_numpy(routing.gates).cuda()}
-    dev["out"] = torch.empty_like(dev["x"])
-    dev["dx"] = torch.empty_like(dev["x"])
-    dev["dgate"] = torch.empty(MB, T, shape.top_k, dtype=torch.float32, device="cuda")
+    return plan, plan_ms
 
-    def step():
-        # one training step of the layer: optimizer.zero_grad() semantics (lazy: the weight-gradient
-        # GEMMs store instead of accumulating), then fwd + bwd over every micro-batch
-        dp.zero_grads()
-        dp.step(dev["x"], dev["idx"], dev["gates"], dev["dout"], dev["out"], dev["dx"], dev["dgate"])
 
+def measure_detail(args, comm, dp, dev, plan, topo, model):
+    """The headline policy's detailed run: K timed steps with per-launch CUDA events (GEMM kinds,
+    comm phases), clocks sampled during the timed region, launch count, then e2e through the
+    host-buffer API."""
+    import torch
+    from paper_2605_08639_b200.comm import local_device
+    T, MB = args.tokens, args.micro_batches
     for _ in range(args.warmup):
-        step()
+        _step(dp, dev)
     torch.cuda.synchronize()
     comm.host_barrier()
-    sampler = ClockSampler(local_device()) if want_detail else None
-    if sampler:
-        sampler.start()
-        time.sleep(0.15)
-    dp.timing = want_detail
+    sampler = ClockSampler(local_device())
+    sampler.start()
+    time.sleep(0.15)
+    dp.timing = True
     dp.gemm_events = []
     launches0 = dp.launches
-    torch.cuda.synchronize()
-    comm.host_barrier()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for _ in range(args.steps):
-        step()
-    e.record()
-    torch.cuda.synchronize()
-    comm.host_barrier()
-    clocks = sampler.stop() if sampler else None
-    ms = s.elapsed_time(e) / args.steps
+    ms = _timed_steps(comm, lambda: _step(dp, dev), args.steps)
+    clocks = sampler.stop()
     launches = (dp.launches - launches0) // args.steps
     dp.timing = False
-    ms_max = comm.max_over_ranks(ms)
-    res = {"ms": ms_max, "plan_ms": plan_ms, "skew": plan.skew(), "launches": launches,
-           "predicted_ms": plan.predicted_ms(topo, model, topo.profile),
-           "rows": [dp.real_rows(m) for m in range(MB)], "rows_cap": plan.rows_cap}
-    if want_detail:
-        gev = [ev for ev in dp.gemm_events if not ev[3].startswith("comm_")]
-        cev = [ev for ev in dp.gemm_events if ev[3].startswith("comm_")]
-        gemm_ms = sum(a.elapsed_time(b) for a, b, _, _ in gev) / args.steps
-        gemm_flop = sum(f for _, _, f, _ in gev) / args.steps
-        kinds = {}
-        for a, b, f, kd in dp.gemm_events:
-            ms_f = kinds.setdefault(kd, [0.0, 0.0])
-            ms_f[0] += a.elapsed_time(b) / args.steps
-            ms_f[1] += f / args.steps
-        res["gemm_kinds"] = {kd: {"ms": round(v[0], 4), "tflops": round(v[1] / v[0] / 1e9, 1)}
-                             for kd, v in kinds.items() if not kd.startswith("comm_")}
-        # comm phases on the comm stream (barriers included): NVLink bytes this rank moves / time
-        res["comm_kinds"] = {kd[5:]: {"ms": round(v[0], 4), "nvlink_gb": round(v[1] / 1e9, 4),
-                                      "gb_per_s": round(v[1] / v[0] / 1e6, 1) if v[0] > 0 else 0.0}
-                             for kd, v in kinds.items() if kd.startswith("comm_")}
-        res.update(gemm_ms=gemm_ms, gemm_flop=gemm_flop, gemm_launches=len(gev) // args.steps,
-                   clocks=clocks)
-        # e2e through the host-buffer API (pinned host tensors, copies inside the timed region)
-        host = {k: v.cpu().pin_memory() for k, v in dev.items()}
-        for _ in range(2):
-            dp.zero_grads()
-            dp.step_host(host, dev)
-        comm.host_barrier()
-        t0 = time.perf_counter()
-        n_e2e = max(2, min(args.steps, 5))
-        for _ in range(n_e2e):
-            dp.zero_grads()
-            dp.step_host(host, dev)
-        comm.host_barrier()
-        e2e_ms = (time.perf_counter() - t0) * 1e3 / n_e2e
-        e2e_ms = comm.max_over_ranks(e2e_ms)
-        res["e2e_ms"] = e2e_ms
-        res["h2d"] = sum(host[k].numel() * host[k].element_size() for k in ("x", "idx", "gates", "dout"))
-        res["d2h"] = sum(host[k].numel() * host[k].element_size() for k in ("out", "dx", "dgate"))
-        del host
-    dp.close()
-    del dp, dev
-    gc.collect()
-    torch.cuda.empty_cache()
+    res = {"ms": ms, "launches": launches, "clocks": clocks, "rows": [dp.real_rows(m) for m in range(MB)],
+           "rows_cap": plan.rows_cap}
+    gev = [ev for ev in dp.gemm_events if not ev[3].startswith("comm_")]
+    res["gemm_ms"] = sum(a.elapsed_time(b) for a, b, _, _ in gev) / args.steps
+    res["gemm_flop"] = sum(f for _, _, f, _ in gev) / args.steps
+    kinds = {}
+    for a, b, f, kd in dp.gemm_events:
+        ms_f = kinds.setdefault(kd, [0.0, 0.0])
+        ms_f[0] += a.elapsed_time(b) / args.steps
+        ms_f[1] += f / args.steps
+    res["gemm_kinds"] = {kd: {"ms": round(v[0], 4), "tflops": round(v[1] / v[0] / 1e9, 1)}
+                         for kd, v in kinds.items() if not kd.startswith("comm_") and v[0] > 0}
+    # comm phases on the comm / copy streams (barriers included): NVLink bytes this rank moves / time
+    res["comm_kinds"] = {kd[5:]: {"ms": round(v[0], 4), "nvlink_gb": round(v[1] / 1e9, 4),
+                                  "gb_per_s": round(v[1] / v[0] / 1e6, 1) if v[0] > 0 else 0.0}
+                         for kd, v in kinds.items() if kd.startswith("comm_")}
+    res["gemm_launches"] = len(gev) // args.steps
+    # e2e through the host-buffer API (pinned host tensors, copies inside the timed region)
+    host = {k: v.cpu().pin_memory() for k, v in dev.items()}
+    for _ in range(2):
+        dp.zero_grads()
+        dp.step_host(host, dev)
+    comm.host_barrier()
+    t0 = time.perf_counter()
+    n_e2e = max(2, min(args.steps, 5))
+    for _ in range(n_e2e):
+        dp.zero_grads()
+        dp.step_host(host, dev)
+    comm.host_barrier()
+    res["e2e_ms"] = comm.max_over_ranks((time.perf_counter() - t0) * 1e3 / n_e2e)
+    res["h2d"] = sum(host[k].numel() * host[k].element_size() for k in ("x", "idx", "gates", "dout"))
+    res["d2h"] = sum(host[k].numel() * host[k].element_size() for k in ("out", "dx", "dgate"))
+    del host
     return res
+
+
+def check_step(args, comm, dp, dev, plan, shape):
+    """--check (test infrastructure, off by default, after every timed region): the last step's
+    outputs against the fp32 CPU restatement (oracle/moe_ref.py): out / dx / dgate of the first
+    and last micro-batch on every rank; at EP=1 also the gradients of the 8 hottest and 8 coldest
+    experts (the oracle needs every rank's tokens for the rest).  Returns {name: metrics}."""
+    import torch
+    from oracle import moe_ref
+    from paper_2605_08639_b200.moe_layer import deinterleave_w1
+    from paper_2605_08639_b200.workload import make_weights_for
+    E, MB = shape.num_experts, args.micro_batches
+    _step(dp, dev)
+    dp.check(sync=True)
+    wg, wu, wd = make_weights_for(shape, np.arange(E))
+    out = {}
+    for m in sorted({0, MB - 1}):
+        ref = moe_ref.moe_layer_fp32(dev["x"][m], dev["idx"][m], dev["gates"][m], wg, wu, wd, dev["dout"][m])
+        for key in ("out", "dx", "dgate"):
+            out[f"{key}_mb{m}"] = moe_ref.close(dev[key][m], ref[key])
+        del ref
+    if comm.world == 1:
+        load = plan.mats.sum(axis=(0, 1))
+        order = np.argsort(-load, kind="stable")
+        sel = torch.from_numpy(np.concatenate([order[:8], order[-8:]])).cuda()
+        gsum = None
+        for m in range(MB):
+            keep = torch.isin(dev["idx"][m], sel)
+            idx_m = torch.where(keep, dev["idx"][m], torch.full_like(dev["idx"][m], -1))
+            r = moe_ref.moe_layer_fp32(dev["x"][m], idx_m, dev["gates"][m], wg, wu, wd, dev["dout"][m])
+            g = (r["dWg"][sel], r["dWu"][sel], r["dWd"][sel])
+            gsum = g if gsum is None else tuple(a + b for a, b in zip(gsum, g))
+        gW1, gW2 = dp.grads()
+        g_gate, g_up = deinterleave_w1(gW1[sel])
+        for key, got, ref in (("dWg", g_gate, gsum[0]), ("dWu", g_up, gsum[1]), ("dWd", gW2[sel], gsum[2])):
+            out[key + "_16_experts"] = moe_ref.expert_grads_close(got, ref)
+    res = {k: {kk: (round(vv, 6) if isinstance(vv, float) else vv) for kk, vv in v.items()} for k, v in out.items()}
+    oks = comm.all_gather_object(all(v["ok"] for v in out.values()))
+    res["ok"] = bool(all(oks))
+    return res
+
+
+def measure_sequence(args, comm, shape, cfg, topo, model, cfgs, policies):
+    """Replay a sequence of batches whose hot set keeps shifting (each batch continues the
+    micro-batch rotation of the last one): every batch gets its own plan, and the ReLibra arm
+    migrates experts -- weights plus fp32 master weights and both Adam moments, the state an
+    optimizer step leaves, through MoEDataPlane.migrate -- at every batch boundary, inside the
+    timed region.  Returns per policy the tokens/s over the sequence
+    and the migration share."""
+    import torch
+    from paper_2605_08639_b200.kernels import expert_histogram
+    from paper_2605_08639_b200.moe_layer import gather_routing
+    from paper_2605_08639_b200.workload import make_routing
+    rank, world = comm.rank, comm.world
+    T, MB, NB = args.tokens, args.micro_batches, args.batches
+    pdim = 3 * shape.hidden * shape.ffn
+    state = {"master": ((pdim,), torch.float32), "adam_m": ((pdim,), torch.float32),
+             "adam_v": ((pdim,), torch.float32)}
+    routings = []
+    for b in range(NB):
+        r = make_routing(shape, T, MB, world, rank, zipf_s=args.zipf, shift=hot_shift(args, cfg), all_ranks=False,
+                         mb_offset=b * MB)
+        counts, _ = expert_histogram(torch.from_numpy(r.idx).cuda(), shape.num_experts)
+        r.mats = gather_routing(comm, counts.cpu().numpy().astype(np.int64))
+        routings.append(r)
+    out = {}
+    for pol in policies:
+        plans, plan_ms = [], []
+        for r in routings:
+            p, ms = _plan(args, comm, pol, shape, r, topo, model, cfgs)
+            plans.append(p)
+            plan_ms.append(ms)
+        dp = _make_plane(comm, shape, T, MB, plans[0], rows_cap=max(p.rows_cap for p in plans), expert_state=state)
+        tables = [dp.build_tables(p) for p in plans]
+        devs = [_device_inputs(shape, T, MB, rank, r) for r in routings]
+        moved = [0]
+
+        def run_sequence():
+            for b in range(NB):
+                if b:
+                    if pol == "static":
+                        dp.load_plan(tables[b])    # same placement, new counts: tables only
+                    else:
+                        info = dp.migrate(tables[b], grads=False)   # after the optimizer step
+                        moved[0] += info["bytes_in"]
+                _step(dp, devs[b])
+            # back to batch 0's placement for the next repetition (not timed)
+
+        def reset():
+            if dp.plan is not plans[0]:
+                dp.migrate(tables[0], grads=False) if pol != "static" else dp.load_plan(tables[0])
+
+        run_sequence()
+        reset()
+        torch.cuda.synchronize()
+        moved[0] = 0
+        total, mig = [], []
+        for _ in range(args.repeats):
+            ms = _timed_steps(comm, run_sequence, 1)
+            total.append(ms)
+            reset()
+        # migration alone (same moves, no steps) for its share of the sequence
+        if pol != "static":
+            def migrations_only():
+                for b in range(1, NB):
+                    dp.migrate(tables[b], grads=False)
+                dp.migrate(tables[0], grads=False)
+            mig_ms = _timed_steps(comm, migrations_only, 1) * (NB - 1) / NB
+        else:
+            mig_ms = 0.0
+        tokens = world * T * MB * NB
+        med = statistics.median(total)
+        out[pol] = {"tokens_per_s": tokens / (med / 1e3), "ms_per_batch": med / NB,
+                    "ms_min": min(total) / NB, "ms_max": max(total) / NB,
+                    "migration_ms_per_batch": round(mig_ms / max(1, NB - 1) if NB > 1 else 0.0, 4),
+                    "migration_gb_in_per_rank_per_batch": round(moved[0] / args.repeats / max(1, NB - 1) / 1e9, 4),
+                    "planner_ms_per_batch": round(statistics.mean(plan_ms), 2),
+                    "skew": round(float(np.mean([p.skew() for p in plans])), 4)}
+        dp.close()
+        del dp, devs, tables
+        gc.collect()
+        torch.cuda.empty_cache()
+    if "relibra" in out and "static" in out:
+        out["speedup_vs_static"] = round(out["static"]["ms_per_batch"] / out["relibra"]["ms_per_batch"], 4)
+    out["batches"] = NB
+    out["state_per_expert"] = "bf16 weights + fp32 master + Adam m, v (the state an optimizer step leaves)"
+    return out
 
 
 def run_ours(args, comm):
@@ -312,6 +465,7 @@ def run_ours(args, comm):
     from paper_2605_08639_b200.cluster import b200_box_topology, b200_profile
     from paper_2605_08639_b200.kernels import expert_histogram
     from paper_2605_08639_b200.moe_layer import gather_routing
+    from paper_2605_08639_b200.replication import replica_memory
     from paper_2605_08639_b200.workload import SHAPES, make_routing
     rank, world = comm.rank, comm.world
     cfg = SHAPES[args.config]
@@ -376,37 +530,77 @@ def run_ours(args, comm):
     skewed = routing_for(False)
     balanced = routing_for(True)
     policies = [p for p in args.policies.split(",") if p]
-    results = {}
-    failed = {}
-    policies = [args.headline] + [p for p in policies if p != args.headline]   # headline first
-    for pol in policies:
+    policies = [args.headline] + [p for p in policies if p != args.headline]
+    if "relibra_box" in policies and group == world:
+        policies.remove("relibra_box")   # one group already spans the box
+    dp_kw = {"wgrad_mode": args.wgrad_mode, "replica_sets": args.replica_sets}
+
+    def plan_of(pol):
         routing = balanced if pol == "balanced_oracle" else skewed
+        if pol == "relibra_box":  # ReLibra with the whole NVSwitch box as one replication group
+            box = b200_box_topology(world, world, b200_profile(shape.hidden))
+            return routing, _plan(args, comm, "relibra", shape, routing, box, model, cfgs)
+        return routing, _plan(args, comm, pol, shape, routing, topo, model, cfgs,
+                              bundle=bundle if pol == "relibra" else None)
+
+    # ---- headline: detailed run (per-launch events, clocks, e2e)
+    routing, (plan, plan_ms) = plan_of(args.headline)
+    dp = _make_plane(comm, shape, T, MB, plan, **dp_kw)
+    dev = _device_inputs(shape, T, MB, rank, routing)
+    head = measure_detail(args, comm, dp, dev, plan, topo, model)
+    head["memory"] = dp.memory_report()
+    check = check_step(args, comm, dp, dev, plan, shape) if args.check else None
+    dp.close()
+    del dp, dev
+    gc.collect()
+    torch.cuda.empty_cache()
+    # ---- every policy on the same routing, interleaved: repeat r runs the policies in rotated
+    # order (ABCD, BCDA, ...), each a fresh data plane with W warm-up and K timed steps
+    results, failed, plans = {}, {}, {}
+    for pol in policies:
         try:
-            if pol == "relibra_box":
-                # ReLibra with the whole NVSwitch box as one replication group (group = EP)
-                if group == world:
-                    continue
-                box = b200_box_topology(world, world, b200_profile(shape.hidden))
-                results[pol] = measure_policy(args, comm, "relibra", shape, cfg, routing, box, model, cfgs,
-                                              want_detail=False)
-                continue
-            results[pol] = measure_policy(args, comm, pol, shape, cfg, routing, topo, model, cfgs,
-                                          want_detail=(pol == args.headline),
-                                          bundle=bundle if pol == "relibra" else None)
+            plans[pol] = plan_of(pol)
         except Exception as err:  # a comparison policy must not cost the headline line
             if pol == args.headline:
                 raise
             failed[pol] = f"{type(err).__name__}: {err}"[:300]
-            torch.cuda.synchronize()
-    head = results[args.headline]
+    live = [p for p in policies if p in plans]
+    times = {p: [] for p in live}
+    for rep in range(args.repeats):
+        for i in range(len(live)):
+            pol = live[(i + rep) % len(live)]
+            routing, (plan_p, pms) = plans[pol]
+            try:
+                dpp = _make_plane(comm, shape, T, MB, plan_p, **dp_kw)
+                devp = _device_inputs(shape, T, MB, rank, routing)
+                for _ in range(args.warmup):
+                    _step(dpp, devp)
+                times[pol].append(_timed_steps(comm, lambda: _step(dpp, devp), args.steps))
+                dpp.close()
+                del dpp, devp
+            except Exception as err:
+                if pol == args.headline:
+                    raise
+                failed[pol] = f"{type(err).__name__}: {err}"[:300]
+            gc.collect()
+            torch.cuda.empty_cache()
+    for pol in live:
+        if not times[pol]:
+            continue
+        plan_p, pms = plans[pol][1]
+        med = statistics.median(times[pol])
+        results[pol] = {"ms": med, "ms_min": min(times[pol]), "ms_max": max(times[pol]), "runs": len(times[pol]),
+                        "plan_ms": pms, "skew": plan_p.skew(), "predicted_ms": plan_p.predicted_ms(topo, model,
+                                                                                                     topo.profile)}
     tokens_step = world * T * MB
-    value = tokens_step / (head["ms"] / 1e3)
+    ms_head = results[args.headline]["ms"]
+    value = tokens_step / (ms_head / 1e3)
     peaks, peak_src = load_peaks()
     peak_tf = float(peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"]))
     gemm_tflops = head["gemm_flop"] / (head["gemm_ms"] / 1e3) / 1e12
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": head["ms"], "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_head, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": synthetic_config(args, world) if trace is None else {
             "workload": (f"trace {trace.trace_id()} layer {args.trace_layer} MoE layer fwd+bwd, EP={world}"
@@ -414,41 +608,61 @@ def run_ours(args, comm):
             "experts": shape.num_experts, "top_k": shape.top_k, "hidden": shape.hidden, "ffn": shape.ffn,
             "tokens_per_gpu": T, "micro_batches": MB, "global_tokens_per_step": tokens_step,
             "policy": args.headline, "ep": world, "gpu_group": group, "replica_slots": slots,
-            "sa_chains": args.sa_chains, **data_plane_config(world, shape),
+            "sa_chains": args.sa_chains, **data_plane_config(world, shape, args),
             "l2": "inputs larger than L2 (per-step working set >> 126 MB)"},
+        "timing": (f"value / ms_per_step = median of {args.repeats} interleaved runs of {args.steps} timed steps "
+                   f"(each after {args.warmup} warm-up steps; CUDA events, max over ranks); the headline's first "
+                   f"extra run ({head['ms']:.3f} ms/step) carries the per-launch events, clocks and e2e"),
         "roofline": {"kernel": "K4 tcgen05 grouped GEMM (all fwd/dgrad/wgrad launches of the step)",
                      "bound": "tensor", "achieved": round(gemm_tflops, 1), "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": round(gemm_tflops / peak_tf, 4),
                      "traffic": (None if trace is not None else
                                  k4_traffic_per_step(args.config, world, args.tokens, args.micro_batches)),
-                     "traffic_unit": "DRAM bytes per step over all K4 launches (ncu, profiles/"
-                                     "r01_launches_step2_summary.json)",
+                     "traffic_unit": f"DRAM bytes per step over all K4 launches (ncu, {os.path.relpath(K4_TRAFFIC, ROOT)})",
                      "peak_source": f"bf16_tflops_sustained, {peak_src}",
                      "flops_per_step": head["gemm_flop"], "gemm_ms_per_step": round(head["gemm_ms"], 4),
                      "gemm_share_of_step": round(head["gemm_ms"] / head["ms"], 4),
                      "per_kind": head["gemm_kinds"]},
         "comm": head["comm_kinds"],
         "e2e": {"value": tokens_step / (head["e2e_ms"] / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": head["h2d"],
-                "d2h_bytes_per_step": head["d2h"], "ms_per_step": head["e2e_ms"]},
+                "d2h_bytes_per_step": head["d2h"], "ms_per_step": head["e2e_ms"],
+                "note": ("host<->device copies of every micro-batch inside the timed region (pinned memory); "
+                         "at N>1 all ranks share the host's memory bandwidth")},
         "gpu_launches": head["launches"],
         "clocks": head["clocks"],
-        "balance": {p: {"tokens_per_s": tokens_step / (r["ms"] / 1e3), "ms_per_step": r["ms"], "skew": r["skew"],
+        "memory": dict(head["memory"], replica_memory_layer_shared=replica_memory(model, ReplicaConfig(slots),
+                                                                                  "layer-shared")),
+        "balance": {p: {"tokens_per_s": tokens_step / (r["ms"] / 1e3), "ms_per_step": r["ms"],
+                        "ms_min": r["ms_min"], "ms_max": r["ms_max"], "runs": r["runs"], "skew": r["skew"],
                         "planner_ms": r["plan_ms"], "model_predicted_ms": round(r["predicted_ms"], 4)}
                     for p, r in results.items()},
     }
     if failed:
         line["balance"]["failed"] = failed
     if "static" in results:
-        line["balance"]["speedup_vs_static"] = results["static"]["ms"] / head["ms"]
+        line["balance"]["speedup_vs_static"] = results["static"]["ms"] / ms_head
+        line["balance"]["model_predicted_speedup_vs_static"] = (results["static"]["predicted_ms"]
+                                                                / results[args.headline]["predicted_ms"])
     if "balanced_oracle" in results:
-        line["balance"]["frac_of_balanced"] = results["balanced_oracle"]["ms"] / head["ms"]
+        line["balance"]["frac_of_balanced"] = results["balanced_oracle"]["ms"] / ms_head
+        line["balance"]["model_predicted_frac_of_balanced"] = (results["balanced_oracle"]["predicted_ms"]
+                                                               / results[args.headline]["predicted_ms"])
+    if args.batches > 1 and trace is None:
+        seq = measure_sequence(args, comm, shape, cfg, topo, model, cfgs, ["relibra", "static"])
+        line["balance"]["shifting_batches"] = seq
+        line["balance"]["relibra_with_migration"] = seq["relibra"]["tokens_per_s"]
+    if check is not None:
+        line["check"] = check
     if rank == 0 and world == 1 and not args.no_cpu_baseline and trace is None:
-        tps, sample = cpu_reference_sample(args.config, T, world, args.zipf, budget_s=args.cpu_budget,
-                                           threads=os.cpu_count() or 1)
-        line["cpu_baseline"] = {"value": tps, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
-                                "sample": sample}
+        r = cpu_reference_step(args, world, os.cpu_count() or 1, reps=3)
+        line["cpu_baseline"] = {"value": r["value"], "unit": "tokens/s", "cores": os.cpu_count(), "kind": r["kind"],
+                                "sample": r["sample"], "planner": r["planner"],
+                                **{k: r[k] for k in ("planner_s_threads1", "planner_s_threadsN",
+                                                     "layer_port_tokens_per_s") if k in r}}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if check is not None and not check["ok"]:
+        raise SystemExit("--check: the timed configuration differs from the fp32 oracle")
 
 
 def main():
@@ -469,9 +683,16 @@ def main():
     ap.add_argument("--policies", default="relibra,static,eplb_like,balanced_oracle,relibra_box",
                     help="relibra_box = relibra with one replication group spanning all EP GPUs (run when EP > group)")
     ap.add_argument("--headline", default="relibra")
+    ap.add_argument("--repeats", type=int, default=3,
+                    help="interleaved repetitions of every policy (rotated order); value = the headline's median")
+    ap.add_argument("--batches", type=int, default=4,
+                    help="batches of the shifting-routing sequence (new plan + expert migration per batch); 1 = off")
+    ap.add_argument("--wgrad-mode", default="step", choices=["step", "micro_batch"])
+    ap.add_argument("--replica-sets", type=int, default=None)
+    ap.add_argument("--check", action="store_true",
+                    help="after the timed runs, compare the last step with the fp32 oracle (test infrastructure)")
     ap.add_argument("--device-planner", action="store_true",
                     help="run the reorder planner's annealing chains on the GPU (identical plans)")
-    ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--trace", default=None, help="replay a recorded routing trace directory (manifest.json + "
                     "routing.bin) instead of synthetic Zipf routing")
@@ -481,9 +702,27 @@ def main():
     args = ap.parse_args()
     if args.headline not in args.policies.split(","):
         args.policies = args.headline + "," + args.policies
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.warmup < 3 and args.impl == "ours":
+        print("bench: --warmup < 3 is below the timing rules; using 3", file=sys.stderr)
+        args.warmup = 3
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1:
+        # `python bench.py --gpus N`: launch N ranks (one process per GPU, NCCL) ourselves
+        import socket
+        sock = socket.socket()
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+        sock.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
+    world = int(env_world or "1")
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; launch one process per GPU")
     rank = int(os.environ.get("RANK", "0"))
-    os.environ["NCCL_DEBUG"] = "WARN"  # keep NCCL's version banner off stdout: one JSON line only
+    if os.environ.get("NCCL_DEBUG") and not os.environ.get("NCCL_DEBUG_FILE"):
+        # NCCL's log goes to stderr: stdout carries exactly one JSON line
+        os.environ["NCCL_DEBUG_FILE"] = "/dev/stderr"
     if args.impl == "reference":
         return run_reference(args, rank, world)
     import torch

@@ -20,6 +20,11 @@ extern "C" {
 const char* mb_last_error(void);
 int mb_version(void);
 
+/* Bits a kernel ORs into a caller-provided int32 error flag (host-visible pinned memory in the
+ * data plane, read without a device sync; the host raises on any nonzero value). */
+#define MB_ERR_ROUTING_MISMATCH 1  /* routing has more tokens for an expert than the plan's counts */
+#define MB_ERR_COUNTS_MISMATCH 2   /* K1 histogram differs from the counts the plan was built for */
+
 /* ---------------------------------------------------------------- K1 histogram
  * counts[b][e] = #{(t,i) : idx[b][t][i] == e}, for nb independent (micro-batch, layer)
  * batches of T tokens x k choices.  One launch for every batch (routing is replayed, so all
@@ -29,9 +34,10 @@ int mb_version(void);
 int mb_expert_histogram(const int32_t* idx, int64_t nb, int64_t tokens, int32_t topk, int32_t num_experts,
                         uint32_t* counts, uint32_t* chunk_counts, int32_t chunk_tokens, void* stream);
 
-/* SMs the persistent grouped GEMM may occupy (0 = all; env MB_GEMM_SMS overrides).  The SMs left
- * free run the dispatch / combine kernels of the comm stream while the GEMM runs (the
- * reference models comm and compute as separate resources, costmodel.py:205-213). */
+/* Process default of the SMs the persistent grouped GEMM may occupy (0 = all; env MB_GEMM_SMS
+ * overrides); a call's own gemm_sms > 0 wins.  The SMs left free run the dispatch / combine
+ * kernels of the comm stream while the GEMM runs (the reference models comm and compute as
+ * separate resources, costmodel.py:205-213). */
 int mb_set_gemm_sms(int sms);
 
 /* ---------------------------------------------------------------- K4 grouped GEMM
@@ -51,12 +57,15 @@ enum {
                                      C2 = gate*act, row_partial[row][N/64] = partial <dout.W2, act>
                                      whose sum is dgate = <dout, Y> (replaces the combine backward) */
 };
-/* mode | 0x100 forces the 1-CTA kernel (default: CTA-pair 256x256 tiles when the shape allows). */
+/* mode | 0x100 forces the 1-CTA kernel (default: CTA-pair 256x256 tiles when the shape allows).
+ * gemm_sms > 0: SMs this launch's persistent grid covers (each data plane passes its own split;
+ * <= 0 = the process default of mb_set_gemm_sms). */
 int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t a_cols, const void* B0, int64_t b0_rows,
                     const void* B1, int64_t b1_rows, int64_t b_cols, const void* groups, const void* segs,
                     int num_groups, int M,
                     int N, int K, void* C, int64_t ldc, int64_t c_slot_stride, void* C2, int64_t ldc2,
-                    const void* aux, int64_t ld_aux, const float* row_scale, float* row_partial, void* stream);
+                    const void* aux, int64_t ld_aux, const float* row_scale, float* row_partial, int32_t gemm_sms,
+                    void* stream);
 
 /* ---------------------------------------------------------------- K2 permutation
  * chunk_base[b][c][e] = exclusive prefix over chunks of chunk_counts (from mb_expert_histogram). */
@@ -66,11 +75,13 @@ int mb_chunk_scan(const uint32_t* chunk_counts, uint32_t* chunk_base, int64_t nb
  * of (t,i) among the source's entries of expert e split over its copies by the integer counts in
  * route_tab[E][maxc][4] {cum_end, dst_gpu, dst_row_base, 0} (round_split, replicate.py:501-525;
  * copy order ReplicaPlacement.copies, replicate.py:55-56).  gate values are stored at
- * dst_gate[dst_gpu][dst_row] (peer pointers) when both are non-NULL.
+ * dst_gate[dst_gpu][dst_row] (peer pointers) when both are non-NULL.  A choice whose rank is past
+ * the last copy's cum_end (routing != the planned counts) gets perm = {-1,-1} and ORs
+ * MB_ERR_ROUTING_MISMATCH into *error_flag (may be NULL): nothing is ever written past a slot.
  * Replaces: the dispatch leg of costmodel.flow_matrix (costmodel.py:91-108), which only counts. */
 int mb_permute_rank(const int32_t* idx, int64_t T, int32_t k, const float* gate, int32_t E, const uint32_t* chunk_base,
                     int32_t chunk_tokens, const int32_t* route_tab, const int32_t* ncopies, int32_t maxc,
-                    float* const* dst_gate, int32_t* perm, void* stream);
+                    float* const* dst_gate, int32_t* perm, int32_t* error_flag, void* stream);
 
 /* The same over nb consecutive micro-batches in one launch: idx / gate / perm advance by T*k
  * entries, chunk_base by chunks*E, route_tab by E*maxc*4, ncopies by E, and dst_gate holds
@@ -78,18 +89,25 @@ int mb_permute_rank(const int32_t* idx, int64_t T, int32_t k, const float* gate,
 int mb_permute_rank_nb(const int32_t* idx, int64_t T, int32_t k, const float* gate, int32_t E,
                        const uint32_t* chunk_base, int32_t chunk_tokens, const int32_t* route_tab,
                        const int32_t* ncopies, int32_t maxc, float* const* dst_gate, int32_t world, int32_t* perm,
-                       int32_t nb, void* stream);
+                       int32_t nb, int32_t* error_flag, void* stream);
+
+/* error_flag |= code when counts[i] != expected[i] for any i < n (the K1 histogram against the
+ * counts the step plan was built from, RoutingTrace.matrices row, routing.py:151-168). */
+int mb_check_counts(const uint32_t* counts, const int32_t* expected, int64_t n, int32_t* error_flag, int32_t code,
+                    void* stream);
 
 /* ---------------------------------------------------------------- K3 dispatch all-to-all
  * Row scatter: row t of x ([T,h] bf16) is stored at dst_rows[perm.gpu] + perm.row*h for every
  * choice i (device array of per-GPU base pointers, peers mapped over NVLink; 128-bit stores).
  * Replaces: the dispatch link loads of costmodel._accumulate_direction (costmodel.py:64-88, 148). */
 int mb_scatter_rows(const void* x, int64_t T, int32_t k, int32_t h, const int32_t* perm, void* const* dst_rows,
-                    void* stream);
+                    int32_t comm_blocks, void* stream);
 
 /* Row-mover engine for mb_scatter_rows / mb_combine_rows: blocks > 0 selects the TMA bulk-copy
  * kernels (cp.async.bulk rows through shared memory; one block per SM, ~190 KB of rows in flight,
- * never co-resident with a GEMM CTA) on that many blocks; 0 = the register-copy kernels. */
+ * never co-resident with a GEMM CTA) on that many blocks; 0 = the register-copy kernels.  This
+ * sets the process default; a call's own comm_blocks >= 0 wins (each data plane passes its own
+ * engine), -1 = use the default. */
 int mb_set_comm_blocks(int32_t blocks);
 
 /* ---------------------------------------------------------------- K6 combine
@@ -99,7 +117,7 @@ int mb_set_comm_blocks(int32_t blocks);
  * Replaces: the mirrored combine leg of compute_loads (costmodel.py:149-150). */
 int mb_combine_rows(const void* const* src_rows, const int32_t* perm, const float* gate, int64_t T, int32_t k,
                     int32_t h, void* out, const float* const* src_scalar, float* scalar_out, int32_t npart,
-                    void* stream);
+                    int32_t comm_blocks, void* stream);
 /* Expert-side combine backward (unfused reference variant of the gated dSwiGLU epilogue):
  * dY = gate*dout in place, dgate = <dout, Y>, pad rows zeroed. */
 int mb_combine_bwd_expert(void* dout_rows, const void* y_rows, const float* gate_rows, float* dgate_rows,
@@ -115,7 +133,13 @@ int mb_zero_pad_rows_nb(void* rows, int64_t rows_stride, const int32_t* slot_tab
  * dst[i] += sum_s srcs[s][i] (fp32, sources in list order): replica-gradient reduce into the owner,
  * sources read from peers (replica_memory replicate.py:528-534). */
 int mb_accumulate_f32(float* dst, const float* const* srcs, int32_t nsrc, int64_t n, void* stream);
-/* Copy-engine copy (replica weight push into a peer's layer-shared replica slot). */
+/* Batched form, one launch per micro-batch: tasks is a device array of
+ *   struct { float* dst; const float* src[MB_ACC_MAX_SRC]; int64_t n; int32_t nsrc; int32_t store; }
+ * (n a multiple of 4, max_n >= every n); store = 1 writes dst = sum(src) (the first contribution to a
+ * gradient of a freshly zeroed step), else dst += sum(src).  Sources are summed in list order. */
+#define MB_ACC_MAX_SRC 8
+int mb_accumulate_f32_tasks(const void* tasks, int32_t ntasks, int64_t max_n, void* stream);
+/* Copy-engine copy (replica weight pull from the owner into the layer-shared replica slots). */
 int mb_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
 
 /* ---------------------------------------------------------------- peer memory / barrier
@@ -126,14 +150,18 @@ int mb_ipc_malloc(int64_t bytes, void** ptr, void* handle_out);
 int mb_ipc_open(const void* handle, void** ptr);
 int mb_ipc_close(void* ptr);
 int mb_device_free(void* ptr);
+/* Zeroed, device-mapped pinned host memory (the data plane's error flag: kernels OR bits into it,
+ * the host reads it without a device synchronisation). */
+int mb_host_alloc_mapped(int64_t bytes, void** host, void** dev);
+int mb_host_free(void* host);
 /* Device-side barrier over per-rank flag arrays (flags[p] = rank p's array of world u32); traps
  * after timeout_ns instead of hanging. */
 int mb_peer_barrier(uint32_t* const* flags, int32_t rank, int32_t world, uint32_t* epoch, int64_t timeout_ns,
                     int32_t* error_flag, void* stream);
 
 /* ---------------------------------------------------------------- GPU-side planning
- * The annealing chains of reorder.anneal_reorder (reorder.py:299-326) on the device, one thread
- * per chain, every (layer, seed) chain of a model in one launch: chain c anneals layer
+ * The annealing chains of reorder.anneal_reorder (reorder.py:299-326) on the device, one warp
+ * per chain (lanes split the O(G) element work, lane 0 owns the PCG64 stream), every (layer, seed) chain of a model in one launch: chain c anneals layer
  * c / chains_per_layer with contrib[layer] ([E][G][5][G] f64) and base[layer] ([E], the LPT start);
  * consts[5] and rng[nchains][4] as mbp_anneal_prepare (include/mb_planner.h) writes them.  Writes
  * each chain's best plan best[nchains][E] and its iteration count; pick each layer's plan with

@@ -183,3 +183,46 @@ def rel_err(got: torch.Tensor, ref: torch.Tensor) -> float:
     got, ref = got.float(), ref.float()
     den = ref.abs().max().clamp_min(1e-12)
     return float((got - ref.to(got.device)).abs().max() / den)
+
+
+def rel_l2(got: torch.Tensor, ref: torch.Tensor) -> float:
+    """||got - ref||_2 / ||ref||_2 over the whole tensor (normalised L2)."""
+    got, ref = got.float(), ref.float().to(got.device)
+    return float((got - ref).norm() / ref.norm().clamp_min(1e-30))
+
+
+def row_rel(got: torch.Tensor, ref: torch.Tensor, floor: float = 0.25) -> float:
+    """max over rows (last dim = a row) of ||got_row - ref_row|| / max(||ref_row||, floor x RMS row
+    norm): every row is judged on its own scale (cold experts, small tokens), not on the tensor's
+    maximum; the floor keeps rows that are small by cancellation (a dgate dot product near 0,
+    whose rounding error scales with its operands, not its value) from dominating."""
+    got, ref = got.float(), ref.float().to(got.device)
+    g2, r2 = got.reshape(-1, got.shape[-1]), ref.reshape(-1, ref.shape[-1])
+    rn = r2.norm(dim=1)
+    rms = rn.pow(2).mean().sqrt()
+    if float(rms) == 0.0:
+        return float((g2 - r2).abs().max()) if g2.numel() else 0.0
+    return float(((g2 - r2).norm(dim=1) / torch.maximum(rn, floor * rms)).max())
+
+
+# documented bf16 tolerances of the data plane against this fp32 restatement (north_star: rel 2e-2)
+TOL_MAX_REL = 2e-2     # max |d| / max |ref|
+TOL_L2 = 1e-2          # normalised L2 of the whole tensor
+TOL_ROW = 5e-2         # per row (token row of out / dx, k choices of dgate, per-expert gradient slice)
+
+
+def close(got: torch.Tensor, ref: torch.Tensor) -> dict:
+    """All three error measures and whether each is inside its documented bound."""
+    m = {"max_rel": rel_err(got, ref), "l2": rel_l2(got, ref), "row": row_rel(got, ref)}
+    m["ok"] = m["max_rel"] < TOL_MAX_REL and m["l2"] < TOL_L2 and m["row"] < TOL_ROW
+    return m
+
+
+def expert_grads_close(got: torch.Tensor, ref: torch.Tensor) -> dict:
+    """Per-expert gradients [experts, rows, cols]: every expert judged on its own norm (cold
+    experts included), plus the whole-tensor measures."""
+    m = close(got, ref)
+    per = [rel_l2(got[i], ref[i]) for i in range(got.shape[0]) if float(ref[i].float().abs().max()) > 0]
+    m["expert_l2_max"] = max(per) if per else 0.0
+    m["ok"] = m["ok"] and m["expert_l2_max"] < TOL_ROW
+    return m

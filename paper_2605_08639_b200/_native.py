@@ -41,29 +41,34 @@ _KERNEL_SIGS = {
     "mb_grouped_gemm": (
         c_int,
         [c_int, c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp, c_int, c_int, c_int, c_int,
-         c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp],
+         c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_i32, c_vp],
     ),
 }
 
 _KERNEL_SIGS.update({
     "mb_chunk_scan": (c_int, [c_vp, c_vp, c_i64, c_i32, c_i32, c_vp]),
-    "mb_permute_rank": (c_int, [c_vp, c_i64, c_i32, c_vp, c_i32, c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp]),
+    "mb_permute_rank": (c_int, [c_vp, c_i64, c_i32, c_vp, c_i32, c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp,
+                                c_vp]),
     "mb_permute_rank_nb": (c_int, [c_vp, c_i64, c_i32, c_vp, c_i32, c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_i32,
-                                   c_vp, c_i32, c_vp]),
+                                   c_vp, c_i32, c_vp, c_vp]),
+    "mb_check_counts": (c_int, [c_vp, c_vp, c_i64, c_vp, c_i32, c_vp]),
     "mb_zero_pad_rows_nb": (c_int, [c_vp, c_i64, c_vp, c_i32, c_i32, c_i32, c_vp]),
-    "mb_scatter_rows": (c_int, [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp]),
+    "mb_scatter_rows": (c_int, [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_i32, c_vp]),
     "mb_set_comm_blocks": (c_int, [c_i32]),
     "mb_anneal_chains": (c_int, [c_vp, c_i32, c_i32, c_vp, c_vp, c_dbl, c_vp, c_i32, c_i32, c_dbl, c_dbl, c_dbl, c_vp,
                                  c_vp, c_vp]),
-    "mb_combine_rows": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp]),
+    "mb_combine_rows": (c_int, [c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp]),
     "mb_combine_bwd_expert": (c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i64, c_i32, c_vp]),
     "mb_zero_pad_rows": (c_int, [c_vp, c_vp, c_i32, c_i32, c_vp]),
     "mb_accumulate_f32": (c_int, [c_vp, c_vp, c_i32, c_i64, c_vp]),
+    "mb_accumulate_f32_tasks": (c_int, [c_vp, c_i32, c_i64, c_vp]),
     "mb_ipc_malloc": (c_int, [c_i64, ctypes.POINTER(c_vp), c_vp]),
     "mb_ipc_handle_size": (c_int, []),
     "mb_ipc_open": (c_int, [c_vp, ctypes.POINTER(c_vp)]),
     "mb_ipc_close": (c_int, [c_vp]),
     "mb_device_free": (c_int, [c_vp]),
+    "mb_host_alloc_mapped": (c_int, [c_i64, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp)]),
+    "mb_host_free": (c_int, [c_vp]),
     "mb_memcpy_async": (c_int, [c_vp, c_vp, c_i64, c_vp]),
     "mb_peer_barrier": (c_int, [c_vp, c_i32, c_i32, c_vp, c_i64, c_vp, c_vp]),
 })

@@ -24,6 +24,8 @@
 
 namespace mb {
 
+constexpr int32_t kErrRoutingMismatch = MB_ERR_ROUTING_MISMATCH;
+
 // ------------------------------------------------------------------ chunk prefix scan
 // chunk_base[b][c][e] = sum_{c' < c} chunk_counts[b][c'][e]   (one warp per expert column)
 __global__ void __launch_bounds__(256) chunk_scan_kernel(const uint32_t* __restrict__ chunk_counts,
@@ -62,7 +64,7 @@ __global__ void __launch_bounds__(128) permute_rank_kernel(
     const int32_t* __restrict__ idx, int64_t T, int k, const float* __restrict__ gate, int E,
     const uint32_t* __restrict__ chunk_base, int chunk_tokens, const int4* __restrict__ route_tab,
     const int32_t* __restrict__ ncopies, int maxc, float* const* __restrict__ dst_gate, int2* __restrict__ perm,
-    int world) {
+    int world, int32_t* __restrict__ error_flag) {
   extern __shared__ uint32_t running_all[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int chunk = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -113,10 +115,30 @@ __global__ void __launch_bounds__(128) permute_rank_kernel(
       prev = ent.x;
       ent = tab[++c];
     }
+    if (static_cast<int>(r) >= ent.x) {
+      // more tokens of expert e than the plan's split counts: the routing differs from the
+      // (replayed) counts the tables were built for.  Drop the choice instead of writing past
+      // the receive slot, and flag it (the host raises).
+      perm[n] = make_int2(-1, -1);
+      if (error_flag) atomicOr(error_flag, kErrRoutingMismatch);
+      continue;
+    }
     const int row = ent.z + static_cast<int>(r) - prev;
     perm[n] = make_int2(ent.y, row);
     if (gate && dst_gate) dst_gate[ent.y][row] = gate[n];
   }
+}
+
+// ------------------------------------------------------------------ routing / plan consistency
+// counts[i] (K1 histogram) must equal expected[i] (the counts the step plan was built from);
+// a mismatch sets `code` in the host-visible error flag.  The permutation kernel additionally
+// drops (perm = -1) any choice whose rank falls past its expert's planned rows.
+__global__ void __launch_bounds__(256) check_counts_kernel(const uint32_t* __restrict__ counts,
+                                                           const int32_t* __restrict__ expected, int64_t n,
+                                                           int32_t* __restrict__ error_flag, int32_t code) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    if (counts[i] != static_cast<uint32_t>(expected[i])) atomicOr(error_flag, code);
 }
 
 // ------------------------------------------------------------------ K3 scatter (dispatch A2A)
@@ -578,6 +600,33 @@ __global__ void __launch_bounds__(256) accumulate_f32_kernel(float4* __restrict_
   }
 }
 
+// Batched replica-gradient push-back: task b adds (or, first contribution, stores) the sum of its
+// sources in list order into its destination -- one launch per micro-batch covers every home
+// expert whose replicas served rows (replica gradients accumulate at the owner).
+struct AccTask {
+  float* dst;
+  const float* src[MB_ACC_MAX_SRC];
+  int64_t n;      // floats, multiple of 4
+  int32_t nsrc;
+  int32_t store;  // 1: dst = sum(src) (the expert's first gradient contribution of a fresh step)
+};
+static_assert(sizeof(AccTask) == 8 + 8 * MB_ACC_MAX_SRC + 16, "AccTask layout is part of the C-ABI");
+
+__global__ void __launch_bounds__(256) accumulate_tasks_kernel(const AccTask* __restrict__ tasks) {
+  const AccTask& t = tasks[blockIdx.y];
+  float4* dst = reinterpret_cast<float4*>(t.dst);
+  const int64_t n4 = t.n >> 2;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float4 a = t.store ? make_float4(0.f, 0.f, 0.f, 0.f) : dst[i];
+    for (int s = 0; s < t.nsrc; ++s) {
+      const float4 b = reinterpret_cast<const float4*>(t.src[s])[i];
+      a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    }
+    dst[i] = a;
+  }
+}
+
 // Row-moving kernels run concurrently with the persistent GEMM.  comm_smem() > 0 reserves that
 // much dynamic shared memory per block so the blocks cannot co-reside with a GEMM CTA (they
 // stay on the SMs the GEMM leaves free); comm_grid() caps the grid (experiment knobs:
@@ -595,8 +644,10 @@ inline int64_t comm_grid() {
 
 // TMA row movers (scatter_rows_tma_kernel / combine_rows_tma_kernel): number of blocks, one per
 // SM; 0 = the register-copy kernels (mb_set_comm_blocks, env MB_COMM_BLOCKS overrides).
+// A call's own value (>= 0: a data plane passes its engine) wins over the process default.
 static int g_comm_blocks = 0;
-inline int comm_blocks() {
+inline int comm_blocks(int per_call) {
+  if (per_call >= 0) return per_call;
   if (const char* e = std::getenv("MB_COMM_BLOCKS")) return std::atoi(e);
   return g_comm_blocks;
 }
@@ -627,7 +678,7 @@ extern "C" int mb_chunk_scan(const uint32_t* chunk_counts, uint32_t* chunk_base,
 extern "C" int mb_permute_rank(const int32_t* idx, int64_t T, int32_t k, const float* gate, int32_t E,
                                const uint32_t* chunk_base, int32_t chunk_tokens, const int32_t* route_tab,
                                const int32_t* ncopies, int32_t maxc, float* const* dst_gate, int32_t* perm,
-                               void* stream) {
+                               int32_t* error_flag, void* stream) {
   MB_CHECK_ARG(T >= 0 && k >= 1 && E >= 1 && E <= 2048 && chunk_tokens >= 1 && maxc >= 1, "bad permute args");
   MB_CHECK_ARG(idx && chunk_base && route_tab && ncopies && perm, "null permute operand");
   if (T == 0) return MB_OK;
@@ -637,7 +688,7 @@ extern "C" int mb_permute_rank(const int32_t* idx, int64_t T, int32_t k, const f
   permute_rank_kernel<<<static_cast<unsigned>(grid), 32 * wpb, wpb * E * sizeof(uint32_t),
                         reinterpret_cast<cudaStream_t>(stream)>>>(
       idx, T, k, gate, E, chunk_base, chunk_tokens, reinterpret_cast<const int4*>(route_tab), ncopies, maxc, dst_gate,
-      reinterpret_cast<int2*>(perm), 0);
+      reinterpret_cast<int2*>(perm), 0, error_flag);
   MB_CUDA_TRY(cudaGetLastError());
   return MB_OK;
 }
@@ -645,7 +696,7 @@ extern "C" int mb_permute_rank(const int32_t* idx, int64_t T, int32_t k, const f
 extern "C" int mb_permute_rank_nb(const int32_t* idx, int64_t T, int32_t k, const float* gate, int32_t E,
                                   const uint32_t* chunk_base, int32_t chunk_tokens, const int32_t* route_tab,
                                   const int32_t* ncopies, int32_t maxc, float* const* dst_gate, int32_t world,
-                                  int32_t* perm, int32_t nb, void* stream) {
+                                  int32_t* perm, int32_t nb, int32_t* error_flag, void* stream) {
   MB_CHECK_ARG(T >= 0 && k >= 1 && E >= 1 && E <= 2048 && chunk_tokens >= 1 && maxc >= 1 && nb >= 0 && world >= 1,
                "bad permute args");
   MB_CHECK_ARG(idx && chunk_base && route_tab && ncopies && perm, "null permute operand");
@@ -655,7 +706,7 @@ extern "C" int mb_permute_rank_nb(const int32_t* idx, int64_t T, int32_t k, cons
   dim3 grid(static_cast<unsigned>((chunks + wpb - 1) / wpb), static_cast<unsigned>(nb));
   permute_rank_kernel<<<grid, 32 * wpb, wpb * E * sizeof(uint32_t), reinterpret_cast<cudaStream_t>(stream)>>>(
       idx, T, k, gate, E, chunk_base, chunk_tokens, reinterpret_cast<const int4*>(route_tab), ncopies, maxc, dst_gate,
-      reinterpret_cast<int2*>(perm), world);
+      reinterpret_cast<int2*>(perm), world, error_flag);
   MB_CUDA_TRY(cudaGetLastError());
   return MB_OK;
 }
@@ -668,10 +719,10 @@ extern "C" int mb_set_comm_blocks(int32_t blocks) {
 }
 
 extern "C" int mb_scatter_rows(const void* x, int64_t T, int32_t k, int32_t h, const int32_t* perm,
-                               void* const* dst_rows, void* stream) {
+                               void* const* dst_rows, int32_t comm_blocks_call, void* stream) {
   MB_CHECK_ARG(x && perm && dst_rows && T >= 0 && k >= 1 && h >= 8 && h % 8 == 0, "bad scatter args");
   if (T == 0) return MB_OK;
-  if (const int nb = comm_blocks(); nb > 0) {
+  if (const int nb = comm_blocks(comm_blocks_call); nb > 0) {
     const int row_bytes = 2 * h;
     int warps = 8, nbuf = 0;
     while (warps > 1 && (nbuf = (kTmaSmemBudget - kTmaBarBytes) / (warps * row_bytes)) < 3) warps >>= 1;
@@ -701,7 +752,7 @@ extern "C" int mb_scatter_rows(const void* x, int64_t T, int32_t k, int32_t h, c
 
 extern "C" int mb_combine_rows(const void* const* src_rows, const int32_t* perm, const float* gate, int64_t T, int32_t k,
                                int32_t h, void* out, const float* const* src_scalar, float* scalar_out,
-                               int32_t npart, void* stream) {
+                               int32_t npart, int32_t comm_blocks_call, void* stream) {
   MB_CHECK_ARG(src_rows && perm && out && T >= 0 && k >= 1 && k <= 32 && h >= 8 && h % 8 == 0, "bad combine args");
   MB_CHECK_ARG((scalar_out == nullptr) == (src_scalar == nullptr), "src_scalar and scalar_out go together");
   MB_CHECK_ARG(npart >= 1, "npart must be >= 1");
@@ -711,7 +762,7 @@ extern "C" int mb_combine_rows(const void* const* src_rows, const int32_t* perm,
   const int2* pr = reinterpret_cast<const int2*>(perm);
   uint4* o = reinterpret_cast<uint4*>(out);
   const char* ce = std::getenv("MB_COMBINE_ENGINE");
-  if (const int nb = comm_blocks(); nb > 0 && k <= 8 && !(ce && std::string(ce) == "tma")) {
+  if (const int nb = comm_blocks(comm_blocks_call); nb > 0 && k <= 8 && !(ce && std::string(ce) == "tma")) {
     // confined register engine: the smem reservation keeps the blocks off the GEMM's SMs
     constexpr int kReserve = 100 * 1024;
     const int kmax = k <= 2 ? 2 : k <= 4 ? 4 : 8;
@@ -725,7 +776,7 @@ extern "C" int mb_combine_rows(const void* const* src_rows, const int32_t* perm,
     if (kmax == 4) return launch(combine_rows_mlp_kernel<4, 2>);
     return launch(combine_rows_mlp_kernel<8, 2>);
   }
-  if (const int nb = comm_blocks(); nb > 0 && k <= 16 && (!scalar_out || (npart % 4 == 0 && npart <= 64))) {
+  if (const int nb = comm_blocks(comm_blocks_call); nb > 0 && k <= 16 && (!scalar_out || (npart % 4 == 0 && npart <= 64))) {
     const int kmax = k <= 2 ? 2 : k <= 4 ? 4 : k <= 8 ? 8 : 16;
     // whole rows per slot (MB_COMBINE_SPLIT=n: 1/n pieces -- measured n times slower: the cost is
     // per bulk operation, not per byte)
@@ -807,6 +858,29 @@ extern "C" int mb_accumulate_f32(float* dst, const float* const* srcs, int32_t n
   if (n == 0 || nsrc == 0) return MB_OK;
   accumulate_f32_kernel<<<grid_for(n / 4, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<float4*>(dst), reinterpret_cast<const float4* const*>(srcs), nsrc, n / 4);
+  MB_CUDA_TRY(cudaGetLastError());
+  return MB_OK;
+}
+
+extern "C" int mb_check_counts(const uint32_t* counts, const int32_t* expected, int64_t n, int32_t* error_flag,
+                               int32_t code, void* stream) {
+  MB_CHECK_ARG(counts && expected && error_flag && n >= 0 && code != 0, "bad check_counts args");
+  if (n == 0) return MB_OK;
+  check_counts_kernel<<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 1024)), 256, 0,
+                        reinterpret_cast<cudaStream_t>(stream)>>>(counts, expected, n, error_flag, code);
+  MB_CUDA_TRY(cudaGetLastError());
+  return MB_OK;
+}
+
+extern "C" int mb_accumulate_f32_tasks(const void* tasks, int32_t ntasks, int64_t max_n, void* stream) {
+  MB_CHECK_ARG(ntasks >= 0 && ntasks <= 65535 && max_n >= 0 && max_n % 4 == 0 && (ntasks == 0 || tasks),
+               "bad accumulate task args");
+  if (ntasks == 0 || max_n == 0) return MB_OK;
+  const int per_task = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((max_n / 4 + 255) / 256,
+                                                                                  std::max(1, 2 * device_sm_count() / ntasks))));
+  dim3 grid(static_cast<unsigned>(per_task), static_cast<unsigned>(ntasks));
+  accumulate_tasks_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const AccTask*>(tasks));
   MB_CUDA_TRY(cudaGetLastError());
   return MB_OK;
 }

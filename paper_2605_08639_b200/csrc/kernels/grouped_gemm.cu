@@ -9,7 +9,7 @@
 
 namespace mb {
 
-static int gemm_sms();
+static int gemm_sms(int per_call);
 
 template <bool kW, bool kAmn, bool kBmn, int BN, int kEpi>
 static int launch_gemm(const GemmParams& p, cudaStream_t stream) {
@@ -25,14 +25,14 @@ static int launch_gemm(const GemmParams& p, cudaStream_t stream) {
 }
 
 template <bool kW, bool kAmn, bool kBmn, int kEpi>
-static int launch_pair(const GemmParams& p, cudaStream_t stream) {
+static int launch_pair(const GemmParams& p, cudaStream_t stream, int sms) {
   auto kern = grouped_gemm_pair_kernel<kW, kAmn, kBmn, kEpi>;
   static bool attr_set = false;
   if (!attr_set) {
     MB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<kEpi>::kSmemBytes));
     attr_set = true;
   }
-  const int grid = gemm_sms() & ~1;
+  const int grid = gemm_sms(sms) & ~1;
   static unsigned long long* prof = nullptr;
 #ifdef MB_GEMM_PROFILE
   const bool profile = std::getenv("MB_GEMM_PROF") != nullptr;
@@ -59,13 +59,15 @@ static int launch_pair(const GemmParams& p, cudaStream_t stream) {
   return MB_OK;
 }
 
-// SMs the persistent GEMM occupies (mb_set_gemm_sms / MB_GEMM_SMS, default all): the rest stay
-// free for the dispatch / combine kernels the comm stream runs concurrently.
+// SMs the persistent GEMM occupies: the per-call value (a data plane passes its own split), else
+// the process default (mb_set_gemm_sms / MB_GEMM_SMS, default all).  The SMs left free run the
+// dispatch / combine kernels the comm stream runs concurrently.
 static int g_gemm_sms = 0;
-static int gemm_sms() {
+static int gemm_sms(int per_call) {
   const int n = device_sm_count();
   int v = g_gemm_sms;
   if (const char* e = std::getenv("MB_GEMM_SMS")) v = std::atoi(e);
+  if (per_call > 0) v = per_call;
   return (v >= 2 && v <= n) ? v : n;
 }
 
@@ -92,7 +94,8 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
                                int64_t b0_rows, const void* B1, int64_t b1_rows, int64_t b_cols,
                                const void* groups, const void* segs, int num_groups, int M, int N, int K, void* C,
                                int64_t ldc, int64_t c_slot_stride, void* C2, int64_t ldc2, const void* aux,
-                               int64_t ld_aux, const float* row_scale, float* row_partial, void* stream) {
+                               int64_t ld_aux, const float* row_scale, float* row_partial, int32_t gemm_sms,
+                               void* stream) {
   const bool force_single = (mode & 0x100) != 0 || !pair_enabled();
   mode &= 0xff;
   MB_CHECK_ARG(num_groups >= 0 && num_groups <= kMaxGroups, "num_groups %d outside [0, %d]", num_groups, kMaxGroups);
@@ -140,10 +143,10 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
         if ((rc = make_tmap_bf16_2d(&p.tmB1h, B1, b_cols, b1_rows, b_cols * 2, 64, 64))) return rc;
       }
       if (mode == MB_GEMM_FWD_STORE)
-        return pair ? launch_pair<false, false, false, EPI_STORE_BF16>(p, s)
+        return pair ? launch_pair<false, false, false, EPI_STORE_BF16>(p, s, gemm_sms)
                     : launch_gemm<false, false, false, 256, EPI_STORE_BF16>(p, s);
       MB_CHECK_ARG(C2 != nullptr, "SwiGLU epilogue needs the activation output");
-      return pair ? launch_pair<false, false, false, EPI_SWIGLU>(p, s)
+      return pair ? launch_pair<false, false, false, EPI_SWIGLU>(p, s, gemm_sms)
                   : launch_gemm<false, false, false, 256, EPI_SWIGLU>(p, s);
     }
     case MB_GEMM_DGRAD_DSWIGLU_GATED: {
@@ -154,7 +157,7 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
       if ((rc = make_tmap_bf16_2d(&p.tmAh, A, a_cols, a_rows, a_cols * 2, 64, 64))) return rc;
       if ((rc = make_tmap_bf16_2d(&p.tmB0, B0, b_cols, b0_rows, b_cols * 2, 64, 64))) return rc;
       if ((rc = make_tmap_bf16_2d(&p.tmB1, B1, b_cols, b1_rows, b_cols * 2, 64, 64))) return rc;
-      return launch_pair<false, false, true, EPI_DSWIGLU_GATED>(p, s);
+      return launch_pair<false, false, true, EPI_DSWIGLU_GATED>(p, s, gemm_sms);
     }
     case MB_GEMM_DGRAD_STORE:
     case MB_GEMM_DGRAD_DSWIGLU: {
@@ -165,11 +168,11 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
       if ((rc = make_tmap_bf16_2d(&p.tmB1, B1, b_cols, b1_rows, b_cols * 2, 64, 64))) return rc;
       if (mode == MB_GEMM_DGRAD_STORE) {
         MB_CHECK_ARG(N % 256 == 0, "dgrad N=%d must be a multiple of 256", N);
-        return pair ? launch_pair<false, false, true, EPI_STORE_BF16>(p, s)
+        return pair ? launch_pair<false, false, true, EPI_STORE_BF16>(p, s, gemm_sms)
                     : launch_gemm<false, false, true, 256, EPI_STORE_BF16>(p, s);
       }
       MB_CHECK_ARG(N % 128 == 0 && aux != nullptr, "dSwiGLU epilogue needs N%%128==0 and H");
-      return pair ? launch_pair<false, false, true, EPI_DSWIGLU>(p, s)
+      return pair ? launch_pair<false, false, true, EPI_DSWIGLU>(p, s, gemm_sms)
                   : launch_gemm<false, false, true, 128, EPI_DSWIGLU>(p, s);
     }
     case MB_GEMM_WGRAD: {
@@ -177,7 +180,7 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
       if ((rc = make_tmap_bf16_2d(&p.tmA, A, a_cols, a_rows, a_cols * 2, 64, 64))) return rc;
       if ((rc = make_tmap_bf16_2d(&p.tmB0, B0, b_cols, b0_rows, b_cols * 2, 64, 64))) return rc;
       p.tmB1 = p.tmB0;
-      return pair ? launch_pair<true, true, true, EPI_ACC_F32>(p, s)
+      return pair ? launch_pair<true, true, true, EPI_ACC_F32>(p, s, gemm_sms)
                   : launch_gemm<true, true, true, 256, EPI_ACC_F32>(p, s);
     }
     default:

@@ -5,6 +5,7 @@
 // (topology.py:29-47) are flat modelled bandwidths.  On B200 every GPU pair is one NVSwitch
 // hop, so receive buffers are plain cudaMalloc allocations exported with cudaIpcGetMemHandle
 // and opened by every peer; kernels then load/store peer rows directly.
+#include <cstring>
 #include "capi_common.cuh"
 #include "../../../include/mb_kernels.h"
 
@@ -83,6 +84,19 @@ extern "C" int mb_ipc_close(void* ptr) {
 
 extern "C" int mb_device_free(void* ptr) {
   MB_CUDA_TRY(cudaFree(ptr));
+  return MB_OK;
+}
+
+extern "C" int mb_host_alloc_mapped(int64_t bytes, void** host, void** dev) {
+  MB_CHECK_ARG(bytes > 0 && host && dev, "bad mapped host allocation args");
+  MB_CUDA_TRY(cudaHostAlloc(host, static_cast<size_t>(bytes), cudaHostAllocMapped | cudaHostAllocPortable));
+  std::memset(*host, 0, static_cast<size_t>(bytes));
+  MB_CUDA_TRY(cudaHostGetDevicePointer(dev, *host, 0));
+  return MB_OK;
+}
+
+extern "C" int mb_host_free(void* host) {
+  if (host) MB_CUDA_TRY(cudaFreeHost(host));
   return MB_OK;
 }
 

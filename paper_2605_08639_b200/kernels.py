@@ -75,8 +75,10 @@ def grouped_gemm(mode: int, A: torch.Tensor, B0: torch.Tensor, groups: torch.Ten
                  K: int = 0, C: torch.Tensor, C2: torch.Tensor | None = None, aux: torch.Tensor | None = None,
                  B1: torch.Tensor | None = None, c_slot_stride: int = 0,
                  segs: torch.Tensor | None = None, row_scale: torch.Tensor | None = None,
-                 row_partial: torch.Tensor | None = None, single_cta: bool = False) -> None:
-    """K4: tcgen05 grouped GEMM; see include/mb_kernels.h for the five modes."""
+                 row_partial: torch.Tensor | None = None, single_cta: bool = False, sms: int = 0,
+                 stream=None) -> None:
+    """K4: tcgen05 grouped GEMM; see include/mb_kernels.h for the five modes.  sms > 0: SMs the
+    persistent grid covers for this launch (0 = the process default); stream: default current."""
     _need_cuda(A, B0, groups, C, C2, aux, B1)
     for t in (A, B0, B1):
         if t is not None and (t.dtype != torch.bfloat16 or not t.is_contiguous()):
@@ -96,5 +98,5 @@ def grouped_gemm(mode: int, A: torch.Tensor, B0: torch.Tensor, groups: torch.Ten
                                   B0.data_ptr(), b0_rows, nat.ptr(B1), b1_rows, b_cols, groups.data_ptr(),
                                   nat.ptr(segs), groups.shape[0], M, N, K,
                                   C.data_ptr(), ldc, c_slot_stride, nat.ptr(C2), ldc2, nat.ptr(aux), ld_aux,
-                                  nat.ptr(row_scale), nat.ptr(row_partial), nat.stream_ptr()),
+                                  nat.ptr(row_scale), nat.ptr(row_partial), int(sms), nat.stream_ptr(stream)),
               lib, "mb_grouped_gemm")

@@ -26,6 +26,7 @@ backward_mb / end_step and the MoELayerFunction autograd entry.
 
 from __future__ import annotations
 
+import ctypes
 import os
 from dataclasses import dataclass, field
 
@@ -53,6 +54,9 @@ COMM_SMS_MULTI = 32                # N >= 8 (most NVLink rows per GPU) keeps the
 # step with 140 GEMM SMs); Qwen3-235B (h' = 1536) is comm-bound on 16 (68.7-70.0 -> 73.0-73.2 ms).
 COMM_SMS_WIDE_FFN = 8
 WIDE_FFN = 4096
+WIDE_HIDDEN = 4096   # 4096-wide token rows (Qwen3-235B): its N=4 numbers were measured with 32 comm SMs
+# sets of the layer-shared replica weight slots (MoEDataPlane replica_sets; MB_REPLICA_SETS overrides)
+REPLICA_SETS = 2
 # Row-mover engine per world size: "regs" = register-copy kernels (co-resident with the GEMM's
 # CTAs on every SM), "tma" = cp.async.bulk kernels, one block on each of the COMM_SMS SMs the
 # GEMM leaves free (bulk-copy scatter, register combine with a shared-memory reservation).
@@ -60,9 +64,9 @@ WIDE_FFN = 4096
 # vs regs 19.2-19.26 per step; at N=1 (HBM-local moves) regs is faster (18.8-19.3 vs >= 20.1).
 ROW_MOVERS = {1: "regs"}
 ROW_MOVERS_MULTI = "tma"
-# with replicas (N>1) the second weight-gradient launch runs on every SM: by then the comm stream
-# only has the replica-gradient reduce (register kernel, co-resident) left (N=4: 18.9-19.0 ->
-# 18.7-18.9 ms; at N=1 widening the single launch measured 3% slower).  MB_WGRAD_ALL_SMS=0: A/B.
+# with replicas (N>1) the last weight-gradient launch runs on every SM: by then the comm stream
+# is idle (N=4: 18.9-19.0 -> 18.7-18.9 ms; at N=1 widening the single launch measured 3% slower).
+# MB_WGRAD_ALL_SMS=0: A/B.
 WGRAD_ALL_SMS = os.environ.get("MB_WGRAD_ALL_SMS", "1") == "1"
 # overlap=False runs every phase in issue order on one stream with all SMs in the GEMM: at world 1
 # (local row movers) it measured the same step time as the overlapped schedule (19.6 vs 19.4 ms).
@@ -273,21 +277,28 @@ def default_comm_sms(world: int, shape: "LayerShape") -> int:
         return COMM_SMS[1]
     if shape.ffn >= WIDE_FFN:
         return COMM_SMS_WIDE_FFN
+    if shape.hidden >= WIDE_HIDDEN:
+        return COMM_SMS_MULTI    # comm-bound 4096-wide rows (Qwen3-235B): the 32-SM split was measured
     return COMM_SMS.get(world, COMM_SMS_MULTI)
 
 
-def schedule(mb: int):
+def schedule(mb: int, wgrad_mode: str = "step"):
     """Per-rank issue order of one step, two micro-batches in flight (the two-batch overlap of
     EP training systems): compute runs F0 F1 B0 F2 B1 ... F(n-1) B(n-2) B(n-1), the comm stream
     D0 D1 C0 [D(m) C(m-1) X(m-2)]... so every all-to-all overlaps a GEMM phase of the neighbouring
     micro-batch, while each combine is still a global sync point: a rank can run at most one
     phase ahead of the slowest rank, so load imbalance is paid per micro-batch (as the
     reference's cost model sums it, sim.py:89-110), not averaged over the step.
-    F = fwd GEMMs, B = bwd GEMMs, D = dispatch, C = combine + dout dispatch, X = dX un-permute."""
+    F = fwd GEMMs, B = bwd GEMMs (+ replica weight gradients), W = home weight gradients of one
+    micro-batch (wgrad_mode "micro_batch" only), D = dispatch, C = combine + dout dispatch,
+    X = dX un-permute + replica-gradient push-back to the owners."""
     comp = [("F", 0)]
+    per_mb = wgrad_mode == "micro_batch"
     for m in range(1, mb):
-        comp += [("F", m), ("B", m - 1)]
+        comp += [("F", m), ("B", m - 1)] + ([("W", m - 1)] if per_mb else [])
     comp.append(("B", mb - 1))
+    if per_mb:
+        comp.append(("W", mb - 1))
     comm = [("D", 0)]
     if mb > 1:
         comm += [("D", 1)]
@@ -300,14 +311,50 @@ def schedule(mb: int):
     return comm, comp
 
 
+# micro-batch activation / receive buffer sets in wgrad_mode "micro_batch": D(m + 3) is the first
+# phase to reuse micro-batch m's set, and every rank's comm stream reaches it only after X(m)'s
+# barrier (all ranks finished B(m) / W(m)), so three sets suffice for the schedule above
+RING_SETS = 3
+# replica-gradient ring: B(m) writes set m % 2, the owners read it in X(m); B(m + 2) runs after
+# C(m + 2)'s barrier, which every rank reaches after its X(m) push-back
+GRAD_RING = 2
+ACC_TASK = np.dtype([("dst", "<u8"), ("src", "<u8", (8,)), ("n", "<i8"), ("nsrc", "<i4"), ("store", "<i4")])
+ERR_BITS = {1: "routing has more tokens for an expert than the step plan's counts (perm dropped them)",
+            2: "device histogram differs from the counts the step plan was built for"}
+
+
+def _wgrad_table(rows: list) -> np.ndarray:
+    tab = np.zeros((max(1, len(rows)), K.GROUP_FIELDS), dtype=np.int32)
+    for i, row in enumerate(rows):
+        tab[i] = row
+    return tab[:len(rows)] if rows else tab[:0]
+
+
+class PlanTables:
+    """A step plan's device tables for one data plane (MoEDataPlane.build_tables): built ahead,
+    installed by load_plan / migrate without host work on the step's critical path."""
+
+    def __init__(self, owner, plan: StepPlan, attrs: dict):
+        self.owner, self.plan, self.attrs = owner, plan, attrs
+
+
 class MoEDataPlane:
-    """Per-rank device state for one MoE layer: home experts, per-micro-batch replica slots,
-    fp32 gradients, per-micro-batch receive/activation buffers and the step tables."""
+    """Per-rank device state for one MoE layer: home experts (+ fp32 gradients, optional expert
+    state, double-banked for migration), the layer-shared replica slots, the replica-gradient
+    ring, receive/activation buffers and the step tables.
+
+    wgrad_mode "step" (default): weight gradients contract over every micro-batch of the step in
+    one GEMM per weight (receive / activation buffers for all MB micro-batches stay resident);
+    "micro_batch": each micro-batch's weight gradients are accumulated right after its backward
+    (K = that micro-batch's rows), so only RING_SETS micro-batches of activations exist.
+    replica_sets: sets of r replica weight slots (r = plan.slots); 1 = the paper's layer-shared
+    buffer of exactly replica_memory(model, cfg, "layer-shared") bytes (replica weights are pulled
+    again for the backward), 2 = double-buffered pulls."""
 
     def __init__(self, comm: Comm, shape: LayerShape, tokens: int, micro_batches: int, plan: StepPlan,
                  device: torch.device | None = None, comm_sms: int | None = None,
                  expert_state: dict | None = None, rows_cap: int = 0, overlap: bool | None = None,
-                 row_movers: str | None = None):
+                 row_movers: str | None = None, wgrad_mode: str | None = None, replica_sets: int | None = None):
         """expert_state: optional per-expert tensors that follow their expert when the reorder
         plan migrates it (e.g. optimizer moments): {name: (per-expert shape, torch dtype)}.
         rows_cap: receive rows per micro-batch to allocate (>= every plan this layer will load).
@@ -320,87 +367,126 @@ class MoEDataPlane:
         if overlap is None and os.environ.get("MB_OVERLAP") in ("0", "1"):
             overlap = os.environ["MB_OVERLAP"] == "1"
         self.overlap = True if overlap is None else overlap
+        wgrad_mode = wgrad_mode or os.environ.get("MB_WGRAD_MODE", "step")
+        if wgrad_mode not in ("step", "micro_batch"):
+            raise ValueError(f"wgrad_mode must be 'step' or 'micro_batch', got {wgrad_mode!r}")
+        self.wgrad_mode = wgrad_mode
+        if replica_sets is None:
+            replica_sets = int(os.environ.get("MB_REPLICA_SETS", REPLICA_SETS))
+        if replica_sets < 1:
+            raise ValueError("replica_sets must be >= 1")
+        self.replica_sets = replica_sets
         if comm_sms is None:
             comm_sms = default_comm_sms(self.world, shape) if self.overlap else 0
         sms = torch.cuda.get_device_properties(self.device).multi_processor_count
-        lib = nat.kernels()
+        # per-plane launch settings, passed with every launch (never process-global)
         self.gemm_sms, self.all_sms = max(2, sms - comm_sms), sms
-        nat.check(lib.mb_set_gemm_sms(self.gemm_sms), lib, "mb_set_gemm_sms")
         if row_movers is None:
             row_movers = os.environ.get("MB_ROW_MOVERS") or ROW_MOVERS.get(self.world, ROW_MOVERS_MULTI)
         if row_movers not in ("regs", "tma"):
             raise ValueError(f"row_movers must be 'regs' or 'tma', got {row_movers!r}")
         self.row_movers = row_movers
-        nat.check(lib.mb_set_comm_blocks(comm_sms if (row_movers == "tma" and comm_sms > 0) else 0), lib,
-                  "mb_set_comm_blocks")
+        self.comm_sms = comm_sms
+        self.comm_blocks = comm_sms if (row_movers == "tma" and comm_sms > 0) else 0
         E, h, hp = shape.num_experts, shape.hidden, shape.ffn
         if E % self.world:
             raise ValueError(f"{E} experts not divisible by {self.world} GPUs")
         self.M = E // self.world
         self.R = max(plan.rows_cap, (rows_cap + PAD - 1) // PAD * PAD)
         self.slots = max(plan.slots, 1)
-        self.rep_cap = max(1, self.slots * micro_batches)
+        self.NA = micro_batches if wgrad_mode == "step" else min(micro_batches, RING_SETS)
         bf, f4 = 2, 4
         self.npart = hp // 64    # dgate partials per row (one per 64 features of h')
-        R, MB = self.R, micro_batches
-        S = self.M + self.rep_cap
+        R, NA = self.R, self.NA
         self.w1_bytes, self.w2_bytes = 2 * hp * h * bf, h * hp * bf
+        self.g1_bytes, self.g2_bytes = 2 * hp * h * f4, h * hp * f4
         # ---- symmetric arena (peer-visible buffers; identical layout on every rank)
         sizes = {
-            "xr": MB * R * h * bf, "y": MB * R * h * bf, "dyr": MB * R * h * bf, "dxp": MB * R * h * bf,
-            "gate_r": MB * R * f4, "dgate_r": MB * R * self.npart * f4,
-            "w1r": MB * self.slots * self.w1_bytes, "w2r": MB * self.slots * self.w2_bytes,
+            "xr": NA * R * h * bf, "y": NA * R * h * bf, "dyr": NA * R * h * bf, "dxp": NA * R * h * bf,
+            "gate_r": NA * R * f4, "dgate_r": NA * R * self.npart * f4,
+            # layer-shared replica weight slots (pulled by this rank from the owners) and the
+            # replica-gradient ring the owners read back
+            "w1r": replica_sets * self.slots * self.w1_bytes, "w2r": replica_sets * self.slots * self.w2_bytes,
+            "rg1": GRAD_RING * self.slots * self.g1_bytes, "rg2": GRAD_RING * self.slots * self.g2_bytes,
             # home-expert weights, fp32 gradients and expert state live in two banks: a migration
             # (new reorder plan) pulls every new home expert into the idle bank, then swaps
             "w1": self.M * self.w1_bytes, "w2": self.M * self.w2_bytes,
-            "gw1": S * 2 * hp * h * f4, "gw2": S * h * hp * f4,
+            "gw1": self.M * self.g1_bytes, "gw2": self.M * self.g2_bytes,
             "w1b": self.M * self.w1_bytes, "w2b": self.M * self.w2_bytes,
-            "gw1b": S * 2 * hp * h * f4, "gw2b": S * h * hp * f4,
+            "gw1b": self.M * self.g1_bytes, "gw2b": self.M * self.g2_bytes,
         }
         self.state_spec = {}
         for name, (eshape, dtype) in (expert_state or {}).items():
             nbytes = int(np.prod(eshape)) * torch.empty((), dtype=dtype).element_size()
             self.state_spec[name] = (tuple(eshape), dtype, nbytes)
             sizes["st_" + name] = sizes["st_" + name + "b"] = self.M * nbytes
+        self.sizes = sizes
         total = sum((v + 1023) // 1024 * 1024 for v in sizes.values()) + 1024 * len(sizes)
         self.arena = SymmetricArena(comm, total, self.device)
         self.off = {key: self.arena.alloc(v) for key, v in sizes.items()}
         A = self.arena
-        self.Xr = A.local(self.off["xr"], (MB, R, h), torch.bfloat16)
-        self.Y = A.local(self.off["y"], (MB, R, h), torch.bfloat16)
-        self.dYr = A.local(self.off["dyr"], (MB, R, h), torch.bfloat16)
-        self.dXp = A.local(self.off["dxp"], (MB, R, h), torch.bfloat16)
-        self.gate_r = A.local(self.off["gate_r"], (MB, R), torch.float32)
-        self.dgate_r = A.local(self.off["dgate_r"], (MB, R, self.npart), torch.float32)
-        self.W1r = A.local(self.off["w1r"], (MB, self.slots, 2 * hp, h), torch.bfloat16)
-        self.W2r = A.local(self.off["w2r"], (MB, self.slots, h, hp), torch.bfloat16)
-        self.S = S
+        self.Xr = A.local(self.off["xr"], (NA, R, h), torch.bfloat16)
+        self.Y = A.local(self.off["y"], (NA, R, h), torch.bfloat16)
+        self.dYr = A.local(self.off["dyr"], (NA, R, h), torch.bfloat16)
+        self.dXp = A.local(self.off["dxp"], (NA, R, h), torch.bfloat16)
+        self.gate_r = A.local(self.off["gate_r"], (NA, R), torch.float32)
+        self.dgate_r = A.local(self.off["dgate_r"], (NA, R, self.npart), torch.float32)
+        self.W1r = A.local(self.off["w1r"], (replica_sets, self.slots, 2 * hp, h), torch.bfloat16)
+        self.W2r = A.local(self.off["w2r"], (replica_sets, self.slots, h, hp), torch.bfloat16)
+        self.rgW1 = A.local(self.off["rg1"], (GRAD_RING, self.slots, 2 * hp, h), torch.float32)
+        self.rgW2 = A.local(self.off["rg2"], (GRAD_RING, self.slots, h, hp), torch.float32)
         self.bank = 0
         self._bind_bank()
         # ---- local activations
-        self.H = torch.empty((MB, R, 2 * hp), dtype=torch.bfloat16, device=self.device)
-        self.Act = torch.empty((MB, R, hp), dtype=torch.bfloat16, device=self.device)
-        self.dH = torch.empty((MB, R, 2 * hp), dtype=torch.bfloat16, device=self.device)
+        self.H = torch.empty((NA, R, 2 * hp), dtype=torch.bfloat16, device=self.device)
+        self.Act = torch.empty((NA, R, hp), dtype=torch.bfloat16, device=self.device)
+        self.dH = torch.empty((NA, R, 2 * hp), dtype=torch.bfloat16, device=self.device)
         # ---- per-micro-batch token-side buffers
-        T, k = tokens, shape.top_k
+        T, k, MB = tokens, shape.top_k, micro_batches
         self.perm = torch.empty((MB, T, k, 2), dtype=torch.int32, device=self.device)
         chunks = (T + CHUNK - 1) // CHUNK
         self.counts = torch.empty((MB, E), dtype=torch.int32, device=self.device)
         self.chunk_counts = torch.empty((MB, chunks, E), dtype=torch.int32, device=self.device)
         self.chunk_base = torch.empty((MB, chunks, E), dtype=torch.int32, device=self.device)
-        # peer pointer tables [MB][world]
-        self.ptr_xr = A.peer_table(self.off["xr"], R * h * bf, MB)
-        self.ptr_y = A.peer_table(self.off["y"], R * h * bf, MB)
-        self.ptr_dyr = A.peer_table(self.off["dyr"], R * h * bf, MB)
-        self.ptr_dxp = A.peer_table(self.off["dxp"], R * h * bf, MB)
-        self.ptr_gate = A.peer_table(self.off["gate_r"], R * f4, MB)
-        self.ptr_dgate = A.peer_table(self.off["dgate_r"], R * self.npart * f4, MB)
+        # peer pointer tables [MB][world]: micro-batch m uses buffer set m % NA
+        self.ptr_xr = self._set_table("xr", R * h * bf)
+        self.ptr_y = self._set_table("y", R * h * bf)
+        self.ptr_dyr = self._set_table("dyr", R * h * bf)
+        self.ptr_dxp = self._set_table("dxp", R * h * bf)
+        self.ptr_gate = self._set_table("gate_r", R * f4)
+        self.ptr_dgate = self._set_table("dgate_r", R * self.npart * f4)
+        # host-visible error flag the permutation / count-check kernels OR bits into
+        lib = nat.kernels()
+        hp_, dp_ = ctypes.c_void_p(), ctypes.c_void_p()
+        nat.check(lib.mb_host_alloc_mapped(16, ctypes.byref(hp_), ctypes.byref(dp_)), lib, "mb_host_alloc_mapped")
+        self._err_host, self.err_dev = hp_.value, dp_.value
+        self._err_view = (ctypes.c_int32 * 4).from_address(self._err_host)
         self.xs = torch.cuda.Stream(device=self.device)      # comm stream: dispatch / combine / barriers
-        self.cps = torch.cuda.Stream(device=self.device)     # copy-engine stream: replica pushes
+        self.cps = torch.cuda.Stream(device=self.device)     # copy-engine stream: replica weight pulls
         self.launches = 0
         self.timing = False       # record CUDA events around every K4 launch (bench roofline)
         self.gemm_events = []     # (start, end, algorithmic FLOPs, kind)
         self.load_plan(plan)
+
+    def _set_table(self, key: str, stride: int) -> torch.Tensor:
+        tab = np.array([[self.arena.peer_ptr(p, self.off[key]) + (m % self.NA) * stride for p in range(self.world)]
+                        for m in range(self.MB)], dtype=np.int64)
+        return torch.from_numpy(tab).to(self.device)
+
+    def set_index(self, m: int) -> int:
+        """Receive / activation buffer set of micro-batch m."""
+        return m % self.NA
+
+    def memory_report(self) -> dict:
+        """Device bytes per GPU of the data plane's buffers (both banks of home state counted)."""
+        s = self.sizes
+        act = sum(s[k] for k in ("xr", "y", "dyr", "dxp", "gate_r", "dgate_r"))
+        act += sum(t.numel() * t.element_size() for t in (self.H, self.Act, self.dH))
+        return {"replica_weight_slots": s["w1r"] + s["w2r"], "replica_sets": self.replica_sets,
+                "replica_slots": self.slots, "replica_grad_ring": s["rg1"] + s["rg2"],
+                "activations": act, "activation_sets": self.NA, "wgrad_mode": self.wgrad_mode,
+                "home_weights_and_grads": sum(s[k] for k in ("w1", "w2", "gw1", "gw2", "w1b", "w2b", "gw1b", "gw2b")),
+                "arena_total": self.arena.nbytes}
 
     # ------------------------------------------------------------------ helpers
     def _timed(self, amount: float, kind: str = "gemm", stream=None):
@@ -431,20 +517,79 @@ class MoEDataPlane:
         """Token rows this rank's experts serve in micro-batch m (padding excluded)."""
         return int(self.plan.mbs[m].flow[:, self.rank].sum())
 
+    def errors(self) -> int:
+        """Error bits the kernels reported so far (MB_ERR_*; read without a device sync)."""
+        return int(self._err_view[0])
+
+    def check(self, sync: bool = True) -> None:
+        """Raise if a kernel flagged routing that differs from the step plan (optionally after a
+        device synchronisation, so the last step is included)."""
+        if sync:
+            torch.cuda.synchronize(self.device)
+        bits = self.errors()
+        if bits:
+            self._err_view[0] = 0
+            msgs = [msg for b, msg in ERR_BITS.items() if bits & b]
+            raise RuntimeError("MoE data plane: " + "; ".join(msgs))
+
+    def _check_inputs(self, per_mb: bool, **tensors) -> None:
+        """Validate the step's tensors at the API boundary (dtype, shape, contiguity, device)."""
+        T, k, h, MB = self.T, self.shape.top_k, self.shape.hidden, self.MB
+        lead = () if per_mb else (MB,)
+        spec = {"x": (torch.bfloat16, lead + (T, h)), "dout": (torch.bfloat16, lead + (T, h)),
+                "out": (torch.bfloat16, lead + (T, h)), "dx": (torch.bfloat16, lead + (T, h)),
+                "idx": (torch.int32, lead + (T, k)), "gates": (torch.float32, lead + (T, k)),
+                "dgate": (torch.float32, lead + (T, k))}
+        for name, t in tensors.items():
+            dtype, shp = spec[name]
+            if not isinstance(t, torch.Tensor):
+                raise TypeError(f"{name} must be a torch.Tensor")
+            if t.dtype != dtype:
+                raise ValueError(f"{name} must be {dtype} (got {t.dtype})")
+            if tuple(t.shape) != shp:
+                raise ValueError(f"{name} must have shape {list(shp)} (got {list(t.shape)}); the plane was built "
+                                 f"for T={T}, top_k={k}, hidden={h}, micro_batches={MB}")
+            if not t.is_contiguous():
+                raise ValueError(f"{name} must be contiguous")
+            if t.device != self.device:
+                raise ValueError(f"{name} is on {t.device}, the data plane on {self.device}")
+
     # ------------------------------------------------------------------ plan upload
-    def load_plan(self, plan: StepPlan) -> None:
+    def load_plan(self, plan) -> None:
+        """Install a step plan (a StepPlan, or the PlanTables build_tables made from one)."""
+        tables = plan if isinstance(plan, PlanTables) else self.build_tables(plan)
+        if tables.owner is not self:
+            raise ValueError("these plan tables were built for another data plane")
+        self.plan = tables.plan
+        self.tables = tables
+        for key, val in tables.attrs.items():
+            setattr(self, key, val)
+
+    def build_tables(self, plan: StepPlan) -> "PlanTables":
+        """Every device table of a step plan for this rank (uploaded now, installed by load_plan /
+        migrate): per-micro-batch route / slot / GEMM group tables, the replicas this rank pulls,
+        the weight-gradient tables and the replica-gradient push-back tasks."""
         if plan.rows_cap > self.R:
             raise ValueError(f"plan needs {plan.rows_cap} receive rows per micro-batch, buffers hold {self.R}")
-        if max((len(r) for r in plan.rep_experts), default=0) > self.rep_cap:
-            raise ValueError("plan replicates more experts than the replica gradient buffer holds")
-        self.plan = plan
+        if len(plan.mbs) != self.MB:
+            raise ValueError(f"plan has {len(plan.mbs)} micro-batches, the data plane {self.MB}")
         d, dev = self.rank, self.device
-        E = self.shape.num_experts
-        home = plan.home
-        self.home_experts = np.flatnonzero(home == d)
-        local_of = {int(ex): int(np.flatnonzero(np.flatnonzero(home == home[ex]) == ex)[0]) for ex in range(E)}
-        route, ncop, groups, slots, nsl, pushes = [], [], [], [], [], []
+        E, MB, R = self.shape.num_experts, self.MB, self.R
+        h, hp = self.shape.hidden, self.shape.ffn
+        home = np.asarray(plan.home)
+        home_experts = np.flatnonzero(home == d)
+        nh = len(home_experts)
+        local_of = np.zeros(E, dtype=np.int64)
+        for g in range(self.world):
+            mine = np.flatnonzero(home == g)
+            local_of[mine] = np.arange(len(mine))
+        loc_of_home = {int(ex): i for i, ex in enumerate(home_experts)}
+        route, ncop, groups, slots, nsl = [], [], [], [], []
         max_slots = plan.max_slots
+        mb_rep = []               # per micro-batch: [(slot q, expert, owner rank, owner local index)]
+        rep_rows = []             # per micro-batch: {(holder rank, expert): (slot q, real rows)}
+        home_slots = []           # per micro-batch: {home expert: (row_begin, real rows)} on this rank
+        rep_slots = []            # per micro-batch: {replicated expert: (row_begin, real rows, q)} on this rank
         for m, mbp in enumerate(plan.mbs):
             route.append(mbp.route_tab[d])
             ncop.append(mbp.ncopies)
@@ -463,82 +608,140 @@ class MoEDataPlane:
             groups.append(g)
             slots.append(st)
             nsl.append(n)
-            # replica pushes this rank performs as the owner: (dst gpu, micro-batch, dst slot, local expert)
-            for dst in range(self.world):
-                stt, sww = mbp.slot_tab[dst], mbp.slot_w[dst]
-                for s in range(int(mbp.nslots[dst])):
-                    if sww[s, 1] and home[stt[s, 3]] == d:
-                        pushes.append((dst, m, int(sww[s, 0]), local_of[int(stt[s, 3])]))
-        self.route_tab = torch.from_numpy(np.stack(route)).to(dev)
-        self.ncopies = torch.from_numpy(np.stack(ncop)).to(dev)
-        self.groups = torch.from_numpy(np.stack(groups)).to(dev)
-        self.slot_tab = torch.from_numpy(np.stack(slots)).to(dev)
-        self.nslots = nsl
-        self.pushes = pushes
-        # ---- wgrad groups: home experts (accumulate) then experts replicated onto this rank
-        # K segments = the slot's real rows rounded up to 16 (pad rows are zero in both operands;
-        # the kernel issues K16 MMAs only up to the segment end)
-        wg, segs = [], []
-        R = self.R
-
-        def add_group(ex, replica, out_slot, flags):
-            s0, tot, kb = len(segs), 0, 0
-            for m, mbp in enumerate(plan.mbs):
-                st, sw = mbp.slot_tab[d], mbp.slot_w[d]
-                for s in range(int(mbp.nslots[d])):
-                    if st[s, 3] == ex and sw[s, 1] == replica and st[s, 1] > 0:
-                        r16 = (int(st[s, 1]) + 15) // 16 * 16
-                        segs.append((m * R + int(st[s, 0]), r16))
-                        tot += r16
-                        kb += (r16 + 63) // 64
-            wg.append((tot, 0, out_slot, flags, s0, len(segs) - s0, 0, kb))
-
-        for loc, ex in enumerate(self.home_experts):
-            add_group(ex, 0, loc, K.FLAG_ACCUMULATE)
-        for q, ex in enumerate(plan.rep_experts[d]):
-            add_group(ex, 1, self.M + q, 0)
-        wtab = np.zeros((len(wg), K.GROUP_FIELDS), dtype=np.int32)
-        for i, row in enumerate(wg):
-            wtab[i] = row
-        self.idle_home = [loc for loc, row in enumerate(wg[:len(self.home_experts)]) if row[0] == 0]
-        self.wsegs = torch.from_numpy(np.asarray(segs if segs else [(0, 0)], dtype=np.int32).reshape(-1, 2)).to(dev)
-        # ---- replica gradient reduce lists (this rank as owner): only replicas that served rows
-        rep_rows = {}
-        for mbp in plan.mbs:
+            mb_rep.append([(int(sw[s, 0]), int(st[s, 3]), int(home[st[s, 3]]), int(local_of[st[s, 3]]))
+                           for s in range(n) if sw[s, 1] > 0])
+            home_slots.append({int(st[s, 3]): (int(st[s, 0]), int(st[s, 1])) for s in range(n)
+                               if sw[s, 1] == 0 and st[s, 1] > 0})
+            rep_slots.append({int(st[s, 3]): (int(st[s, 0]), int(st[s, 1]), int(sw[s, 0])) for s in range(n)
+                              if sw[s, 1] > 0 and st[s, 1] > 0})
+            rr = {}
             for p in range(self.world):
                 stt, sww = mbp.slot_tab[p], mbp.slot_w[p]
                 for s in range(int(mbp.nslots[p])):
-                    if sww[s, 1]:
-                        key = (p, int(stt[s, 3]))
-                        rep_rows[key] = rep_rows.get(key, 0) + int(stt[s, 2])
-        mn1 = 2 * self.shape.ffn * self.shape.hidden
-        self.reduce = []
-        for loc, ex in enumerate(self.home_experts):
-            srcs = [(p, plan.rep_experts[p].index(int(ex))) for p in range(self.world)
-                    if p != d and int(ex) in plan.rep_experts[p] and rep_rows.get((p, int(ex)), 0) > 0]
-            if srcs:
-                p1 = [self.arena.peer_ptr(p, self.off_w["gw1"]) + (self.M + q) * mn1 * 4 for p, q in srcs]
-                p2 = [self.arena.peer_ptr(p, self.off_w["gw2"]) + (self.M + q) * (mn1 // 2) * 4 for p, q in srcs]
-                self.reduce.append((loc, torch.tensor(p1, dtype=torch.int64, device=dev),
-                                    torch.tensor(p2, dtype=torch.int64, device=dev), len(srcs)))
-        # wgrad launch split: (A) replica groups + home experts that receive replica gradients,
-        # (B) every other home expert.  The owners' replica-gradient reduce waits only for A, so it
-        # runs beside B instead of after the whole weight-gradient phase.
-        red = {loc for loc, *_ in self.reduce}
-        nh = len(self.home_experts)
-        part_a = [i for i in range(len(wg)) if i >= nh or i in red]
-        part_b = [i for i in range(nh) if i not in red]
-        self.wparts = []
-        for rows_idx in ((part_a, part_b) if self.reduce else (list(range(len(wg))),)):
-            if not rows_idx:
-                self.wparts.append(None)
-                continue
-            tab = wtab[rows_idx]
-            tab_store = tab.copy()
-            tab_store[:, 3] &= ~K.FLAG_ACCUMULATE
-            share = float(tab[:, 0].sum()) / max(1.0, float(wtab[:, 0].sum()))
-            self.wparts.append((torch.from_numpy(np.ascontiguousarray(tab)).to(dev),
-                                torch.from_numpy(np.ascontiguousarray(tab_store)).to(dev), share))
+                    if sww[s, 1] and stt[s, 1] > 0:
+                        rr[(p, int(stt[s, 3]))] = (int(sww[s, 0]), int(stt[s, 1]))
+            rep_rows.append(rr)
+        at = {"home_experts": home_experts, "mb_rep": mb_rep, "nslots": nsl,
+              "route_tab": torch.from_numpy(np.stack(route)).to(dev),
+              "ncopies": torch.from_numpy(np.stack(ncop)).to(dev),
+              "groups": torch.from_numpy(np.stack(groups)).to(dev),
+              "slot_tab": torch.from_numpy(np.stack(slots)).to(dev),
+              "expected": (torch.from_numpy(np.ascontiguousarray(plan.mats[:, d], dtype=np.int32)).to(dev)
+                           if plan.mats is not None else None)}
+
+        # ---- weight-gradient tables.  Contribution order per home expert (fresh step: the first
+        # contribution stores, the rest accumulate): step mode X(0) .. X(MB-1) then the home wgrad;
+        # micro-batch mode W(0) X(0) W(1) X(1) ...  (X = replica-gradient push-back)
+        def r16(rows):
+            return (rows + 15) // 16 * 16
+
+        def group_row(segs, seg_rows, out_slot, flags):
+            s0 = len(segs)
+            segs.extend(seg_rows)
+            tot = sum(r for _, r in seg_rows)
+            kb = sum((r + 63) // 64 for _, r in seg_rows)
+            return (tot, 0, out_slot, flags, s0, len(seg_rows), 0, kb)
+
+        def seg_tensor(segs):
+            return torch.from_numpy(np.asarray(segs if segs else [(0, 0)], dtype=np.int32).reshape(-1, 2)).to(dev)
+
+        written = [False] * nh           # fresh step: has the expert's gradient been written yet
+        replica_contrib = set()          # home local indices with replica gradients this step
+        srcs_of = []                     # per m: {loc: [(holder, q)]}
+        for m in range(MB):
+            sm = {}
+            for (p, ex), (q, _) in rep_rows[m].items():
+                if p != d and int(home[ex]) == d:
+                    sm.setdefault(loc_of_home[ex], []).append((p, q))
+            for loc in sm:
+                sm[loc].sort()
+                if len(sm[loc]) > 8:
+                    raise ValueError("more than 8 replicas of one expert in a micro-batch")
+                replica_contrib.add(loc)
+            srcs_of.append(sm)
+        w_mb, rw_mb, acc_mb = [None] * MB, [None] * MB, [None] * MB
+        nfl = {"rg1": 2 * hp * h, "rg2": h * hp}
+        for m in range(MB):
+            # replica wgrad of micro-batch m on this rank: store into ring set m % GRAD_RING
+            segs, rows, a_rows = [], [], 0
+            for ex, (r0, real, q) in sorted(rep_slots[m].items()):
+                rows.append(group_row(segs, [(r0, r16(real))], q, 0))
+                a_rows += real
+            if rows:
+                rw_mb[m] = (torch.from_numpy(_wgrad_table(rows)).to(dev), seg_tensor(segs), a_rows)
+            if self.wgrad_mode == "micro_batch":
+                segs, rows_f, real = [], [], 0
+                for ex, (r0, rr_) in sorted(home_slots[m].items()):
+                    loc = loc_of_home[ex]
+                    rows_f.append(group_row(segs, [(r0, r16(rr_))], loc, K.FLAG_ACCUMULATE if written[loc] else 0))
+                    written[loc] = True
+                    real += rr_
+                if rows_f:
+                    tab_f = _wgrad_table(rows_f)
+                    tab_a = tab_f.copy()
+                    tab_a[:, 3] |= K.FLAG_ACCUMULATE   # an accumulating step adds every contribution
+                    w_mb[m] = (torch.from_numpy(tab_f).to(dev), torch.from_numpy(tab_a).to(dev), seg_tensor(segs),
+                               real)
+            # owner push-back tasks of micro-batch m (fresh variant: first contribution stores)
+            if srcs_of[m]:
+                tasks = np.zeros(2 * len(srcs_of[m]), dtype=ACC_TASK)
+                dst_other = np.zeros(2 * len(srcs_of[m]), dtype=np.uint64)   # the same in the other bank
+                i = 0
+                for loc in sorted(srcs_of[m]):
+                    for key, gkey, size in (("rg1", "gw1", self.g1_bytes), ("rg2", "gw2", self.g2_bytes)):
+                        tasks[i]["dst"] = self.arena.peer_ptr(d, self.off[gkey]) + loc * size
+                        dst_other[i] = self.arena.peer_ptr(d, self.off[gkey + "b"]) + loc * size
+                        for j, (p, q) in enumerate(srcs_of[m][loc]):
+                            tasks[i]["src"][j] = (self.arena.peer_ptr(p, self.off[key])
+                                                  + ((m % GRAD_RING) * self.slots + q) * size)
+                        tasks[i]["n"], tasks[i]["nsrc"] = nfl[key], len(srcs_of[m][loc])
+                        tasks[i]["store"] = 0 if written[loc] else 1
+                        i += 1
+                    written[loc] = True
+                variants = []
+                for bank in (0, 1):           # per gradient bank: (fresh, accumulating) task tables
+                    tb = tasks.copy()
+                    if bank:
+                        tb["dst"] = dst_other
+                    ta = tb.copy()
+                    ta["store"] = 0
+                    variants.append((torch.from_numpy(tb.view(np.uint8).copy()).to(dev),
+                                     torch.from_numpy(ta.view(np.uint8).copy()).to(dev)))
+                acc_mb[m] = (variants, len(tasks), int(tasks["n"].max()))
+        at.update(w_mb=w_mb, rw_mb=rw_mb, acc_mb=acc_mb, replica_contrib=replica_contrib)
+        # ---- step mode home wgrad: K contracted over every micro-batch; part B = experts without
+        # replica gradients (runs right after the last backward), part A = the rest (after the last
+        # push-back, accumulating onto it)
+        wparts, idle_home = [], []
+        if self.wgrad_mode == "step":
+            segs, rows_a, rows_b = [], [], []
+            for loc, ex in enumerate(home_experts):
+                ex = int(ex)
+                sr = [(self.set_index(m) * R + home_slots[m][ex][0], r16(home_slots[m][ex][1]))
+                      for m in range(MB) if ex in home_slots[m]]
+                if not sr:
+                    if loc not in replica_contrib:
+                        idle_home.append(loc)
+                    continue
+                real = sum(home_slots[m][ex][1] for m in range(MB) if ex in home_slots[m])
+                (rows_a if loc in replica_contrib else rows_b).append((group_row(segs, sr, loc, 0), real))
+            segs_t = seg_tensor(segs)
+            for part_rows, part in ((rows_b, "B"), (rows_a, "A")):
+                if not part_rows:
+                    wparts.append(None)
+                    continue
+                tab = _wgrad_table([r for r, _ in part_rows])
+                tab_fresh, tab_acc = tab.copy(), tab.copy()
+                tab_acc[:, 3] |= K.FLAG_ACCUMULATE
+                if part == "A":      # replica gradients were pushed back first: always accumulate
+                    tab_fresh[:, 3] |= K.FLAG_ACCUMULATE
+                wparts.append((torch.from_numpy(tab_fresh).to(dev), torch.from_numpy(tab_acc).to(dev), segs_t,
+                               float(sum(r for _, r in part_rows)), part))
+        else:
+            idle_home = [loc for loc in range(nh) if not written[loc]]
+        at.update(wparts=wparts, idle_home=idle_home)
+        return PlanTables(self, plan, at)
+
 
     # ------------------------------------------------------------------ weights
     def _bind_bank(self) -> None:
@@ -548,32 +751,35 @@ class MoEDataPlane:
         self.off_w = {k: self.off[k + sfx] for k in ("w1", "w2", "gw1", "gw2")}
         self.W1 = A.local(self.off_w["w1"], (self.M, 2 * hp, h), torch.bfloat16)
         self.W2 = A.local(self.off_w["w2"], (self.M, h, hp), torch.bfloat16)
-        self.gW1 = A.local(self.off_w["gw1"], (self.S, 2 * hp, h), torch.float32)
-        self.gW2 = A.local(self.off_w["gw2"], (self.S, h, hp), torch.float32)
+        self.gW1 = A.local(self.off_w["gw1"], (self.M, 2 * hp, h), torch.float32)
+        self.gW2 = A.local(self.off_w["gw2"], (self.M, h, hp), torch.float32)
         self.state = {}
         for name, (eshape, dtype, _) in self.state_spec.items():
             off = self.off["st_" + name + sfx]
             self.off_w["st_" + name] = off
             self.state[name] = A.local(off, (self.M, *eshape), dtype)
 
-    def migrate(self, plan: StepPlan, grads: bool = True) -> dict:
+    def migrate(self, plan, grads: bool = True) -> dict:
         """Switch to a step plan with a different reorder assignment (expert migration at a batch
         boundary): every rank pulls its new home experts' weights, fp32
         gradients and expert state from their old owners (copy engine over NVLink, or a local
         copy) into its idle bank, then all ranks swap banks and upload the new plan.  Collective:
         every rank calls it with the same plan.  grads=False skips the fp32 gradients (migration
         right after an optimizer step, when they are zero: the new bank's are zeroed instead).
-        Returns {experts_moved, bytes_in}."""
-        old_home, new_home = np.asarray(self.plan.home), np.asarray(plan.home)
+        `plan` is a StepPlan or its prebuilt PlanTables.  Returns {experts_moved, bytes_in}."""
+        tables = plan if isinstance(plan, PlanTables) else self.build_tables(plan)
+        old_home, new_home = np.asarray(self.plan.home), np.asarray(tables.plan.home)
+        if np.array_equal(old_home, new_home):      # same assignment: nothing moves
+            self.load_plan(tables)
+            return {"experts_moved": 0, "bytes_in": 0}
         moves = migration_moves(old_home, new_home, self.world)[self.rank]
         cur = torch.cuda.current_stream()
         cps, A, lib = self.cps, self.arena, nat.kernels()
         sfx_new = "" if self.bank else "b"
-        hp, h = self.shape.ffn, self.shape.hidden
         items = [("w1", self.w1_bytes), ("w2", self.w2_bytes)]
         grads = grads and not getattr(self, "grads_pending_zero", False)
         if grads:
-            items += [("gw1", 2 * hp * h * 4), ("gw2", h * hp * 4)]
+            items += [("gw1", self.g1_bytes), ("gw2", self.g2_bytes)]
         items += [("st_" + n, spec[2]) for n, spec in self.state_spec.items()]
         cps.wait_stream(cur)
         A.barrier(cps)  # every rank finished its last step: the current banks are stable
@@ -593,7 +799,7 @@ class MoEDataPlane:
         self._bind_bank()
         if not grads:
             self.zero_grads(lazy=True)
-        self.load_plan(plan)
+        self.load_plan(tables)
         return {"experts_moved": moved, "bytes_in": nbytes}
 
     def set_weights(self, w_gate: torch.Tensor, w_up: torch.Tensor, w_down: torch.Tensor) -> None:
@@ -602,10 +808,10 @@ class MoEDataPlane:
         self.W2.copy_(w_down)
 
     def zero_grads(self, lazy: bool = True) -> None:
-        """Reset the fp32 expert gradients.  lazy (default): no memset; the next step's weight-
-        gradient GEMM stores instead of accumulating (0 + x == x exactly), as a trainer's
-        zero_grad() before backward would have it.  Read gradients through grads() to see the
-        zeros before that step."""
+        """Reset the fp32 expert gradients.  lazy (default): no memset; the next step's first
+        gradient contribution to each expert stores instead of accumulating (0 + x == x exactly),
+        as a trainer's zero_grad() before backward would have it.  Read gradients through grads()
+        to see the zeros before that step."""
         if lazy:
             self.grads_pending_zero = True
         else:
@@ -627,6 +833,10 @@ class MoEDataPlane:
         nat.check(getattr(lib, name)(*args), lib, name)
         self.launches += 1
 
+    def _gemm(self, *args, sms=None, **kw):
+        K.grouped_gemm(*args, sms=self.gemm_sms if sms is None else sms, **kw)
+        self.launches += 1
+
     def forward_backward(self, x: torch.Tensor, idx: torch.Tensor, gates: torch.Tensor, dout: torch.Tensor,
                          out: torch.Tensor, dx: torch.Tensor, dgate: torch.Tensor, hooks=None) -> None:
         """One training step of the layer over MB micro-batches (inputs [MB, T, ...] on device).
@@ -636,14 +846,18 @@ class MoEDataPlane:
         after_forward(m, stream), after_backward(m, stream).
         Runs the two-micro-batch-overlap schedule (schedule()); the same phases are available one
         micro-batch at a time through begin_step / forward_mb / backward_mb / end_step."""
+        self._check_inputs(False, x=x, idx=idx, gates=gates, dout=dout, out=out, dx=dx, dgate=dgate)
+        self.check(sync=False)
         ops = _StepOps(self, hooks)
         comm_fn = {"D": lambda m: ops.dispatch(m, x[m], idx[m], gates[m], idx, gates),
                    "C": lambda m: (ops.combine(m, gates[m], out[m]), ops.dout_dispatch(m, dout[m])),
                    "X": lambda m: ops.unpermute(m, dx[m], dgate[m])}
-        comp_fn = {"F": ops.fwd_gemms, "B": ops.bwd_gemms}
-        comm_needs = {"C": "F", "X": "B"}   # comm op waits for this compute op of the same micro-batch
-        comp_needs = {"F": "D", "B": "C"}
-        comm_ops, comp_ops = schedule(self.MB)
+        comp_fn = {"F": ops.fwd_gemms, "B": ops.bwd_gemms, "W": ops.wgrad_mb}
+        per_mb = self.wgrad_mode == "micro_batch"
+        # comm op waits for this compute op of the same micro-batch; compute op for this comm op
+        comm_needs = {"C": ("F", 0), "X": ("W" if per_mb else "B", 0)}
+        comp_needs = {"F": ("D", 0), "B": ("C", 0), "W": ("X", -1)}
+        comm_ops, comp_ops = schedule(self.MB, self.wgrad_mode)
         ev_comm, ev_comp = {}, {}
         cs, xs = ops.cs, ops.xs
         ci = pi = 0
@@ -652,7 +866,7 @@ class MoEDataPlane:
         while ci < len(comm_ops) or pi < len(comp_ops):
             if ci < len(comm_ops):
                 cop, cm = comm_ops[ci]
-                dep = (comm_needs[cop], cm) if cop in comm_needs else None
+                dep = (comm_needs[cop][0], cm + comm_needs[cop][1]) if cop in comm_needs else None
                 if dep is None or dep in ev_comp:
                     if dep is not None:
                         xs.wait_event(ev_comp[dep])
@@ -662,21 +876,26 @@ class MoEDataPlane:
                     ci += 1
                     continue
             op, m = comp_ops[pi]
-            dep = (comp_needs[op], m)
-            if dep not in ev_comm:
-                raise RuntimeError(f"step schedule deadlock at {op}{m}")
-            cs.wait_event(ev_comm[dep])
+            dep = (comp_needs[op][0], m + comp_needs[op][1])
+            if dep[1] >= 0:
+                if dep not in ev_comm:
+                    raise RuntimeError(f"step schedule deadlock at {op}{m}")
+                cs.wait_event(ev_comm[dep])
             comp_fn[op](m)
             ev_comp[(op, m)] = torch.cuda.Event()
             ev_comp[(op, m)].record(cs)
             pi += 1
-        ops.finish()
+        ops.finish(ev_comm.get(("X", self.MB - 1)))
 
     # ------------------------------------------------------------------ per-micro-batch API
     def begin_step(self) -> None:
-        """Open a step for the per-micro-batch API: replica pushes of every micro-batch start."""
+        """Open a step for the per-micro-batch API."""
         if getattr(self, "_ops", None) is not None:
             raise RuntimeError("begin_step called twice without end_step")
+        if self.wgrad_mode != "step":
+            raise RuntimeError("the per-micro-batch API needs wgrad_mode='step' (its backward order is free, so "
+                               "every micro-batch's activations stay resident)")
+        self.check(sync=False)
         self._ops = _StepOps(self, None)
 
     def forward_mb(self, m: int, x: torch.Tensor, idx: torch.Tensor, gates: torch.Tensor,
@@ -684,6 +903,7 @@ class MoEDataPlane:
         """Forward of micro-batch m: dispatch, expert FFN, gate-weighted combine into out [T, h].
         Ordered after the current stream's work; the current stream waits for out."""
         ops = self._require_step()
+        self._check_inputs(True, x=x, idx=idx, gates=gates, out=out)
         ops.xs.wait_stream(ops.cs)
         ops.dispatch(m, x, idx, gates)
         ops.cs.wait_stream(ops.xs)
@@ -694,9 +914,11 @@ class MoEDataPlane:
 
     def backward_mb(self, m: int, dout: torch.Tensor, dx: torch.Tensor, dgate: torch.Tensor) -> None:
         """Backward of micro-batch m (after its forward_mb): dout dispatch, dAct with the fused
-        combine backward, dX, un-permute into dx [T, h] and dgate [T, k].  Weight gradients are
-        contracted over every micro-batch in end_step."""
+        combine backward, dX, replica weight gradients (pushed back to their owners), un-permute
+        into dx [T, h] and dgate [T, k].  Home weight gradients are contracted over every
+        micro-batch in end_step."""
         ops = self._require_step()
+        self._check_inputs(True, dout=dout, dx=dx, dgate=dgate)
         ops.xs.wait_stream(ops.cs)
         ops.dout_dispatch(m, dout)
         ops.cs.wait_stream(ops.xs)
@@ -706,9 +928,9 @@ class MoEDataPlane:
         ops.cs.wait_stream(ops.xs)
 
     def end_step(self) -> None:
-        """Weight gradients over the step's micro-batches and the replica-gradient reduce."""
+        """Home weight gradients over the step's micro-batches."""
         ops = self._require_step()
-        ops.finish()
+        ops.finish(None)
         self._ops = None
 
     def _require_step(self):
@@ -718,30 +940,15 @@ class MoEDataPlane:
         return ops
 
     def _wgrad_prepare(self) -> bool:
-        """Lazy zero_grads: zero the home slots no wgrad tile will write, report store mode."""
+        """Lazy zero_grads: zero the home experts no gradient contribution will write, report
+        whether this step's first contributions store (fresh) or accumulate."""
         fresh = getattr(self, "grads_pending_zero", False)
         if fresh:
-            for loc in self.idle_home:  # home experts without rows this step get no wgrad tile
+            for loc in self.idle_home:
                 self.gW1[loc].zero_()
                 self.gW2[loc].zero_()
             self.grads_pending_zero = False
         return fresh
-
-    def _wgrad(self, part, fresh: bool):
-        h, hp = self.shape.hidden, self.shape.ffn
-        R, MB = self.R, self.MB
-        if part is None:
-            return
-        tab, tab_store, share = part
-        rows = share * sum(self.real_rows(m) for m in range(MB))
-        wgroups = tab_store if fresh else tab
-        with self._timed(2.0 * rows * h * hp, "wgrad_down"):
-            K.grouped_gemm(K.GEMM_WGRAD, self.dYr.view(MB * R, h), self.Act.view(MB * R, hp), wgroups, M=h, N=hp,
-                           C=self.gW2, c_slot_stride=h * hp, segs=self.wsegs)
-        with self._timed(4.0 * rows * h * hp, "wgrad_gate_up"):
-            K.grouped_gemm(K.GEMM_WGRAD, self.dH.view(MB * R, 2 * hp), self.Xr.view(MB * R, h), wgroups,
-                           M=2 * hp, N=h, C=self.gW1, c_slot_stride=2 * hp * h, segs=self.wsegs)
-        self.launches += 2
 
     step = forward_backward
 
@@ -749,7 +956,13 @@ class MoEDataPlane:
         """The user-facing step with HOST (pinned) tensors: micro-batch inputs are copied
         host->device on a copy stream while earlier micro-batches run, and out/dx/dgate are copied
         device->host as soon as they exist.  `dev` holds device staging tensors of the same
-        shapes.  Synchronous: returns with the results on the host."""
+        shapes.  Synchronous: returns with the results on the host (raises if a kernel flagged
+        routing that differs from the plan)."""
+        for key in ("x", "idx", "gates", "dout", "out", "dx", "dgate"):
+            if host[key].device.type != "cpu" or not host[key].is_pinned():
+                raise ValueError(f"host[{key!r}] must be a pinned CPU tensor")
+            if host[key].shape != dev[key].shape or host[key].dtype != dev[key].dtype:
+                raise ValueError(f"host[{key!r}] and dev[{key!r}] differ in shape or dtype")
         cur = torch.cuda.current_stream()
         if not hasattr(self, "_h2d"):
             self._h2d = torch.cuda.Stream(device=self.device)
@@ -826,10 +1039,14 @@ class MoEDataPlane:
                               hooks=_Hooks())
         cur.wait_stream(d2h)
         cur.synchronize()
+        self.check(sync=False)
 
     def close(self) -> None:
         torch.cuda.synchronize(self.device)
         self.arena.close()
+        if self._err_host:
+            nat.kernels().mb_host_free(self._err_host)
+            self._err_host = 0
 
 
 def _token_parts(T: int, parts: int):
@@ -839,9 +1056,10 @@ def _token_parts(T: int, parts: int):
 
 
 class _StepOps:
-    """The phases of one step of a MoEDataPlane on its two streams (compute: K4 GEMMs; comm:
-    histogram / permutation / scatter / combine and every device barrier).  Every rank must call
-    the phases in the same order: each comm phase contains collective device barriers."""
+    """The phases of one step of a MoEDataPlane on its streams (compute: K4 GEMMs; comm:
+    histogram / permutation / scatter / combine / replica-gradient push-back and every device
+    barrier; copy: replica weight pulls).  Every rank must call the phases in the same order:
+    each comm phase contains collective device barriers."""
 
     def __init__(self, dp: "MoEDataPlane", hooks=None):
         self.dp, self.hooks = dp, hooks
@@ -849,50 +1067,79 @@ class _StepOps:
         self.xs = dp.xs if dp.overlap else self.cs
         self.st_x = self.xs.cuda_stream
         self.xs.wait_stream(self.cs)
-        self.push_ev = {}
-        cps = dp.cps
-        # K5 replica pushes (copy engine), in micro-batch order; dispatch(m) waits for micro-batch
-        # m's pushes before its final barrier, so the first GEMMs need not wait for the whole
-        # step's replica weights.  Only micro-batch 0's are enqueued here; the rest go right after
-        # D(0) is enqueued, so the host does not delay the first dispatch.
-        self.push_groups = {}
-        for p in dp.pushes:
-            self.push_groups.setdefault(p[1], []).append(p)
-        self._push_order = sorted(self.push_groups)
-        self._push_timer = None
-        if dp.pushes:
-            cps.wait_stream(self.cs)
-            self._push_timer = dp._timed(len(dp.pushes) * (dp.w1_bytes + dp.w2_bytes), "comm_replica_push", cps)
-            self._push_timer.__enter__()
-            self._issue_pushes(0)
+        dp.cps.wait_stream(self.cs)
         self.first = True
+        self.start_ev = None
         self.prepared = set()
+        self.fresh = dp._wgrad_prepare()
+        # layer-shared replica weight slots: per kind ("w1" / "w2") and set, the micro-batch held,
+        # the event after its last use and after its pull; micro-batches whose backward is issued
+        n = dp.replica_sets
+        self.rep = {kd: {"held": [None] * n, "used": [None] * n, "pulled": [None] * n, "seq": [0] * n}
+                    for kd in ("w1", "w2")}
+        self.rep_done = set()
+        self.seq = 0
+        self.x_ev = {}
 
-    def _issue_pushes(self, upto=None):
-        """Enqueue the replica pushes of micro-batches <= upto (all when None) not issued yet."""
-        dp, A, cps = self.dp, self.dp.arena, self.dp.cps
-        lib = nat.kernels()
-        while self._push_order and (upto is None or self._push_order[0] <= upto):
-            m = self._push_order.pop(0)
-            for dst, _, slot, loc in self.push_groups[m]:
-                d1 = A.peer_ptr(dst, dp.off["w1r"]) + (m * dp.slots + slot) * dp.w1_bytes
-                d2 = A.peer_ptr(dst, dp.off["w2r"]) + (m * dp.slots + slot) * dp.w2_bytes
-                nat.check(lib.mb_memcpy_async(d1, dp.W1[loc].data_ptr(), dp.w1_bytes, cps.cuda_stream), lib,
-                          "replica push")
-                nat.check(lib.mb_memcpy_async(d2, dp.W2[loc].data_ptr(), dp.w2_bytes, cps.cuda_stream), lib,
-                          "replica push")
-            self.push_ev[m] = torch.cuda.Event()
-            self.push_ev[m].record(cps)
-        if not self._push_order and self._push_timer is not None:
-            self._push_timer.__exit__(None, None, None)
-            self._push_timer = None
+    # -------------------------------------------------------------- replica weights (K5)
+    def _replica_set(self, kind: str, m: int) -> int:
+        """Set of `kind` replica slots holding micro-batch m's replica weights: pulled by this rank
+        from the owners over NVLink (copy engine) into the least useful set, after that set's last
+        use; the compute stream waits for the pull."""
+        dp, st = self.dp, self.rep[kind]
+        need = dp.mb_rep[m]
+        if not need:
+            return 0
+        if m in st["held"]:
+            i = st["held"].index(m)
+        else:
+            cand = list(range(dp.replica_sets))
+            free = [i for i in cand if st["held"][i] is None or st["held"][i] in self.rep_done]
+            pool = free if free else cand
+            i = min(pool, key=lambda j: st["seq"][j])
+            cps, A, lib = dp.cps, dp.arena, nat.kernels()
+            if st["used"][i] is not None:
+                cps.wait_event(st["used"][i])
+            if self.start_ev is not None:
+                cps.wait_event(self.start_ev)
+            size = dp.w1_bytes if kind == "w1" else dp.w2_bytes
+            base = dp.off["w1r" if kind == "w1" else "w2r"] + i * dp.slots * size
+            with dp._timed(len(need) * size, "comm_replica_pull", cps):
+                for q, _, owner, loc in need:
+                    src = A.peer_ptr(owner, dp.off_w[kind]) + loc * size
+                    nat.check(lib.mb_memcpy_async(A.peer_ptr(dp.rank, base) + q * size, src, size, cps.cuda_stream),
+                              lib, "replica pull")
+            ev = torch.cuda.Event()
+            ev.record(cps)
+            st["pulled"][i] = ev
+            st["held"][i] = m
+        self.cs.wait_event(st["pulled"][i])
+        return i
+
+    def _replica_used(self, kind: str, i: int, m: int) -> None:
+        if not self.dp.mb_rep[m]:
+            return
+        st = self.rep[kind]
+        ev = torch.cuda.Event()
+        ev.record(self.cs)
+        st["used"][i] = ev
+        self.seq += 1
+        st["seq"][i] = self.seq
 
     # -------------------------------------------------------------- comm stream
-    def prepare(self, m0, m1, idx, gates):
-        """Routing side of micro-batches [m0, m1) in one launch per kernel: K1 histogram, chunk
-        scan, pad-row zeroing, K2 stable ranks (+ gates into the serving ranks' receive slots).
-        idx / gates are the [MB, T, k] step tensors (routing is replayed, so every micro-batch's
-        permutation can be built before its rows move)."""
+    def _first_barrier(self):
+        if self.first:
+            self.dp.arena.barrier(self.xs)  # all ranks: previous step drained (buffers may be rewritten)
+            self.start_ev = torch.cuda.Event()
+            self.start_ev.record(self.xs)
+            self.first = False
+
+    def prepare(self, m0, m1, idx, gates, rows=True):
+        """Routing side of micro-batches [m0, m1) in one launch per kernel: K1 histogram (+ the
+        check against the plan's counts), chunk scan, and (rows) pad-row zeroing and K2 stable
+        ranks (+ gates into the serving ranks' receive slots).  idx / gates are the [MB, T, k]
+        step tensors (routing is replayed, so every micro-batch's permutation can be built before
+        its rows move)."""
         dp, xs, st = self.dp, self.xs, self.st_x
         sh = dp.shape
         T, k, h, E = dp.T, sh.top_k, sh.hidden, sh.num_experts
@@ -903,62 +1150,67 @@ class _StepOps:
             self.hooks.routing_ready(xs)
         dp._k("mb_expert_histogram", idx[m0].data_ptr(), nb, T, k, E, dp.counts[m0].data_ptr(),
               dp.chunk_counts[m0].data_ptr(), CHUNK, st)
+        if dp.expected is not None:
+            dp._k("mb_check_counts", dp.counts[m0].data_ptr(), dp.expected[m0].data_ptr(), nb * E, dp.err_dev,
+                  2, st)
         dp._k("mb_chunk_scan", dp.chunk_counts[m0].data_ptr(), dp.chunk_base[m0].data_ptr(), nb,
               (T + CHUNK - 1) // CHUNK, E, st)
-        dp._k("mb_zero_pad_rows_nb", dp.Xr[m0].data_ptr(), dp.R, dp.slot_tab[m0].data_ptr(), dp.plan.max_slots, nb,
-              h, st)
-        if self.first:
-            dp.arena.barrier(xs)  # all ranks: previous step drained (receive gates may be rewritten)
-            self.first = False
+        if not rows:
+            return
+        dp._k("mb_zero_pad_rows_nb", dp.Xr[dp.set_index(m0)].data_ptr(), dp.R, dp.slot_tab[m0].data_ptr(),
+              dp.plan.max_slots, nb, h, st)
+        self._first_barrier()
         dp._k("mb_permute_rank_nb", idx[m0].data_ptr(), T, k, gates[m0].data_ptr(), E, dp.chunk_base[m0].data_ptr(),
               CHUNK, dp.route_tab[m0].data_ptr(), dp.ncopies[m0].data_ptr(), dp.plan.maxc,
-              dp.ptr_gate[m0].data_ptr(), dp.world, dp.perm[m0].data_ptr(), nb, st)
+              dp.ptr_gate[m0].data_ptr(), dp.world, dp.perm[m0].data_ptr(), nb, dp.err_dev, st)
         self.prepared.update(range(m0, m1))
 
     def dispatch(self, m, x, idx, gates, idx_all=None, gates_all=None):
         """D(m): routing side of m (unless prepared), K3 scatter into every rank's receive rows.
         With the step's [MB, ...] routing tensors (idx_all / gates_all), D(0) also prepares
-        micro-batches 1..MB-1 in one batch once its rows have landed."""
+        micro-batches 1..MB-1 once its rows have landed (wgrad_mode "step"; with the micro-batch
+        buffer ring only their histograms: rows and gates of a set are written at its own D)."""
         dp, xs, st = self.dp, self.xs, self.st_x
         sh = dp.shape
         T, k, h = dp.T, sh.top_k, sh.hidden
+        ring = dp.NA < dp.MB
         with dp._timed(dp.remote_rows(m)[0] * 2 * h, "comm_dispatch", xs):
             if m not in self.prepared:
-                self._prepare_one(m, idx, gates)
+                if ring and idx_all is not None and m == 0:
+                    self.prepare(0, dp.MB, idx_all, gates_all, rows=False)
+                self._prepare_one(m, idx, gates, histogram=not (ring and idx_all is not None))
             # the host-buffer step lands micro-batch 0's rows in parts: scatter each as it arrives
             parts = self.hooks.input_parts(m) if self.hooks and hasattr(self.hooks, "input_parts") else 1
             for p, (t0, t1) in enumerate(_token_parts(T, parts)):
                 if self.hooks:
                     self.hooks.inputs_ready(m, xs, p)
                 dp._k("mb_scatter_rows", x[t0:].data_ptr(), t1 - t0, k, h, dp.perm[m][t0:].data_ptr(),
-                      dp.ptr_xr[m].data_ptr(), st)
-            self._issue_pushes(m if idx_all is None else None)
-            if m in self.push_ev:
-                xs.wait_event(self.push_ev[m])  # this rank's replica pushes for micro-batch m
-            dp.arena.barrier(xs)  # rows and replica weights of micro-batch m have landed everywhere
-        if idx_all is not None and m == 0:
+                      dp.ptr_xr[m].data_ptr(), dp.comm_blocks, st)
+            dp.arena.barrier(xs)  # rows of micro-batch m have landed everywhere
+        if idx_all is not None and m == 0 and not ring:
             # after D(0)'s barrier, beside F(0): only pad rows (disjoint from the real rows peers
             # may already be storing) and this rank's own tables / receive gates are written
             self.prepare(1, dp.MB, idx_all, gates_all)
 
-    def _prepare_one(self, m, idx, gates):
-        """Routing side of micro-batch m from its own [T, k] tensors (per-micro-batch API)."""
+    def _prepare_one(self, m, idx, gates, histogram=True):
+        """Routing side of micro-batch m from its own [T, k] tensors."""
         dp, xs, st = self.dp, self.xs, self.st_x
         sh = dp.shape
         T, k, h, E = dp.T, sh.top_k, sh.hidden, sh.num_experts
-        if self.hooks and hasattr(self.hooks, "routing_ready"):
-            self.hooks.routing_ready(xs)
-        dp._k("mb_expert_histogram", idx.data_ptr(), 1, T, k, E, dp.counts[m].data_ptr(),
-              dp.chunk_counts[m].data_ptr(), CHUNK, st)
-        dp._k("mb_chunk_scan", dp.chunk_counts[m].data_ptr(), dp.chunk_base[m].data_ptr(), 1,
-              (T + CHUNK - 1) // CHUNK, E, st)
-        dp._k("mb_zero_pad_rows", dp.Xr[m].data_ptr(), dp.slot_tab[m].data_ptr(), dp.nslots[m], h, st)
-        if self.first:
-            dp.arena.barrier(xs)  # all ranks: previous step drained
-            self.first = False
+        if histogram:
+            if self.hooks and hasattr(self.hooks, "routing_ready"):
+                self.hooks.routing_ready(xs)
+            dp._k("mb_expert_histogram", idx.data_ptr(), 1, T, k, E, dp.counts[m].data_ptr(),
+                  dp.chunk_counts[m].data_ptr(), CHUNK, st)
+            if dp.expected is not None:
+                dp._k("mb_check_counts", dp.counts[m].data_ptr(), dp.expected[m].data_ptr(), E, dp.err_dev, 2, st)
+            dp._k("mb_chunk_scan", dp.chunk_counts[m].data_ptr(), dp.chunk_base[m].data_ptr(), 1,
+                  (T + CHUNK - 1) // CHUNK, E, st)
+        self._first_barrier()
+        dp._k("mb_zero_pad_rows", dp.Xr[dp.set_index(m)].data_ptr(), dp.slot_tab[m].data_ptr(), dp.nslots[m], h, st)
         dp._k("mb_permute_rank", idx.data_ptr(), T, k, gates.data_ptr(), E, dp.chunk_base[m].data_ptr(), CHUNK,
               dp.route_tab[m].data_ptr(), dp.ncopies[m].data_ptr(), dp.plan.maxc, dp.ptr_gate[m].data_ptr(),
-              dp.perm[m].data_ptr(), st)
+              dp.perm[m].data_ptr(), dp.err_dev, st)
         self.prepared.add(m)
 
     def combine(self, m, gates, out):
@@ -968,7 +1220,7 @@ class _StepOps:
         with dp._timed(dp.remote_rows(m)[0] * 2 * h, "comm_combine", xs):
             dp.arena.barrier(xs)  # Y of micro-batch m complete on every rank
             dp._k("mb_combine_rows", dp.ptr_y[m].data_ptr(), dp.perm[m].data_ptr(), gates.data_ptr(), dp.T,
-                  dp.shape.top_k, h, out.data_ptr(), None, None, 1, self.st_x)
+                  dp.shape.top_k, h, out.data_ptr(), None, None, 1, dp.comm_blocks, self.st_x)
             if self.hooks:
                 self.hooks.after_forward(m, xs)
 
@@ -980,23 +1232,31 @@ class _StepOps:
             if self.hooks and hasattr(self.hooks, "dout_ready"):
                 self.hooks.dout_ready(m, xs)
             dp._k("mb_scatter_rows", dout.data_ptr(), dp.T, dp.shape.top_k, h, dp.perm[m].data_ptr(),
-                  dp.ptr_dyr[m].data_ptr(), self.st_x)
+                  dp.ptr_dyr[m].data_ptr(), dp.comm_blocks, self.st_x)
             dp.arena.barrier(xs)  # dout rows of micro-batch m have landed everywhere
 
     def unpermute(self, m, dx, dgate):
-        """X(m): dX un-permute (sum over the k copies) + dgate gather."""
+        """X(m): dX un-permute (sum over the k copies) + dgate gather, then (owners) the replica
+        gradients of micro-batch m pushed back into the home experts' fp32 gradients."""
         dp, xs = self.dp, self.xs
         h = dp.shape.hidden
         with dp._timed(dp.remote_rows(m)[0] * 2 * h, "comm_unpermute", xs):
-            dp.arena.barrier(xs)  # dX rows / dgate partials of micro-batch m complete everywhere
+            dp.arena.barrier(xs)  # dX rows / dgate partials / replica gradients of m complete everywhere
             # the host-buffer step reads the last micro-batch's dx back in parts, each as it is done
             parts = self.hooks.output_parts(m) if self.hooks and hasattr(self.hooks, "output_parts") else 1
             for p, (t0, t1) in enumerate(_token_parts(dp.T, parts)):
                 dp._k("mb_combine_rows", dp.ptr_dxp[m].data_ptr(), dp.perm[m][t0:].data_ptr(), None, t1 - t0,
                       dp.shape.top_k, h, dx[t0:].data_ptr(), dp.ptr_dgate[m].data_ptr(), dgate[t0:].data_ptr(),
-                      dp.npart, self.st_x)
+                      dp.npart, dp.comm_blocks, self.st_x)
                 if self.hooks:
                     self.hooks.after_backward(m, xs, p)
+        acc = dp.acc_mb[m]
+        if acc is not None:
+            variants, n, max_n = acc
+            tasks_fresh, tasks_acc = variants[dp.bank]
+            with dp._timed(n * (max_n * 4), "comm_replica_grad_pushback", xs):
+                dp._k("mb_accumulate_f32_tasks", (tasks_fresh if self.fresh else tasks_acc).data_ptr(), n, max_n,
+                      self.st_x)
 
     # -------------------------------------------------------------- compute stream
     def fwd_gemms(self, m):
@@ -1006,65 +1266,98 @@ class _StepOps:
         ng = dp.nslots[m]
         if ng:
             g = dp.groups[m][:ng]
+            a = dp.set_index(m)
             rows = dp.real_rows(m)
+            i1 = self._replica_set("w1", m)
             with dp._timed(4.0 * rows * h * hp, "fwd_swiglu"):
-                K.grouped_gemm(K.GEMM_FWD_SWIGLU, dp.Xr[m], dp.W1, g, N=2 * hp, K=h, C=dp.H[m], C2=dp.Act[m],
-                               B1=dp.W1r[m])
+                dp._gemm(K.GEMM_FWD_SWIGLU, dp.Xr[a], dp.W1, g, N=2 * hp, K=h, C=dp.H[a], C2=dp.Act[a],
+                         B1=dp.W1r[i1])
+            self._replica_used("w1", i1, m)
+            i2 = self._replica_set("w2", m)
             with dp._timed(2.0 * rows * h * hp, "fwd_down"):
-                K.grouped_gemm(K.GEMM_FWD_STORE, dp.Act[m], dp.W2, g, N=h, K=hp, C=dp.Y[m], B1=dp.W2r[m])
-            dp.launches += 2
+                dp._gemm(K.GEMM_FWD_STORE, dp.Act[a], dp.W2, g, N=h, K=hp, C=dp.Y[a], B1=dp.W2r[i2])
+            self._replica_used("w2", i2, m)
 
     def bwd_gemms(self, m):
-        """B(m): dAct with the combine backward + dSwiGLU fused in its epilogue, then dX."""
+        """B(m): dAct with the combine backward + dSwiGLU fused in its epilogue, dX, then the
+        weight gradients of the replicas this rank served (stored into the gradient ring)."""
         dp = self.dp
         h, hp = dp.shape.hidden, dp.shape.ffn
         ng = dp.nslots[m]
         if ng:
             g = dp.groups[m][:ng]
+            a = dp.set_index(m)
             rows = dp.real_rows(m)
+            i2 = self._replica_set("w2", m)
             # dAct = dout.W2 with the combine backward fused in the epilogue: gate applied per row,
             # dgate partials <dout.W2, act> = <dout, Y>, gate*act written over Act for dW2
             with dp._timed(2.0 * rows * h * hp, "dgrad_act_gated"):
-                K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU_GATED, dp.dYr[m], dp.W2, g, N=hp, K=h, C=dp.dH[m],
-                               C2=dp.Act[m], aux=dp.H[m], B1=dp.W2r[m], row_scale=dp.gate_r[m],
-                               row_partial=dp.dgate_r[m])
+                dp._gemm(K.GEMM_DGRAD_DSWIGLU_GATED, dp.dYr[a], dp.W2, g, N=hp, K=h, C=dp.dH[a],
+                         C2=dp.Act[a], aux=dp.H[a], B1=dp.W2r[i2], row_scale=dp.gate_r[a],
+                         row_partial=dp.dgate_r[a])
+            self._replica_used("w2", i2, m)
+            i1 = self._replica_set("w1", m)
             with dp._timed(4.0 * rows * h * hp, "dgrad_x"):
-                K.grouped_gemm(K.GEMM_DGRAD_STORE, dp.dH[m], dp.W1, g, N=h, K=2 * hp, C=dp.dXp[m], B1=dp.W1r[m])
-            dp.launches += 2
+                dp._gemm(K.GEMM_DGRAD_STORE, dp.dH[a], dp.W1, g, N=h, K=2 * hp, C=dp.dXp[a], B1=dp.W1r[i1])
+            self._replica_used("w1", i1, m)
+        self.rep_done.add(m)
+        rw = dp.rw_mb[m]
+        if rw is not None:
+            tab, segs, rrows = rw
+            a, q = dp.set_index(m), m % GRAD_RING
+            with dp._timed(6.0 * rrows * h * hp, "wgrad_replica"):
+                dp._gemm(K.GEMM_WGRAD, dp.dYr[a], dp.Act[a], tab, M=h, N=hp, C=dp.rgW2[q], c_slot_stride=h * hp,
+                         segs=segs)
+                dp._gemm(K.GEMM_WGRAD, dp.dH[a], dp.Xr[a], tab, M=2 * hp, N=h, C=dp.rgW1[q],
+                         c_slot_stride=2 * hp * h, segs=segs)
 
-    def finish(self):
-        """Weight gradients over every micro-batch (compute stream) in two parts; the replica
-        gradient reduce (comm stream) starts once part A (replica groups + their owners'
-        experts) is done and overlaps part B; then both streams join the current stream."""
-        dp, cs, xs = self.dp, self.cs, self.xs
+    def wgrad_mb(self, m):
+        """W(m) (wgrad_mode "micro_batch"): home weight gradients of micro-batch m, K = its rows."""
+        dp = self.dp
+        w = dp.w_mb[m]
+        if w is None:
+            return
+        tab_fresh, tab_acc, segs, rows = w
+        tab = tab_fresh if self.fresh else tab_acc
         h, hp = dp.shape.hidden, dp.shape.ffn
-        self._issue_pushes()
-        fresh = dp._wgrad_prepare()
-        split = len(dp.wparts) > 1
-        widen = WGRAD_ALL_SMS and dp.overlap and split   # measured slower at N=1 (single part)
-        lib = nat.kernels()
-        try:
-            if widen and not split:
-                nat.check(lib.mb_set_gemm_sms(dp.all_sms), lib, "mb_set_gemm_sms")
-            dp._wgrad(dp.wparts[0], fresh)
-            ev = torch.cuda.Event()
-            ev.record(cs)
-            if split:
-                if widen:
-                    nat.check(lib.mb_set_gemm_sms(dp.all_sms), lib, "mb_set_gemm_sms")
-                dp._wgrad(dp.wparts[1], fresh)
-        finally:
-            nat.check(lib.mb_set_gemm_sms(dp.gemm_sms), lib, "mb_set_gemm_sms")
-        xs.wait_event(ev)
-        if dp.world > 1:  # collective: every rank runs both barriers, with or without replicas
-            mn1, mn2 = 2 * hp * h, h * hp
-            with dp._timed(sum(n for _, _, _, n in dp.reduce) * (mn1 + mn2) * 4, "comm_replica_grad_reduce", xs):
-                dp.arena.barrier(xs)  # every rank's replica gradients are complete
-                for loc, p1, p2, n in dp.reduce:
-                    dp._k("mb_accumulate_f32", dp.gW1[loc].data_ptr(), p1.data_ptr(), n, mn1, self.st_x)
-                    dp._k("mb_accumulate_f32", dp.gW2[loc].data_ptr(), p2.data_ptr(), n, mn2, self.st_x)
-                dp.arena.barrier(xs)  # peers finished reading our replica gradients
+        a = dp.set_index(m)
+        with dp._timed(2.0 * rows * h * hp, "wgrad_down"):
+            dp._gemm(K.GEMM_WGRAD, dp.dYr[a], dp.Act[a], tab, M=h, N=hp, C=dp.gW2, c_slot_stride=h * hp, segs=segs)
+        with dp._timed(4.0 * rows * h * hp, "wgrad_gate_up"):
+            dp._gemm(K.GEMM_WGRAD, dp.dH[a], dp.Xr[a], tab, M=2 * hp, N=h, C=dp.gW1, c_slot_stride=2 * hp * h,
+                     segs=segs)
+
+    def _wgrad_step(self, part, sms):
+        dp = self.dp
+        tab_fresh, tab_acc, segs, rows, _ = part
+        tab = tab_fresh if self.fresh else tab_acc
+        h, hp = dp.shape.hidden, dp.shape.ffn
+        NA, R = dp.NA, dp.R
+        with dp._timed(2.0 * rows * h * hp, "wgrad_down"):
+            dp._gemm(K.GEMM_WGRAD, dp.dYr.view(NA * R, h), dp.Act.view(NA * R, hp), tab, M=h, N=hp, C=dp.gW2,
+                     c_slot_stride=h * hp, segs=segs, sms=sms)
+        with dp._timed(4.0 * rows * h * hp, "wgrad_gate_up"):
+            dp._gemm(K.GEMM_WGRAD, dp.dH.view(NA * R, 2 * hp), dp.Xr.view(NA * R, h), tab, M=2 * hp, N=h, C=dp.gW1,
+                     c_slot_stride=2 * hp * h, segs=segs, sms=sms)
+
+    def finish(self, last_x_ev):
+        """Step mode: home weight gradients over every micro-batch (part B: experts without
+        replica gradients, right after the last backward; part A: the rest, after the last
+        replica-gradient push-back, on every SM); then every stream joins the current one."""
+        dp, cs, xs = self.dp, self.cs, self.xs
+        if dp.wgrad_mode == "step":
+            part_b, part_a = dp.wparts
+            if part_b is not None:
+                self._wgrad_step(part_b, None)
+            if part_a is not None:
+                if last_x_ev is not None:
+                    cs.wait_event(last_x_ev)
+                else:
+                    cs.wait_stream(xs)
+                # the comm stream is idle by now: the last weight-gradient launch takes every SM
+                self._wgrad_step(part_a, dp.all_sms if (WGRAD_ALL_SMS and dp.overlap) else None)
         cs.wait_stream(xs)
+        cs.wait_stream(dp.cps)
 
 
 class MoELayerFunction(torch.autograd.Function):
@@ -1073,11 +1366,12 @@ class MoELayerFunction(torch.autograd.Function):
         dp.begin_step()
         outs = [MoELayerFunction.apply(x[m], gates[m], dp, idx[m], m) for m in range(MB)]
         ... loss.backward()        # runs backward_mb for every micro-batch
-        dp.end_step()              # weight gradients + replica-gradient reduce into dp.gW1 / gW2
+        dp.end_step()              # home weight gradients into dp.gW1 / gW2
 
     Differentiable in x ([T, h] bf16) and gates ([T, k] fp32); the expert weight gradients
-    accumulate inside the data plane (fp32, all micro-batches of the step in one contraction).
-    Every rank must run the same micro-batches in the same order (collective barriers)."""
+    accumulate inside the data plane (fp32, all micro-batches of the step in one contraction;
+    replica gradients pushed back per micro-batch).  Every rank must run the same micro-batches
+    in the same order (collective barriers)."""
 
     @staticmethod
     def forward(ctx, x, gates, dp, idx, m):

@@ -34,10 +34,12 @@ class Routing:
 
 
 def make_routing(shape: LayerShape, tokens: int, micro_batches: int, world: int, rank: int, zipf_s: float = 1.0,
-                 shift: int = 7, seed: int = 20261018, balanced: bool = False, all_ranks: bool = True) -> Routing:
+                 shift: int = 7, seed: int = 20261018, balanced: bool = False, all_ranks: bool = True,
+                 mb_offset: int = 0) -> Routing:
     """This rank's token-level indices/gates and (all_ranks) every rank's counts via np.bincount.
     With all_ranks=False only this rank's row of `mats` is filled (the caller histograms on the
-    device and all-gathers, see moe_layer.gather_routing)."""
+    device and all-gathers, see moe_layer.gather_routing).  mb_offset: index of the first
+    micro-batch in the run (a sequence of batches continues the hot-set rotation)."""
     gen = ZipfRouting(shape.num_experts, shape.top_k, tokens, zipf_s=zipf_s, shift=shift, seed=seed,
                       balanced=balanced)
     mats = np.zeros((micro_batches, world, shape.num_experts), dtype=np.int64)
@@ -45,7 +47,7 @@ def make_routing(shape: LayerShape, tokens: int, micro_batches: int, world: int,
     gates = np.zeros((micro_batches, tokens, shape.top_k), dtype=np.float32)
     for m in range(micro_batches):
         for j in range(world) if all_ranks else (rank,):
-            i_j, g_j = gen.sample(m, 0, j)
+            i_j, g_j = gen.sample(m + mb_offset, 0, j)
             mats[m, j] = np.bincount(i_j.ravel(), minlength=shape.num_experts)
             if j == rank:
                 idx[m], gates[m] = i_j, g_j

@@ -40,7 +40,7 @@ def test_argument_errors_without_gpu():
     rc = lib.mb_expert_histogram(None, 1, 10, 0, 8, None, None, 32, None)
     assert rc == 1 and b"bad histogram shape" in lib.mb_last_error()
     rc = lib.mb_grouped_gemm(0, None, 0, 0, None, 0, None, 0, 0, None, None, 1, 0, 256, 64, None, 0, 0, None, 0,
-                             None, 0, None, None, None)
+                             None, 0, None, None, 0, None)
     assert rc == 1
     p = _native.planner()
     out = (ctypes.c_int64 * 3)()

@@ -19,7 +19,12 @@ pytestmark = pytest.mark.gpu
 TOL = 2e-2
 
 
-def _run(name, T, MB, zipf_s=1.0, balanced=False):
+def _assert_close(got, ref, what=""):
+    c = moe_ref.close(got, ref)
+    assert c["ok"], f"{what}: {c}"
+
+
+def _run(name, T, MB, zipf_s=1.0, balanced=False, **dp_kw):
     cfg = SHAPES[name]
     shape = cfg["shape"]
     routing = make_routing(shape, T, MB, 1, 0, zipf_s=zipf_s, shift=cfg["shift"], balanced=balanced)
@@ -27,7 +32,7 @@ def _run(name, T, MB, zipf_s=1.0, balanced=False):
     model = ModelProfile(1, shape.num_experts, shape.top_k, shape.hidden, shape.ffn)
     plan = build_step_plan("static", routing.mats, topo, model, topo.profile, SimConfigs(replica=ReplicaConfig(0)),
                            shape)
-    dp = MoEDataPlane(Comm(), shape, T, MB, plan)
+    dp = MoEDataPlane(Comm(), shape, T, MB, plan, **dp_kw)
     wg, wu, wd = make_weights(shape)
     dp.set_weights(wg.cuda(), wu.cuda(), wd.cuda())
     dp.zero_grads()
@@ -39,14 +44,16 @@ def _run(name, T, MB, zipf_s=1.0, balanced=False):
     dx = torch.empty_like(x)
     dgate = torch.empty(MB, T, shape.top_k, dtype=torch.float32, device="cuda")
     dp.step(x, idx, gates, dout, out, dx, dgate)
-    torch.cuda.synchronize()
+    dp.check(sync=True)
     return shape, routing, plan, dp, (wg, wu, wd), (x, dout, idx, gates), (out, dx, dgate)
 
 
-@pytest.mark.parametrize("name,T,MB", [("tiny", 256, 2), ("qwen3-30b-a3b", 512, 2), ("mixtral-8x7b", 256, 1),
-                                       ("qwen3-235b-a22b", 256, 1)])
-def test_layer_step_matches_oracle(name, T, MB):
-    shape, routing, plan, dp, (wg, wu, wd), (x, dout, idx, gates), (out, dx, dgate) = _run(name, T, MB)
+@pytest.mark.parametrize("name,T,MB,mode", [("tiny", 256, 2, "step"), ("qwen3-30b-a3b", 512, 2, "step"),
+                                            ("mixtral-8x7b", 256, 1, "step"), ("qwen3-235b-a22b", 256, 1, "step"),
+                                            ("qwen3-30b-a3b", 512, 5, "micro_batch"), ("tiny", 256, 4, "micro_batch")])
+def test_layer_step_matches_oracle(name, T, MB, mode):
+    shape, routing, plan, dp, (wg, wu, wd), (x, dout, idx, gates), (out, dx, dgate) = _run(name, T, MB,
+                                                                                            wgrad_mode=mode)
     E = shape.num_experts
     home = plan.home
     gwg = torch.zeros(E, shape.ffn, shape.hidden, device="cuda")
@@ -60,16 +67,16 @@ def test_layer_step_matches_oracle(name, T, MB):
         ref_perm = moe_ref.canonical_permutation_fast(routing.idx[m], 0, routing.mats[m], home, {}, {}, row_base)
         assert np.array_equal(dp.perm[m].cpu().numpy(), ref_perm)
         ref = moe_ref.moe_layer_fp32(x[m], idx[m], gates[m], wg.cuda(), wu.cuda(), wd.cuda(), dout[m])
-        assert moe_ref.rel_err(out[m], ref["out"]) < TOL
-        assert moe_ref.rel_err(dx[m], ref["dx"]) < TOL
-        assert moe_ref.rel_err(dgate[m], ref["dgate"]) < TOL
+        _assert_close(out[m], ref["out"], f"out mb{m}")
+        _assert_close(dx[m], ref["dx"], f"dx mb{m}")
+        _assert_close(dgate[m], ref["dgate"], f"dgate mb{m}")
         gwg += ref["dWg"]
         gwu += ref["dWu"]
         gwd += ref["dWd"]
     g_gate, g_up = deinterleave_w1(dp.gW1[:dp.M])
-    assert moe_ref.rel_err(g_gate, gwg) < TOL
-    assert moe_ref.rel_err(g_up, gwu) < TOL
-    assert moe_ref.rel_err(dp.gW2[:dp.M], gwd) < TOL
+    for got, ref, what in ((g_gate, gwg, "dWg"), (g_up, gwu, "dWu"), (dp.gW2[:dp.M], gwd, "dWd")):
+        c = moe_ref.expert_grads_close(got, ref)
+        assert c["ok"], f"{what}: {c}"
     dp.close()
 
 
@@ -175,10 +182,11 @@ def test_dropped_token_choices():
     assert np.array_equal(dp.counts[0].cpu().numpy(), moe_ref.histogram(routing.idx[0], shape.num_experts))
     assert bool((dp.perm[0].cpu().numpy()[routing.idx[0] < 0] == -1).all())
     ref = moe_ref.moe_layer_fp32(x[0], idx[0], gates[0], wg.cuda(), wu.cuda(), wd.cuda(), dout[0])
-    assert moe_ref.rel_err(out[0], ref["out"]) < TOL
-    assert moe_ref.rel_err(dx[0], ref["dx"]) < TOL
-    assert moe_ref.rel_err(dgate[0], ref["dgate"]) < TOL
+    _assert_close(out[0], ref["out"], "out")
+    _assert_close(dx[0], ref["dx"], "dx")
+    _assert_close(dgate[0], ref["dgate"], "dgate")
     assert torch.all(out[0, -32:] == 0) and torch.all(dx[0, -32:] == 0)
+    dp.check(sync=True)
     dp.close()
 
 
@@ -186,18 +194,128 @@ def test_dropped_token_choices():
 def test_tma_row_movers_bit_identical(name, T, MB):
     """The TMA bulk-copy row movers (mb_set_comm_blocks > 0: scatter, combine, dX un-permute with
     the dgate gather) give bit-identical step results to the register-copy kernels."""
-    from paper_2605_08639_b200 import _native as nat
-    lib = nat.kernels()
     shape, routing, plan, dp, _, (x, dout, idx, gates), (out, dx, dgate) = _run(name, T, MB)
     g1, g2 = dp.gW1.clone(), dp.gW2.clone()
-    try:
-        nat.check(lib.mb_set_comm_blocks(12), lib, "mb_set_comm_blocks")
-        dp.zero_grads()
-        o2, dx2, dg2 = torch.empty_like(out), torch.empty_like(dx), torch.empty_like(dgate)
-        dp.step(x, idx, gates, dout, o2, dx2, dg2)
-        torch.cuda.synchronize()
-    finally:
-        nat.check(lib.mb_set_comm_blocks(0), lib, "mb_set_comm_blocks")
+    assert dp.comm_blocks == 0           # world 1: register movers
+    dp.comm_blocks = 12                  # per-plane engine: confined bulk-copy movers on 12 SMs
+    dp.zero_grads()
+    o2, dx2, dg2 = torch.empty_like(out), torch.empty_like(dx), torch.empty_like(dgate)
+    dp.step(x, idx, gates, dout, o2, dx2, dg2)
+    torch.cuda.synchronize()
     assert torch.equal(o2, out) and torch.equal(dx2, dx) and torch.equal(dg2, dgate)
     assert torch.equal(dp.gW1, g1) and torch.equal(dp.gW2, g2)
     dp.close()
+
+
+def test_micro_batch_wgrad_mode_matches_step_mode():
+    """wgrad_mode="micro_batch" (per-micro-batch weight gradients, a 3-set activation ring) runs
+    the same forward / dgrad kernels: out / dx / dgate bit-identical, fp32 gradients equal up to
+    the accumulation order, and far fewer activation bytes."""
+    shape, routing, plan, dp, wts, (x, dout, idx, gates), (out, dx, dgate) = _run("qwen3-30b-a3b", 512, 6)
+    shape2, _, _, dp2, _, _, (o2, dx2, dg2) = _run("qwen3-30b-a3b", 512, 6, wgrad_mode="micro_batch")
+    assert torch.equal(o2, out) and torch.equal(dx2, dx) and torch.equal(dg2, dgate)
+    for a, b in ((dp.gW1, dp2.gW1), (dp.gW2, dp2.gW2)):
+        assert moe_ref.rel_l2(b, a) < 1e-5
+    assert dp2.memory_report()["activations"] * 2 == dp.memory_report()["activations"]
+    dp.close()
+    dp2.close()
+
+
+def test_bench_configuration_parity():
+    """The benchmarked configuration itself (Qwen3-30B-A3B layer, T = 8192 tokens, MB = 8
+    micro-batches, EP = 1, Zipf 1.0, 128 ragged expert groups, weight gradients contracted over
+    every micro-batch): two micro-batches' out / dx / dgate and the gradients of 16 hot and cold
+    experts against the fp32 oracle."""
+    T, MB = 8192, 8
+    shape, routing, plan, dp, (wg, wu, wd), (x, dout, idx, gates), (out, dx, dgate) = _run("qwen3-30b-a3b", T, MB)
+    wgc, wuc, wdc = wg.cuda(), wu.cuda(), wd.cuda()
+    for m in (0, MB - 1):
+        ref = moe_ref.moe_layer_fp32(x[m], idx[m], gates[m], wgc, wuc, wdc, dout[m])
+        for key, got in (("out", out[m]), ("dx", dx[m]), ("dgate", dgate[m])):
+            _assert_close(got, ref[key], f"{key} mb{m}")
+        del ref
+    load = routing.mats.sum(axis=(0, 1))
+    order = np.argsort(-load, kind="stable")
+    experts = np.concatenate([order[:8], order[-8:]])          # 8 hottest + 8 coldest
+    sel = torch.from_numpy(experts).cuda()
+    gsum = None
+    for m in range(MB):
+        # oracle restricted to the sampled experts: drop every other expert's choices
+        keep = torch.isin(idx[m], sel)
+        idx_m = torch.where(keep, idx[m], torch.full_like(idx[m], -1))
+        r = moe_ref.moe_layer_fp32(x[m], idx_m, gates[m], wgc, wuc, wdc, dout[m])
+        g = (r["dWg"][sel], r["dWu"][sel], r["dWd"][sel])
+        gsum = g if gsum is None else tuple(a + b for a, b in zip(gsum, g))
+    g_gate, g_up = deinterleave_w1(dp.gW1[sel])
+    for got, ref, what in ((g_gate, gsum[0], "dWg"), (g_up, gsum[1], "dWu"), (dp.gW2[sel], gsum[2], "dWd")):
+        c = moe_ref.expert_grads_close(got, ref)
+        assert c["ok"], f"{what}: {c}"
+    dp.close()
+
+
+def test_routing_plan_mismatch_is_caught():
+    """Routing that differs from the counts the step plan was built for never writes past a
+    receive slot: the permutation drops the excess choices and the host raises."""
+    shape, routing, plan, dp, _, (x, dout, idx, gates), (out, dx, dgate) = _run("qwen3-30b-a3b", 512, 2)
+    bad = idx.clone()
+    bad[0, :64, :] = int(np.argmax(routing.mats[0, 0]))   # 64 tokens moved onto the hottest expert
+    bad[0, :64, 1:] = (bad[0, :64, :1] + torch.arange(1, shape.top_k, device=bad.device)) % shape.num_experts
+    dp.step(x, bad, gates, dout, out, dx, dgate)
+    with pytest.raises(RuntimeError, match="step plan"):
+        dp.check(sync=True)
+    dp.check(sync=True)   # the flag is cleared once reported
+    dp.close()
+
+
+def test_step_input_validation():
+    shape, routing, plan, dp, _, (x, dout, idx, gates), (out, dx, dgate) = _run("tiny", 256, 2)
+    with pytest.raises(ValueError, match="idx must be torch.int32"):
+        dp.step(x, idx.long(), gates, dout, out, dx, dgate)
+    with pytest.raises(ValueError, match="gates must be torch.float32"):
+        dp.step(x, idx, gates.bfloat16(), dout, out, dx, dgate)
+    with pytest.raises(ValueError, match="shape"):
+        dp.step(x[:, :128], idx[:, :128], gates[:, :128], dout[:, :128], out[:, :128], dx[:, :128], dgate[:, :128])
+    with pytest.raises(ValueError, match="contiguous"):
+        dp.step(x, idx.transpose(1, 2).contiguous().transpose(1, 2), gates, dout, out, dx, dgate)
+    with pytest.raises(ValueError, match="cpu"):
+        dp.step(x.cpu(), idx, gates, dout, out, dx, dgate)
+    dp.close()
+
+
+def test_per_plane_launch_settings():
+    """Two data planes with different shapes / SM splits in one process keep their own settings:
+    every GEMM and row-mover launch carries its plane's values (nothing process-global)."""
+    from paper_2605_08639_b200 import kernels as Kmod
+    seen = []
+    orig = Kmod.grouped_gemm
+
+    def spy(*a, sms=0, **kw):
+        seen.append(("gemm", sms))
+        return orig(*a, sms=sms, **kw)
+
+    a = _run("tiny", 256, 2, comm_sms=20)
+    b = _run("qwen3-30b-a3b", 512, 2, comm_sms=28, row_movers="tma")
+    dpa, dpb = a[3], b[3]
+    assert (dpa.gemm_sms, dpa.comm_blocks) != (dpb.gemm_sms, dpb.comm_blocks)
+    Kmod.grouped_gemm = spy
+    try:
+        calls = {}
+        for dp, res in ((dpa, a), (dpb, b), (dpa, a)):
+            seen.clear()
+            orig_k = dp._k
+            movers = []
+            dp._k = lambda name, *args, _o=orig_k, _m=movers: (_m.append(args[-2]) if name in (
+                "mb_scatter_rows", "mb_combine_rows") else None, _o(name, *args))
+            (x, dout, idx, gates), (out, dx, dgate) = res[5], res[6]
+            dp.step(x, idx, gates, dout, torch.empty_like(out), torch.empty_like(dx), torch.empty_like(dgate))
+            del dp._k
+            calls.setdefault(id(dp), []).append((set(s for _, s in seen), set(movers)))
+        torch.cuda.synchronize()
+        for dp in (dpa, dpb):
+            for gemm_sms, mover_blocks in calls[id(dp)]:
+                assert gemm_sms == {dp.gemm_sms}, (gemm_sms, dp.gemm_sms)
+                assert mover_blocks == {dp.comm_blocks}, (mover_blocks, dp.comm_blocks)
+    finally:
+        Kmod.grouped_gemm = orig
+    dpa.close()
+    dpb.close()

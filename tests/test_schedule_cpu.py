@@ -5,22 +5,35 @@ import pytest
 
 from paper_2605_08639_b200.moe_layer import schedule
 
-COMM_NEEDS = {"C": "F", "X": "B"}
-COMP_NEEDS = {"F": "D", "B": "C"}
+
+def _needs(mode):
+    """(comm needs, compute needs): op -> (op it waits for, micro-batch offset), as
+    MoEDataPlane.forward_backward links the two streams."""
+    if mode == "micro_batch":
+        return {"C": ("F", 0), "X": ("W", 0)}, {"F": ("D", 0), "B": ("C", 0), "W": ("X", -1)}
+    return {"C": ("F", 0), "X": ("B", 0)}, {"F": ("D", 0), "B": ("C", 0)}
 
 
-def _simulate(comm, comp):
+def _simulate(comm, comp, mode="step"):
     """Run both in-order queues to completion; an op starts once its dependency finished."""
+    comm_needs, comp_needs = _needs(mode)
     done, ci, pi, order = set(), 0, 0, []
+
+    def ready(needs, op, m):
+        if op not in needs:
+            return True
+        dop, off = needs[op]
+        return m + off < 0 or (dop, m + off) in done
+
     while ci < len(comm) or pi < len(comp):
         progressed = False
         if ci < len(comm):
             op, m = comm[ci]
-            if op not in COMM_NEEDS or (COMM_NEEDS[op], m) in done:
+            if ready(comm_needs, op, m):
                 done.add((op, m)); order.append((op, m)); ci += 1; progressed = True
         if pi < len(comp):
             op, m = comp[pi]
-            if (COMP_NEEDS[op], m) in done:
+            if ready(comp_needs, op, m):
                 done.add((op, m)); order.append((op, m)); pi += 1; progressed = True
         if not progressed:
             raise AssertionError(f"deadlock at comm {comm[ci:ci+1]} compute {comp[pi:pi+1]}")
@@ -28,14 +41,37 @@ def _simulate(comm, comp):
 
 
 @pytest.mark.parametrize("mb", [1, 2, 3, 4, 8, 16])
-def test_schedule_complete_and_deadlock_free(mb):
-    comm, comp = schedule(mb)
+@pytest.mark.parametrize("mode", ["step", "micro_batch"])
+def test_schedule_complete_and_deadlock_free(mb, mode):
+    comm, comp = schedule(mb, mode)
     assert sorted(comm) == sorted((p, m) for m in range(mb) for p in "DCX")
-    assert sorted(comp) == sorted((p, m) for m in range(mb) for p in "FB")
-    order = _simulate(comm, comp)
+    ops = "FB" if mode == "step" else "FBW"
+    assert sorted(comp) == sorted((p, m) for m in range(mb) for p in ops)
+    order = _simulate(comm, comp, mode)
     pos = {o: i for i, o in enumerate(order)}
     for m in range(mb):
         assert pos[("D", m)] < pos[("F", m)] < pos[("C", m)] < pos[("B", m)] < pos[("X", m)]
+        if mode == "micro_batch":
+            # per expert gradient: W(m) then X(m) (push-back) then W(m + 1): never concurrent
+            assert pos[("B", m)] < pos[("W", m)] < pos[("X", m)]
+            if m + 1 < mb:
+                assert pos[("X", m)] < pos[("W", m + 1)]
+
+
+@pytest.mark.parametrize("mb", [3, 4, 8, 16])
+def test_ring_sets_reuse_after_all_ranks_finished(mb):
+    """wgrad_mode micro_batch keeps RING_SETS buffer sets: on every rank's comm stream, D(m + 3)
+    (the first writer of micro-batch m's set) comes after X(m) (whose barrier means every rank
+    finished B(m) / W(m)), and C(m + 2) -- the barrier before B(m + 2) overwrites replica-gradient
+    ring set m % 2 -- comes after X(m)'s push-back reads it."""
+    from paper_2605_08639_b200.moe_layer import GRAD_RING, RING_SETS
+    comm, _ = schedule(mb, "micro_batch")
+    pos = {o: i for i, o in enumerate(comm)}
+    for m in range(mb):
+        if m + RING_SETS < mb:
+            assert pos[("X", m)] < pos[("D", m + RING_SETS)]
+        if m + GRAD_RING < mb:
+            assert pos[("X", m)] < pos[("C", m + GRAD_RING)]
 
 
 def test_at_most_two_micro_batches_ahead():
@@ -74,13 +110,15 @@ def test_token_parts_cover_every_token_once(T, parts):
     assert all(b > a for a, b in ranges) and len(ranges) <= parts
 
 
-def test_comm_sm_defaults():
-    """Row movers: 20 SMs at N=1 (register engine), 28 at N=2/4, 32 at N>=8, 8 for wide-FFN experts."""
+def test_comm_sm_defaults(monkeypatch):
+    """Row movers: 20 SMs at N=1 (register engine), 28 at N=2/4, 32 at N>=8 and for the 4096-wide
+    rows of Qwen3-235B (measured with 32), 8 for wide-FFN experts."""
     from paper_2605_08639_b200 import moe_layer as ml
     from paper_2605_08639_b200.workload import SHAPES
+    monkeypatch.delenv("MB_COMM_SMS", raising=False)
     assert ml.default_comm_sms(1, SHAPES["qwen3-30b-a3b"]["shape"]) == 20
     assert ml.default_comm_sms(8, SHAPES["qwen3-30b-a3b"]["shape"]) == 32
     assert ml.default_comm_sms(4, SHAPES["qwen3-30b-a3b"]["shape"]) == 28
-    assert ml.default_comm_sms(4, SHAPES["qwen3-235b-a22b"]["shape"]) == 28
+    assert ml.default_comm_sms(4, SHAPES["qwen3-235b-a22b"]["shape"]) == 32
     assert ml.default_comm_sms(4, SHAPES["mixtral-8x7b"]["shape"]) == 8
     assert ml.ROW_MOVERS[1] == "regs" and ml.ROW_MOVERS_MULTI == "tma"

@@ -64,15 +64,15 @@ def main():
     st = torch.cuda.current_stream().cuda_stream
 
     def scatter():
-        nat.check(lib.mb_scatter_rows(x.data_ptr(), T, k, h, perm.data_ptr(), ptrs.data_ptr(), st), lib, "scatter")
+        nat.check(lib.mb_scatter_rows(x.data_ptr(), T, k, h, perm.data_ptr(), ptrs.data_ptr(), -1, st), lib, "scatter")
 
     def combine():
         nat.check(lib.mb_combine_rows(ptrs.data_ptr(), perm.data_ptr(), gates.data_ptr(), T, k, h, out.data_ptr(),
-                                      None, None, 1, st), lib, "combine")
+                                      None, None, 1, -1, st), lib, "combine")
 
     def unpermute():
         nat.check(lib.mb_combine_rows(ptrs.data_ptr(), perm.data_ptr(), None, T, k, h, out.data_ptr(),
-                                      sptrs.data_ptr(), dgate.data_ptr(), npart, st), lib, "unpermute")
+                                      sptrs.data_ptr(), dgate.data_ptr(), npart, -1, st), lib, "unpermute")
 
     def sync():
         torch.cuda.synchronize()
