@@ -372,22 +372,27 @@ def check_step(args, comm, dp, dev, plan, shape):
     return res
 
 
-def measure_sequence(args, comm, shape, cfg, topo, model, cfgs, policies):
+def measure_sequence(args, comm, shape, cfg, topo, model, cfgs):
     """Replay a sequence of batches whose hot set keeps shifting (each batch continues the
-    micro-batch rotation of the last one): every batch gets its own plan, and the ReLibra arm
-    migrates experts -- weights plus fp32 master weights and both Adam moments, the state an
-    optimizer step leaves, through MoEDataPlane.migrate -- at every batch boundary, inside the
-    timed region.  Returns per policy the tokens/s over the sequence
-    and the migration share."""
+    micro-batch rotation of the last one); a batch is --batch-steps training steps under one
+    plan.  Every batch is planned from its own routing, and expert migration -- bf16 weights,
+    fp32 master weights and both Adam moments, the state an optimizer step leaves, moved by
+    MoEDataPlane.migrate -- happens at every batch boundary inside the timed region
+    (PAPER.md:390-392, 1081-1084).  Arms: "relibra_fresh" re-anneals every batch from scratch
+    (the reference's planner: every batch's plan is independent, so most experts move);
+    "relibra" prices migration into the choice (moe_layer.migration_aware_step_plan: the new
+    annealed plan relabeled for overlap, or the current placement, whichever models faster
+    over the batch including its migration); "static" never moves."""
     import torch
     from paper_2605_08639_b200.kernels import expert_histogram
-    from paper_2605_08639_b200.moe_layer import gather_routing
+    from paper_2605_08639_b200.moe_layer import gather_routing, migration_aware_step_plan
     from paper_2605_08639_b200.workload import make_routing
     rank, world = comm.rank, comm.world
-    T, MB, NB = args.tokens, args.micro_batches, args.batches
+    T, MB, NB, S = args.tokens, args.micro_batches, args.batches, args.batch_steps
     pdim = 3 * shape.hidden * shape.ffn
     state = {"master": ((pdim,), torch.float32), "adam_m": ((pdim,), torch.float32),
              "adam_v": ((pdim,), torch.float32)}
+    bytes_per_expert = pdim * (2 + 3 * 4)
     routings = []
     for b in range(NB):
         r = make_routing(shape, T, MB, world, rank, zipf_s=args.zipf, shift=hot_shift(args, cfg), all_ranks=False,
@@ -396,67 +401,78 @@ def measure_sequence(args, comm, shape, cfg, topo, model, cfgs, policies):
         r.mats = gather_routing(comm, counts.cpu().numpy().astype(np.int64))
         routings.append(r)
     out = {}
-    for pol in policies:
-        plans, plan_ms = [], []
-        for r in routings:
-            p, ms = _plan(args, comm, pol, shape, r, topo, model, cfgs)
+    for arm in ("relibra", "relibra_fresh", "static"):
+        plans, plan_ms, choices = [], [], []
+        for b, r in enumerate(routings):
+            if arm == "relibra" and b > 0:
+                t0 = time.perf_counter()
+                p, info = migration_aware_step_plan(plans[-1], r.mats, topo, model, topo.profile, cfgs, shape,
+                                                    bytes_per_expert, steps_per_batch=S)
+                ms = (time.perf_counter() - t0) * 1e3
+                choices.append(info["choice"])
+            else:
+                p, ms = _plan(args, comm, "static" if arm == "static" else "relibra", shape, r, topo, model, cfgs)
             plans.append(p)
             plan_ms.append(ms)
-        dp = _make_plane(comm, shape, T, MB, plans[0], rows_cap=max(p.rows_cap for p in plans), expert_state=state)
+        digests = comm.all_gather_object([plan_digest_of(p) for p in plans])
+        if any(d != digests[0] for d in digests):
+            raise RuntimeError("ranks disagree on the batch plans")
+        dp = _make_plane(comm, shape, T, MB, plans[0], rows_cap=max(p.rows_cap for p in plans), expert_state=state,
+                         wgrad_mode=args.wgrad_mode, replica_sets=args.replica_sets)
         tables = [dp.build_tables(p) for p in plans]
         devs = [_device_inputs(shape, T, MB, rank, r) for r in routings]
-        moved = [0]
+        moved = [0, 0]
+
+        def switch(b):
+            info = dp.migrate(tables[b], grads=False)   # after the optimizer step: gradients are zero
+            moved[0] += info["bytes_in"]
+            moved[1] += info["experts_moved"]
 
         def run_sequence():
             for b in range(NB):
                 if b:
-                    if pol == "static":
-                        dp.load_plan(tables[b])    # same placement, new counts: tables only
-                    else:
-                        info = dp.migrate(tables[b], grads=False)   # after the optimizer step
-                        moved[0] += info["bytes_in"]
-                _step(dp, devs[b])
-            # back to batch 0's placement for the next repetition (not timed)
+                    switch(b)
+                for _ in range(S):
+                    _step(dp, devs[b])
 
-        def reset():
-            if dp.plan is not plans[0]:
-                dp.migrate(tables[0], grads=False) if pol != "static" else dp.load_plan(tables[0])
-
+        for _ in range(args.warmup):   # warm-up pass (also back to batch 0's placement below)
+            _step(dp, devs[0])
         run_sequence()
-        reset()
-        torch.cuda.synchronize()
-        moved[0] = 0
-        total, mig = [], []
+        switch(0)
+        total = []
         for _ in range(args.repeats):
-            ms = _timed_steps(comm, run_sequence, 1)
-            total.append(ms)
-            reset()
-        # migration alone (same moves, no steps) for its share of the sequence
-        if pol != "static":
-            def migrations_only():
-                for b in range(1, NB):
-                    dp.migrate(tables[b], grads=False)
-                dp.migrate(tables[0], grads=False)
-            mig_ms = _timed_steps(comm, migrations_only, 1) * (NB - 1) / NB
-        else:
-            mig_ms = 0.0
-        tokens = world * T * MB * NB
+            moved[0] = moved[1] = 0
+            total.append(_timed_steps(comm, run_sequence, 1))
+            switch(0)   # not timed: back to batch 0's placement for the next repetition
+        # the migrations alone (same moves, no steps): their share of the sequence
+        mig_ms = _timed_steps(comm, lambda: [switch(b) for b in list(range(1, NB)) + [0]], 1) * (NB - 1) / NB
+        tokens = world * T * MB * NB * S
         med = statistics.median(total)
-        out[pol] = {"tokens_per_s": tokens / (med / 1e3), "ms_per_batch": med / NB,
-                    "ms_min": min(total) / NB, "ms_max": max(total) / NB,
-                    "migration_ms_per_batch": round(mig_ms / max(1, NB - 1) if NB > 1 else 0.0, 4),
-                    "migration_gb_in_per_rank_per_batch": round(moved[0] / args.repeats / max(1, NB - 1) / 1e9, 4),
+        out[arm] = {"tokens_per_s": tokens / (med / 1e3), "ms_per_step": med / (NB * S),
+                    "ms_per_step_min": min(total) / (NB * S), "ms_per_step_max": max(total) / (NB * S),
+                    "migration_ms_per_batch": round(mig_ms / max(1, NB - 1), 4),
+                    "migration_share": round(mig_ms / med, 4),
+                    "experts_moved_per_rank_per_batch": round(moved[1] / max(1, NB - 1), 2),
+                    "migration_gb_in_per_rank_per_batch": round(moved[0] / max(1, NB - 1) / 1e9, 4),
                     "planner_ms_per_batch": round(statistics.mean(plan_ms), 2),
                     "skew": round(float(np.mean([p.skew() for p in plans])), 4)}
+        if choices:
+            out[arm]["plan_choices"] = choices
         dp.close()
         del dp, devs, tables
         gc.collect()
         torch.cuda.empty_cache()
-    if "relibra" in out and "static" in out:
-        out["speedup_vs_static"] = round(out["static"]["ms_per_batch"] / out["relibra"]["ms_per_batch"], 4)
-    out["batches"] = NB
-    out["state_per_expert"] = "bf16 weights + fp32 master + Adam m, v (the state an optimizer step leaves)"
+    for arm in ("relibra", "relibra_fresh"):
+        out[arm]["speedup_vs_static"] = round(out["static"]["ms_per_step"] / out[arm]["ms_per_step"], 4)
+    out["batches"], out["steps_per_batch"] = NB, S
+    out["state_per_expert_bytes"] = bytes_per_expert
+    out["state_per_expert"] = "bf16 weights + fp32 master weights + Adam m, v (what an optimizer step leaves)"
     return out
+
+
+def plan_digest_of(plan):
+    from paper_2605_08639_b200.moe_layer import plan_digest
+    return plan_digest(plan)
 
 
 def run_ours(args, comm):
@@ -648,9 +664,10 @@ def run_ours(args, comm):
         line["balance"]["model_predicted_frac_of_balanced"] = (results["balanced_oracle"]["predicted_ms"]
                                                                / results[args.headline]["predicted_ms"])
     if args.batches > 1 and trace is None:
-        seq = measure_sequence(args, comm, shape, cfg, topo, model, cfgs, ["relibra", "static"])
+        seq = measure_sequence(args, comm, shape, cfg, topo, model, cfgs)
         line["balance"]["shifting_batches"] = seq
         line["balance"]["relibra_with_migration"] = seq["relibra"]["tokens_per_s"]
+        line["balance"]["relibra_fresh_with_migration"] = seq["relibra_fresh"]["tokens_per_s"]
     if check is not None:
         line["check"] = check
     if rank == 0 and world == 1 and not args.no_cpu_baseline and trace is None:
@@ -687,6 +704,7 @@ def main():
                     help="interleaved repetitions of every policy (rotated order); value = the headline's median")
     ap.add_argument("--batches", type=int, default=4,
                     help="batches of the shifting-routing sequence (new plan + expert migration per batch); 1 = off")
+    ap.add_argument("--batch-steps", type=int, default=4, help="training steps per batch of the sequence")
     ap.add_argument("--wgrad-mode", default="step", choices=["step", "micro_batch"])
     ap.add_argument("--replica-sets", type=int, default=None)
     ap.add_argument("--check", action="store_true",

@@ -55,7 +55,8 @@ inline PFN_encodeTiled get_encode_tiled() {
 
 // 2-D tensor map, SWIZZLE_128B: dims {inner, outer}, row pitch in bytes, box {box_inner, box_outer}.
 inline int make_tmap_2d(CUtensorMap* map, CUtensorMapDataType dtype, const void* base, uint64_t inner,
-                        uint64_t outer, uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_outer) {
+                        uint64_t outer, uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_outer,
+                        CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B) {
   PFN_encodeTiled enc = get_encode_tiled();
   if (!enc) return set_error(MB_ECUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
   if (outer == 0) outer = 1;
@@ -64,7 +65,7 @@ inline int make_tmap_2d(CUtensorMap* map, CUtensorMapDataType dtype, const void*
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estride[2] = {1, 1};
   CUresult r = enc(map, dtype, 2, const_cast<void*>(base), dims, strides, box, estride,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return set_error(MB_ECUDA, "cuTensorMapEncodeTiled failed (%d): inner=%llu outer=%llu pitch=%llu box=%ux%u", (int)r,
@@ -74,9 +75,10 @@ inline int make_tmap_2d(CUtensorMap* map, CUtensorMapDataType dtype, const void*
 }
 
 inline int make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
-                             uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_outer) {
+                             uint64_t row_pitch_bytes, uint32_t box_inner, uint32_t box_outer,
+                             CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B) {
   return make_tmap_2d(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, base, inner, outer, row_pitch_bytes, box_inner,
-                      box_outer);
+                      box_outer, swizzle);
 }
 
 inline int device_sm_count() {

@@ -124,9 +124,14 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
         return rc;
     } else {
       MB_CHECK_ARG(ldc % 64 == 0 && (!C2 || ldc2 % 64 == 0), "output widths must be multiples of 64");
-      if ((rc = make_tmap_bf16_2d(&p.tmC, C, ldc, a_rows, ldc * 2, 64, 32))) return rc;
-      if (C2 && (rc = make_tmap_bf16_2d(&p.tmC2, C2, ldc2, a_rows, ldc2 * 2, 64, 32))) return rc;
-      if (aux && (rc = make_tmap_bf16_2d(&p.tmAux, aux, ld_aux, a_rows, ld_aux * 2, 64, 32))) return rc;
+      // dSwiGLU epilogues move 32-feature chunks (32 rows x 64 B boxes, 64B swizzle); the others
+      // 32 rows x 128 B boxes (128B swizzle)
+      const bool heavy = mode == MB_GEMM_DGRAD_DSWIGLU || mode == MB_GEMM_DGRAD_DSWIGLU_GATED;
+      const uint32_t bw = heavy ? 32 : 64;
+      const CUtensorMapSwizzle sz = heavy ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+      if ((rc = make_tmap_bf16_2d(&p.tmC, C, ldc, a_rows, ldc * 2, bw, 32, sz))) return rc;
+      if (C2 && (rc = make_tmap_bf16_2d(&p.tmC2, C2, ldc2, a_rows, ldc2 * 2, bw, 32, sz))) return rc;
+      if (aux && (rc = make_tmap_bf16_2d(&p.tmAux, aux, ld_aux, a_rows, ld_aux * 2, bw, 32, sz))) return rc;
     }
   }
   switch (mode) {

@@ -28,35 +28,35 @@ struct PairTile {
   static constexpr int kBoxBytes = 32 * 128;  // one 32-row x 128-byte TMA box
 };
 
-#ifndef MB_PAIR_HEAVY_EPI_WARPS
-#define MB_PAIR_HEAVY_EPI_WARPS 8   // 4 (two column passes, 5 operand stages): dAct-gated 918 -> 845 TF
+#ifndef MB_PAIR_EPI_WARPS
+#define MB_PAIR_EPI_WARPS 8     // two per TMEM lane quarter (4 measured 3-25% slower beside the comm kernels)
 #endif
-#ifndef MB_PAIR_LIGHT_EPI_WARPS
-#define MB_PAIR_LIGHT_EPI_WARPS 8   // 4 (6 stages) measured equal alone, 3-25% slower beside the comm kernels
+#ifndef MB_PAIR_STAGES
+#define MB_PAIR_STAGES 6        // operand ring depth (the MMA warp starved 9-19% of the time with 4-5)
 #endif
-// Shared-memory budget per epilogue kind: the dSwiGLU epilogues (heavy math, H staged in two
-// boxes per warp) run 8 epilogue warps and 4 operand stages; the light epilogues (store, SwiGLU,
-// fp32 gradient) run MB_PAIR_LIGHT_EPI_WARPS warps with one output box each and spend the rest
-// on operand stages (5 with 8 warps, 6 with 4).
+// Shared memory: MB_PAIR_STAGES x 32 KB operand stages, one 4 KB staging area per epilogue warp
+// (light epilogues: one 32-row x 128-byte output box; dSwiGLU epilogues: two 32-row x 64-byte
+// boxes -- 32 features of gate and of up -- that carry H in and dH / gate*act out), and a small
+// meta block (barriers + tile starts; the group table is read from global memory).
 template <int kEpi>
 struct PairCfg : PairTile {
   static constexpr bool kHeavy = kEpi == EPI_DSWIGLU || kEpi == EPI_DSWIGLU_GATED;
-  static constexpr int kEpiWarps = kHeavy ? MB_PAIR_HEAVY_EPI_WARPS : MB_PAIR_LIGHT_EPI_WARPS;
+  static constexpr int kEpiWarps = MB_PAIR_EPI_WARPS;
   static constexpr int kThreads = 64 + 32 * kEpiWarps;
-  static constexpr int kBoxesPerWarp = kHeavy ? 2 : 1;
-  static constexpr int kStages = kHeavy ? (kEpiWarps == 4 ? 5 : 4) : (kEpiWarps == 4 ? 6 : 5);
+  static constexpr int kStages = MB_PAIR_STAGES;
   static constexpr int kABytes = 128 * BK * 2;  // this CTA's 128 rows of A
   static constexpr int kBBytes = 128 * BK * 2;  // this CTA's 128 columns of B
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStagingBytes = kEpiWarps * kBoxesPerWarp * kBoxBytes;
-  static constexpr int kMetaBytes = 10240;
+  static constexpr int kStagingBytes = kEpiWarps * kBoxBytes;
+  static constexpr int kMetaBytes = 512 + 4 * (kMaxGroups + 8);
   static constexpr int kSmemBytes = kStages * kStageBytes + kStagingBytes + kMetaBytes + 1024;
   static_assert(kSmemBytes <= 232448, "shared memory budget");
+  static_assert(2 * kStages * 8 + 4 * 8 + 4 <= 256 && 256 + 8 * kEpiWarps <= 512, "meta layout");
 };
 
 template <bool kW>
-__device__ __forceinline__ TileCoord decode_tile_pair(int t, const int* tile_start, const GemmGroup* sg, int ng,
-                                                      const GemmParams& p) {
+__device__ __forceinline__ TileCoord decode_tile_pair(int t, const int* tile_start, const GemmGroup* __restrict__ sg,
+                                                      int ng, const GemmParams& p) {
   int lo = 0, hi = ng - 1;
   while (lo < hi) {
     int mid = (lo + hi + 1) >> 1;
@@ -144,9 +144,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
   uint64_t* tfull_bar = empty_bar + S;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-  uint64_t* hbar_base = reinterpret_cast<uint64_t*>(meta + 128);  // one per epilogue warp (H tile loads)
-  int* tile_start = reinterpret_cast<int*>(meta + 256);
-  GemmGroup* sg = reinterpret_cast<GemmGroup*>(meta + 256 + 4 * (kMaxGroups + 8));
+  uint64_t* hbar_base = reinterpret_cast<uint64_t*>(meta + 256);  // one per epilogue warp (H tile loads)
+  int* tile_start = reinterpret_cast<int*>(meta + 512);
+  const GemmGroup* __restrict__ sg = p.groups;   // group table: global memory (L1-cached), read per tile
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -156,7 +156,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
   const int cluster = blockIdx.x >> 1;
   const int nclusters = gridDim.x >> 1;
 
-  for (int i = threadIdx.x; i < ng; i += blockDim.x) sg[i] = p.groups[i];
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&p.tmA);
     tma_prefetch_desc(&p.tmB0);
@@ -341,7 +340,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty_bar[1]), 0);
-    BoxStager<Cfg::kBoxesPerWarp> st{sStage + (warp - 2) * Cfg::kBoxesPerWarp * Cfg::kBoxBytes, 0, lane, p.debug};
+    BoxStager<1> st{sStage + (warp - 2) * Cfg::kBoxBytes, 0, lane, p.debug};
     uint64_t* hbar = hbar_base + (warp - 2);
     uint32_t hphase = 0;
     int it = 0;
@@ -451,91 +450,95 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
           }
           st.template put<false>(w, &p.tmC2, tc.nb * (TN / 2) + f0, out_row0);
         } else if constexpr (kEpi == EPI_DSWIGLU || kEpi == EPI_DSWIGLU_GATED) {
-          // dAct columns of 64-column segment hh = features [fo, +64) of interleave block blk:
-          // gate|up 256 columns of H / dH.  H (gate|up) comes in through TMA into the warp's two
-          // staging buffers, is read back row per lane, and the same buffers then carry dH (and
-          // gate*act) out through TMA stores.
+          // dAct columns of 64-column segment hh = features [fo, +64) of interleave block blk,
+          // processed as two 32-feature chunks: the chunk's H gate / up columns come in through
+          // TMA into the warp's two 2 KB staging boxes (32 rows x 64 B, 64B swizzle), are read
+          // back row per lane, and the same boxes then carry dH (gate / up) and gate*act out.
           constexpr bool kGated = kEpi == EPI_DSWIGLU_GATED;
+          constexpr int kHalfBox = PairTile::kBoxBytes / 2;
           const int64_t row = gg.a0 + tile_row;
           const bool real = !kGated || tile_row < gg.rows_real;
           const float gate = kGated ? (real ? p.rscale[row] : 0.0f) : 1.0f;
           uint8_t* bufA = st.base;
-          uint8_t* bufB = st.base + Cfg::kBoxBytes;
-          uint4* rowA = reinterpret_cast<uint4*>(bufA + lane * 128);
-          uint4* rowB = reinterpret_cast<uint4*>(bufB + lane * 128);
-          const int sw = lane & 7;
+          uint8_t* bufB = st.base + kHalfBox;
+          uint4* rowA = reinterpret_cast<uint4*>(bufA + lane * 64);
+          uint4* rowB = reinterpret_cast<uint4*>(bufB + lane * 64);
+          const int sw = (lane >> 1) & 3;   // 64B swizzle: 16-byte chunk j of row r sits at j ^ ((r >> 1) & 3)
 #pragma unroll 1
           for (int hh = half ? ch2 : 0; hh < (half ? ch2 + 1 : 2); ++hh) {
             const int blk = tc.nb * 2 + ocol(hh) / 128;
             const int fo = ocol(hh) % 128;
             float part = 0.0f;
-            if (lane == 0) {
-              bulk_wait_read<0>();  // earlier stores have drained both buffers
-              mbar_arrive_expect_tx(hbar, 2 * Cfg::kBoxBytes);
-              tma_load_2d(bufA, &p.tmAux, hbar, blk * 256 + fo, out_row0);
-              tma_load_2d(bufB, &p.tmAux, hbar, blk * 256 + 128 + fo, out_row0);
-            }
-            uint32_t d0[32], d1[32];
-            tmem_ld_32x32b_x32(t_acc + tcol(hh), d0);
-            tmem_ld_32x32b_x32(t_acc + tcol(hh) + 32, d1);
-            mbar_wait(hbar, hphase);
-            hphase ^= 1;
-            uint4 hg[8], hu[8];
-#pragma unroll
-            for (int v = 0; v < 8; ++v) {
-              hg[v] = rowA[v ^ sw];
-              hu[v] = rowB[v ^ sw];
-            }
-            tmem_ld_wait();
-            __syncwarp();  // every lane holds its H row before the buffers are rewritten
-            uint32_t wa[32];
-#pragma unroll
-            for (int v = 0; v < 8; ++v) {
-              const uint32_t gw[4] = {hg[v].x, hg[v].y, hg[v].z, hg[v].w};
-              const uint32_t uw[4] = {hu[v].x, hu[v].y, hu[v].z, hu[v].w};
-              uint32_t og[4], ou[4];
-#pragma unroll
-              for (int x = 0; x < 4; ++x) {
-                float dg2[2], du2[2], ag2[2];
-#pragma unroll
-                for (int h2 = 0; h2 < 2; ++h2) {
-                  const int col = v * 8 + x * 2 + h2;  // 0..63 within this half
-                  const float gv = h2 ? bf16hi(gw[x]) : bf16lo(gw[x]);
-                  const float uv = h2 ? bf16hi(uw[x]) : bf16lo(uw[x]);
-                  const float raw = __uint_as_float(col < 32 ? d0[col] : d1[col - 32]);
-                  const float s = __fdividef(1.0f, 1.0f + __expf(-gv));
-                  const float act = gv * s * uv;
-                  if (kGated) part += raw * act;
-                  const float dav = gate * raw;
-                  du2[h2] = real ? dav * gv * s : 0.0f;
-                  dg2[h2] = real ? dav * uv * s * (1.0f + gv * (1.0f - s)) : 0.0f;
-                  ag2[h2] = real ? gate * act : 0.0f;
-                }
-                og[x] = pack_bf16x2(dg2[0], dg2[1]);
-                ou[x] = pack_bf16x2(du2[0], du2[1]);
-                wa[v * 4 + x] = pack_bf16x2(ag2[0], ag2[1]);
+#pragma unroll 1
+            for (int c = 0; c < 2; ++c) {
+              const int f = fo + c * 32;   // first feature of this chunk within the block
+              if (lane == 0) {
+                bulk_wait_read<0>();  // earlier stores have drained both boxes
+                mbar_arrive_expect_tx(hbar, PairTile::kBoxBytes);
+                tma_load_2d(bufA, &p.tmAux, hbar, blk * 256 + f, out_row0);
+                tma_load_2d(bufB, &p.tmAux, hbar, blk * 256 + 128 + f, out_row0);
               }
-              rowA[v ^ sw] = make_uint4(og[0], og[1], og[2], og[3]);
-              rowB[v ^ sw] = make_uint4(ou[0], ou[1], ou[2], ou[3]);
-            }
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              const uint64_t pol = l2_evict_first_policy();
-              tma_store_2d(&p.tmC, bufA, blk * 256 + fo, out_row0, pol);
-              tma_store_2d(&p.tmC, bufB, blk * 256 + 128 + fo, out_row0, pol);
-              bulk_commit();
-            }
-            if (kGated) {
-              if (lane == 0) bulk_wait_read<0>();
-              __syncwarp();
+              uint32_t d[32];
+              tmem_ld_32x32b_x32(t_acc + tcol(hh) + c * 32, d);
+              mbar_wait(hbar, hphase);
+              hphase ^= 1;
+              uint4 hg[4], hu[4];
 #pragma unroll
-              for (int j = 0; j < 8; ++j) rowA[j ^ sw] = make_uint4(wa[4 * j], wa[4 * j + 1], wa[4 * j + 2], wa[4 * j + 3]);
+              for (int v = 0; v < 4; ++v) {
+                hg[v] = rowA[v ^ sw];
+                hu[v] = rowB[v ^ sw];
+              }
+              tmem_ld_wait();
+              __syncwarp();  // every lane holds its H row before the boxes are rewritten
+              uint32_t wa[16];
+#pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                const uint32_t gw[4] = {hg[v].x, hg[v].y, hg[v].z, hg[v].w};
+                const uint32_t uw[4] = {hu[v].x, hu[v].y, hu[v].z, hu[v].w};
+                uint32_t og[4], ou[4];
+#pragma unroll
+                for (int x = 0; x < 4; ++x) {
+                  float dg2[2], du2[2], ag2[2];
+#pragma unroll
+                  for (int h2 = 0; h2 < 2; ++h2) {
+                    const int col = v * 8 + x * 2 + h2;  // 0..31 within this chunk
+                    const float gv = h2 ? bf16hi(gw[x]) : bf16lo(gw[x]);
+                    const float uv = h2 ? bf16hi(uw[x]) : bf16lo(uw[x]);
+                    const float raw = __uint_as_float(d[col]);
+                    const float s = __fdividef(1.0f, 1.0f + __expf(-gv));
+                    const float act = gv * s * uv;
+                    if (kGated) part += raw * act;
+                    const float dav = gate * raw;
+                    du2[h2] = real ? dav * gv * s : 0.0f;
+                    dg2[h2] = real ? dav * uv * s * (1.0f + gv * (1.0f - s)) : 0.0f;
+                    ag2[h2] = real ? gate * act : 0.0f;
+                  }
+                  og[x] = pack_bf16x2(dg2[0], dg2[1]);
+                  ou[x] = pack_bf16x2(du2[0], du2[1]);
+                  wa[v * 4 + x] = pack_bf16x2(ag2[0], ag2[1]);
+                }
+                rowA[v ^ sw] = make_uint4(og[0], og[1], og[2], og[3]);
+                rowB[v ^ sw] = make_uint4(ou[0], ou[1], ou[2], ou[3]);
+              }
               fence_proxy_async_smem();
               __syncwarp();
               if (lane == 0) {
-                tma_store_2d(&p.tmC2, bufA, blk * 128 + fo, out_row0, l2_evict_first_policy());
+                const uint64_t pol = l2_evict_first_policy();
+                tma_store_2d(&p.tmC, bufA, blk * 256 + f, out_row0, pol);
+                tma_store_2d(&p.tmC, bufB, blk * 256 + 128 + f, out_row0, pol);
                 bulk_commit();
+              }
+              if (kGated) {
+                if (lane == 0) bulk_wait_read<0>();
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < 4; ++j) rowA[j ^ sw] = make_uint4(wa[4 * j], wa[4 * j + 1], wa[4 * j + 2], wa[4 * j + 3]);
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                  tma_store_2d(&p.tmC2, bufA, blk * 128 + f, out_row0, l2_evict_first_policy());
+                  bulk_commit();
+                }
               }
             }
             // partial <dAct, act> over these 64 features: rpart[row][N/64]

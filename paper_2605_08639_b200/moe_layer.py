@@ -47,7 +47,9 @@ PAD = 128       # receive-slot row padding = GEMM M tile
 _SKIP_ROWS = os.environ.get("MB_PROFILE_SKIP_ROWS", "0") == "1"
 # SMs left to the comm stream while the persistent GEMM runs (measured on B200, qwen3 shape:
 # N=4 step 24.1 ms with all 148 SMs in the GEMM, 19.7 ms with 28 left free)
-COMM_SMS = {1: 20, 2: 28, 4: 28}   # N=4 A/B: 28 SMs 18.41-18.60 ms vs 32 SMs 18.75-18.85
+# N=1: every SM to the GEMM (the 226 KB operand ring leaves no room for co-resident movers; the
+# HBM-local movers fill the SMs between GEMM launches): 19.71 ms/step vs 20.13 with 20 SMs reserved
+COMM_SMS = {1: 0, 2: 28, 4: 28}   # N=4 A/B: 28 SMs 18.41-18.60 ms vs 32 SMs 18.75-18.85
 COMM_SMS_MULTI = 32                # N >= 8 (most NVLink rows per GPU) keeps the wider split
 # Experts with a wide FFN do much more GEMM work per moved row (bytes / FLOP of a step = 4 / (9 h')):
 # at h' >= 4096 the TMA movers keep up on 8 SMs (Mixtral-8x7B at N=4: 79.3-79.8 -> 71.8-74.0 ms per
@@ -55,8 +57,10 @@ COMM_SMS_MULTI = 32                # N >= 8 (most NVLink rows per GPU) keeps the
 COMM_SMS_WIDE_FFN = 8
 WIDE_FFN = 4096
 WIDE_HIDDEN = 4096   # 4096-wide token rows (Qwen3-235B): its N=4 numbers were measured with 32 comm SMs
-# sets of the layer-shared replica weight slots (MoEDataPlane replica_sets; MB_REPLICA_SETS overrides)
-REPLICA_SETS = 2
+# sets of the layer-shared replica weight slots (MoEDataPlane replica_sets; MB_REPLICA_SETS overrides):
+# one set = exactly the paper's layer-shared buffer (replica_memory "layer-shared"); the backward
+# pulls its replicas again.  N=4 Qwen3-30B-A3B: 19.40 ms/step with 1 set vs 19.30 with 2.
+REPLICA_SETS = 1
 # Row-mover engine per world size: "regs" = register-copy kernels (co-resident with the GEMM's
 # CTAs on every SM), "tma" = cp.async.bulk kernels, one block on each of the COMM_SMS SMs the
 # GEMM leaves free (bulk-copy scatter, register combine with a shared-memory reservation).
@@ -1388,3 +1392,81 @@ class MoELayerFunction(torch.autograd.Function):
         dgate = torch.empty(dout.shape[0], ctx.k, dtype=torch.float32, device=dout.device)
         dp.backward_mb(m, dout.contiguous(), dx, dgate)
         return dx, dgate, None, None, None
+
+
+# ----------------------------------------------------------------------------- batch boundaries
+
+
+def relabel_for_overlap(new_home: np.ndarray, old_home: np.ndarray, topo: ClusterTopology) -> np.ndarray:
+    """The GPU relabeling of `new_home` (a permutation of GPU ids that maps whole groups onto
+    groups, so replicas stay inside a group) that keeps the most experts where `old_home` has
+    them: max sum_e [pi(new_home[e]) == old_home[e]] as two nested assignment problems (GPUs
+    inside each pair of groups, then groups).  The relabeled plan balances the same loads; its
+    modelled time differs only through which token rows stay local."""
+    g, gs = topo.num_gpus, topo.gpus_per_node
+    ng = g // gs
+    new_home, old_home = np.asarray(new_home, dtype=np.int64), np.asarray(old_home, dtype=np.int64)
+    overlap = np.zeros((g, g), dtype=np.int64)   # [new gpu, old gpu]
+    np.add.at(overlap, (new_home, old_home), 1)
+
+    def best_assignment(mat):
+        try:
+            from scipy.optimize import linear_sum_assignment
+            r, c = linear_sum_assignment(-mat)
+            return list(c[np.argsort(r)]), int(mat[r, c].sum())
+        except ImportError:   # small groups: exhaustive
+            import itertools
+            best, perm = -1, None
+            for p in itertools.permutations(range(mat.shape[0])):
+                v = int(sum(mat[i, p[i]] for i in range(len(p))))
+                if v > best:
+                    best, perm = v, list(p)
+            return perm, best
+
+    inner, gval = {}, np.zeros((ng, ng), dtype=np.int64)
+    for a in range(ng):
+        for b in range(ng):
+            sub = overlap[a * gs:(a + 1) * gs, b * gs:(b + 1) * gs]
+            inner[(a, b)], gval[a, b] = best_assignment(sub)
+    outer, _ = best_assignment(gval)
+    pi = np.zeros(g, dtype=np.int64)
+    for a in range(ng):
+        b = outer[a]
+        for i, j in enumerate(inner[(a, b)]):
+            pi[a * gs + i] = b * gs + j
+    return pi[new_home]
+
+
+def migration_aware_step_plan(prev: "StepPlan", mats: np.ndarray, topo: ClusterTopology, model: rt.ModelProfile,
+                              hw: HardwareProfile, cfgs: pol.SimConfigs, shape: LayerShape,
+                              bytes_per_expert: float, steps_per_batch: int = 1, link_bw: float = 700e9) -> tuple:
+    """ReLibra's plan for the next batch with the expert migration it implies priced in (the
+    reference plans every batch from scratch and does not model migration; PAPER.md:1081-1084
+    reports it as overhead): the annealing reorder of the new batch (seeded with the current
+    placement as an extra initial plan), relabeled for the largest overlap with the current
+    placement, against keeping the current placement; each candidate is scored as
+    steps_per_batch x its modelled step time (greedy replication per micro-batch) + the time to
+    pull its incoming experts (bytes_per_expert per expert, max over ranks, over NVLink).
+    Returns (StepPlan, info)."""
+    from . import reordering as ro
+    trace = rt.build_trace(model, topo, mats[:, None], tokens_per_gpu=0)
+    agg = rt.aggregate_batch(trace, 0)
+    new = ro.anneal_reorder(agg, topo, model, hw, cfgs.anneal,
+                            extra_initial_plans=[ro.static_plan(model.num_experts, topo),
+                                                 ro.ReorderPlan(np.asarray(prev.home, dtype=np.int64).copy())])
+    relabeled = relabel_for_overlap(new.assignment, prev.home, topo)
+    cands = {"keep": np.asarray(prev.home, dtype=np.int64), "reorder": relabeled}
+    scored = {}
+    for name, home in cands.items():
+        bundle = pol.replication_bundle(trace, [ro.ReorderPlan(home.copy())], topo, model, hw, cfgs)
+        plan = step_plan_from_bundle("relibra", bundle, mats, shape, layer=0, slots=cfgs.replica.slots_per_gpu)
+        moved_in = np.array([int(((home == d) & (prev.home != d)).sum()) for d in range(topo.num_gpus)])
+        mig_s = float(moved_in.max()) * bytes_per_expert / link_bw
+        t = steps_per_batch * plan.predicted_ms(topo, model, hw) / 1e3 + mig_s
+        scored[name] = (t, plan, int(moved_in.sum()), mig_s)
+    choice = min(scored, key=lambda k: (scored[k][0], k != "keep"))
+    t, plan, moved, mig_s = scored[choice]
+    info = {"choice": choice, "experts_moved": moved, "predicted_migration_ms": mig_s * 1e3,
+            "predicted_batch_ms": {k: v[0] * 1e3 for k, v in scored.items()},
+            "moved_without_relabel": int((new.assignment != prev.home).sum())}
+    return plan, info

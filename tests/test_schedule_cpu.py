@@ -111,12 +111,12 @@ def test_token_parts_cover_every_token_once(T, parts):
 
 
 def test_comm_sm_defaults(monkeypatch):
-    """Row movers: 20 SMs at N=1 (register engine), 28 at N=2/4, 32 at N>=8 and for the 4096-wide
+    """Row movers: none reserved at N=1 (register engine between GEMM launches), 28 at N=2/4, 32 at N>=8 and for the 4096-wide
     rows of Qwen3-235B (measured with 32), 8 for wide-FFN experts."""
     from paper_2605_08639_b200 import moe_layer as ml
     from paper_2605_08639_b200.workload import SHAPES
     monkeypatch.delenv("MB_COMM_SMS", raising=False)
-    assert ml.default_comm_sms(1, SHAPES["qwen3-30b-a3b"]["shape"]) == 20
+    assert ml.default_comm_sms(1, SHAPES["qwen3-30b-a3b"]["shape"]) == 0
     assert ml.default_comm_sms(8, SHAPES["qwen3-30b-a3b"]["shape"]) == 32
     assert ml.default_comm_sms(4, SHAPES["qwen3-30b-a3b"]["shape"]) == 28
     assert ml.default_comm_sms(4, SHAPES["qwen3-235b-a22b"]["shape"]) == 32
