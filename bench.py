@@ -422,11 +422,13 @@ def measure_sequence(args, comm, shape, cfg, topo, model, cfgs):
         tables = [dp.build_tables(p) for p in plans]
         devs = [_device_inputs(shape, T, MB, rank, r) for r in routings]
         moved = [0, 0]
+        counting = [False]
 
         def switch(b):
             info = dp.migrate(tables[b], grads=False)   # after the optimizer step: gradients are zero
-            moved[0] += info["bytes_in"]
-            moved[1] += info["experts_moved"]
+            if counting[0]:
+                moved[0] += info["bytes_in"]
+                moved[1] += info["experts_moved"]
 
         def run_sequence():
             for b in range(NB):
@@ -440,9 +442,10 @@ def measure_sequence(args, comm, shape, cfg, topo, model, cfgs):
         run_sequence()
         switch(0)
         total = []
-        for _ in range(args.repeats):
-            moved[0] = moved[1] = 0
+        for rep_i in range(args.repeats):
+            counting[0] = rep_i == 0          # moves of one pass over the sequence
             total.append(_timed_steps(comm, run_sequence, 1))
+            counting[0] = False
             switch(0)   # not timed: back to batch 0's placement for the next repetition
         # the migrations alone (same moves, no steps): their share of the sequence
         mig_ms = _timed_steps(comm, lambda: [switch(b) for b in list(range(1, NB)) + [0]], 1) * (NB - 1) / NB
@@ -452,8 +455,8 @@ def measure_sequence(args, comm, shape, cfg, topo, model, cfgs):
                     "ms_per_step_min": min(total) / (NB * S), "ms_per_step_max": max(total) / (NB * S),
                     "migration_ms_per_batch": round(mig_ms / max(1, NB - 1), 4),
                     "migration_share": round(mig_ms / med, 4),
-                    "experts_moved_per_rank_per_batch": round(moved[1] / max(1, NB - 1), 2),
-                    "migration_gb_in_per_rank_per_batch": round(moved[0] / max(1, NB - 1) / 1e9, 4),
+                    "experts_moved_in_per_batch_rank0": round(moved[1] / max(1, NB - 1), 2),
+                    "migration_gb_in_per_batch_rank0": round(moved[0] / max(1, NB - 1) / 1e9, 4),
                     "planner_ms_per_batch": round(statistics.mean(plan_ms), 2),
                     "skew": round(float(np.mean([p.skew() for p in plans])), 4)}
         if choices:

@@ -91,6 +91,22 @@ int mb_permute_rank_nb(const int32_t* idx, int64_t T, int32_t k, const float* ga
                        const int32_t* ncopies, int32_t maxc, float* const* dst_gate, int32_t world, int32_t* perm,
                        int32_t nb, int32_t* error_flag, void* stream);
 
+/* On-device per-micro-batch tables (one block): round_split of every replicated expert's tokens
+ * over its copies (replicate.py:501-525; fractions from the host token-split LP, per replicated
+ * expert [G][1+R_e] f64 concatenated in rep_experts order, counts out in the same layout), then the
+ * receive layout of every GPU (slot_tab, slot_w, nslots, total_rows), the route table every
+ * source places its rows with (route_tab, ncopies, as mb_permute_rank consumes them) and the
+ * executed flow [G][G] (costmodel.flow_matrix with integer splits, costmodel.py:91-108).
+ * x: [G][E] routing counts (the gathered K1 histograms); home: ReorderPlan.assignment; replicas
+ * as CSR (rep_ptr[n_rep+1] into rep_gpus, ReplicaPlacement.copies order, replicate.py:55-56).
+ * Bit-identical to mbp_round_split + mbp_dispatch_plan (include/mb_planner.h).  *error != 0 on
+ * inconsistent input (bit 1 split sums, 2 copies > maxc, 4 slots > max_slots, 8 rows >= 2^31). */
+int mb_dispatch_tables(int32_t G, int32_t E, const int32_t* x, const int32_t* home, int32_t n_rep,
+                       const int32_t* rep_experts, const int32_t* rep_ptr, const int32_t* rep_gpus, const double* frac,
+                       int32_t pad, int32_t maxc, int32_t max_slots, int64_t* counts, int32_t* route_tab,
+                       int32_t* ncopies, int32_t* slot_tab, int32_t* slot_w, int32_t* nslots, int64_t* total_rows,
+                       int64_t* flow, int32_t* error, void* stream);
+
 /* error_flag |= code when counts[i] != expected[i] for any i < n (the K1 histogram against the
  * counts the step plan was built from, RoutingTrace.matrices row, routing.py:151-168). */
 int mb_check_counts(const uint32_t* counts, const int32_t* expected, int64_t n, int32_t* error_flag, int32_t code,

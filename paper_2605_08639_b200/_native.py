@@ -52,6 +52,8 @@ _KERNEL_SIGS.update({
     "mb_permute_rank_nb": (c_int, [c_vp, c_i64, c_i32, c_vp, c_i32, c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_i32,
                                    c_vp, c_i32, c_vp, c_vp]),
     "mb_check_counts": (c_int, [c_vp, c_vp, c_i64, c_vp, c_i32, c_vp]),
+    "mb_dispatch_tables": (c_int, [c_i32, c_i32, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp,
+                                   c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "mb_zero_pad_rows_nb": (c_int, [c_vp, c_i64, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "mb_scatter_rows": (c_int, [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_i32, c_vp]),
     "mb_set_comm_blocks": (c_int, [c_i32]),

@@ -1,5 +1,6 @@
 // Host launcher + C-ABI for the K4 tcgen05 grouped GEMM (grouped_gemm.cuh: 1-CTA 128xBN
 // tiles; grouped_gemm_pair.cuh: CTA-pair 256x256 tiles, the default when the shape allows).
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 
@@ -40,6 +41,25 @@ static int launch_pair(const GemmParams& p, cudaStream_t stream, int sms) {
   const bool profile = false;
 #endif
   GemmParams q = p;
+  // dynamic tile scheduling: a zeroed counter per launch from a small ring (concurrent launches on
+  // different streams never share one); MB_GEMM_STATIC=1 keeps the static stride (A/B)
+  static int* counters = nullptr;
+  static std::atomic<unsigned> next_counter{0};
+  constexpr unsigned kCounters = 256;
+  static const bool static_sched = [] {
+    const char* e = std::getenv("MB_GEMM_STATIC");
+    return e && e[0] == '1';
+  }();
+  if (!static_sched) {
+    if (!counters) {
+      int* c = nullptr;
+      MB_CUDA_TRY(cudaMalloc(&c, kCounters * 32 * sizeof(int)));
+      MB_CUDA_TRY(cudaMemset(c, 0, kCounters * 32 * sizeof(int)));
+      counters = c;
+    }
+    q.tile_counter = counters + (next_counter.fetch_add(1) % kCounters) * 32;   // own 128-byte line
+    MB_CUDA_TRY(cudaMemsetAsync(q.tile_counter, 0, sizeof(int), stream));
+  }
   if (profile) {
     if (!prof) MB_CUDA_TRY(cudaMalloc(&prof, 8 * sizeof(unsigned long long)));
     MB_CUDA_TRY(cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), stream));

@@ -101,6 +101,7 @@ struct GemmParams {
   const float* rscale;  // per-row scale (gate) for EPI_DSWIGLU_GATED
   float* rpart;         // per-row partial sums [rows][N/64] for EPI_DSWIGLU_GATED
   unsigned long long* prof;  // optional wait-cycle counters (MB_GEMM_PROF): producer/MMA/epilogue
+  int* tile_counter;    // CTA-pair kernel: zeroed counter for dynamic tile scheduling (nullptr = static)
   int debug;            // bit0: skip the epilogue (TMEM drained, nothing stored) -- profiling only
 };
 

@@ -51,8 +51,18 @@ struct PairCfg : PairTile {
   static constexpr int kMetaBytes = 512 + 4 * (kMaxGroups + 8);
   static constexpr int kSmemBytes = kStages * kStageBytes + kStagingBytes + kMetaBytes + 1024;
   static_assert(kSmemBytes <= 232448, "shared memory budget");
-  static_assert(2 * kStages * 8 + 4 * 8 + 4 <= 256 && 256 + 8 * kEpiWarps <= 512, "meta layout");
+  static_assert(2 * kStages * 8 + 4 * 8 + 4 <= 256 && 256 + 8 * kEpiWarps <= 320, "meta layout");
 };
+
+// Tile scheduling: the leader CTA's producer hands every tile id of its cluster, in order, to all
+// roles of both CTAs through a small ring in shared memory (ids written into both CTAs' rings,
+// full barriers completed with cluster-scope releases; the consumers -- leader MMA warp, both
+// CTAs' epilogue warps and the peer's producer -- free a slot on the leader's empty barrier).
+// Each cluster's first tile is its index; later ids come from a global atomic counter (dynamic:
+// a cluster that started late, or whose tiles were cheap, takes fewer tiles -- the GEMM adapts
+// to SMs the comm kernels hold) or, without a counter, from the static stride.
+constexpr int kTileRing = 8;
+constexpr int kTileConsumers = 2 + 2 * MB_PAIR_EPI_WARPS;
 
 template <bool kW>
 __device__ __forceinline__ TileCoord decode_tile_pair(int t, const int* tile_start, const GemmGroup* __restrict__ sg,
@@ -145,6 +155,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   uint64_t* hbar_base = reinterpret_cast<uint64_t*>(meta + 256);  // one per epilogue warp (H tile loads)
+  int* ring = reinterpret_cast<int*>(meta + 320);                   // tile ids [kTileRing]
+  uint64_t* tr_full = reinterpret_cast<uint64_t*>(meta + 352);      // [kTileRing], count 1
+  uint64_t* tr_empty = reinterpret_cast<uint64_t*>(meta + 416);     // [kTileRing] (leader), kTileConsumers
   int* tile_start = reinterpret_cast<int*>(meta + 512);
   const GemmGroup* __restrict__ sg = p.groups;   // group table: global memory (L1-cached), read per tile
 
@@ -170,6 +183,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
       mbar_init(&tempty_bar[i], 2 * Cfg::kEpiWarps);  // every epilogue warp of both CTAs
     }
     for (int i = 0; i < Cfg::kEpiWarps; ++i) mbar_init(&hbar_base[i], 1);
+    for (int i = 0; i < kTileRing; ++i) {
+      mbar_init(&tr_full[i], 1);
+      mbar_init(&tr_empty[i], kTileConsumers);
+    }
     fence_barrier_init();
     fence_proxy_async_smem();
   }
@@ -203,6 +220,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total_tiles = tile_start[ng];
+  // i-th tile id of this cluster (consumer side); the caller's lane 0 frees the slot
+  auto take_tile = [&](int i) -> int {
+    const int slot = i % kTileRing;
+    mbar_wait_cluster(&tr_full[slot], (i / kTileRing) & 1);
+    const int t = *reinterpret_cast<volatile int*>(&ring[slot]);
+    __syncwarp();
+    if (lane == 0) {
+      if (leader) mbar_arrive(&tr_empty[slot]);
+      else mbar_arrive_cluster(mapa_shared(smem_u32(&tr_empty[slot]), 0));
+    }
+    return t;
+  };
 #ifdef MB_GEMM_PROFILE
   constexpr bool kProf = true;   // build with -DMB_GEMM_PROFILE: per-role wait-cycle counters
 #else
@@ -216,7 +245,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cluster; t < total_tiles; t += nclusters) {
+      int t_next = cluster;
+      for (int i = 0;; ++i) {
+        int t;
+        if (leader) {   // publish the i-th tile id to both CTAs
+          t = t_next;
+          const int slot = i % kTileRing;
+          mbar_wait(&tr_empty[slot], ((i / kTileRing) & 1) ^ 1);
+          st_shared_cluster_u32(mapa_shared(smem_u32(&ring[slot]), 0), static_cast<uint32_t>(t));
+          st_shared_cluster_u32(mapa_shared(smem_u32(&ring[slot]), 1), static_cast<uint32_t>(t));
+          mbar_arrive_cluster(mapa_shared(smem_u32(&tr_full[slot]), 0));
+          mbar_arrive_cluster(mapa_shared(smem_u32(&tr_full[slot]), 1));
+          if (t >= total_tiles) break;
+          t_next = p.tile_counter ? nclusters + atomicAdd(p.tile_counter, 1) : t + nclusters;  // fetched early
+        } else {
+          const int slot = i % kTileRing;
+          mbar_wait_cluster(&tr_full[slot], (i / kTileRing) & 1);
+          t = *reinterpret_cast<volatile int*>(&ring[slot]);
+          mbar_arrive_cluster(mapa_shared(smem_u32(&tr_empty[slot]), 0));
+          if (t >= total_tiles) break;
+        }
         const TileCoord tc = decode_tile_pair<kW>(t, tile_start, sg, ng, p);
         const GemmGroup gg = sg[tc.g];
         const CUtensorMap* tmB = (gg.flags & 2) ? &p.tmB1 : &p.tmB0;
@@ -280,8 +328,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
       constexpr uint32_t idesc_h = make_idesc_bf16(128, 128, kAmn ? 1u : 0u, kBmn ? 1u : 0u);
       int stage = 0;
       uint32_t phase = 0;
-      int it = 0;
-      for (int t = cluster; t < total_tiles; t += nclusters, ++it) {
+      for (int it = 0;; ++it) {
+        const int slot = it % kTileRing;
+        mbar_wait_cluster(&tr_full[slot], (it / kTileRing) & 1);
+        const int t = *reinterpret_cast<volatile int*>(&ring[slot]);
+        mbar_arrive(&tr_empty[slot]);
+        if (t >= total_tiles) break;
         const TileCoord tc = decode_tile_pair<kW>(t, tile_start, sg, ng, p);
         const int acc = it & 1;
         {
@@ -343,8 +395,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
     BoxStager<1> st{sStage + (warp - 2) * Cfg::kBoxBytes, 0, lane, p.debug};
     uint64_t* hbar = hbar_base + (warp - 2);
     uint32_t hphase = 0;
-    int it = 0;
-    for (int t = cluster; t < total_tiles; t += nclusters, ++it) {
+    for (int it = 0;; ++it) {
+      const int t = take_tile(it);
+      if (t >= total_tiles) break;
       const TileCoord tc = decode_tile_pair<kW>(t, tile_start, sg, ng, p);
       const GemmGroup gg = sg[tc.g];
       const int acc = it & 1;

@@ -118,6 +118,7 @@ class StepPlan:
     rep_experts: list = field(default_factory=list)   # per GPU: sorted experts replicated onto it this step
     slots: int = 0
     mats: np.ndarray | None = None  # (MB, G, E) routing counts the plan was built for
+    tables: str = "host"            # where the split / dispatch tables were computed ("host" | "device")
 
     def predicted_ms(self, topo: ClusterTopology, model: rt.ModelProfile, hw: HardwareProfile) -> float:
         """The reference cost model's time for this step (sum over micro-batches of
@@ -150,18 +151,68 @@ class StepPlan:
 
 
 def build_step_plan(policy: str, mats: np.ndarray, topo: ClusterTopology, model: rt.ModelProfile,
-                    hw: HardwareProfile, cfgs: pol.SimConfigs, shape: LayerShape) -> StepPlan:
+                    hw: HardwareProfile, cfgs: pol.SimConfigs, shape: LayerShape,
+                    device_tables: bool = False) -> StepPlan:
     """Plan one step (one batch of MB micro-batches, one layer) from the gathered (MB, G, E)
     routing matrices, with the reference policies (sim.build_policy_bundle, sim.py:214-280).
-    'balanced_oracle' is planned like 'static': its token routing must already be uniform."""
+    'balanced_oracle' is planned like 'static': its token routing must already be uniform.
+    device_tables: the integer split and dispatch tables are computed on the GPU
+    (mb_dispatch_tables) instead of the host planner library (identical tables)."""
     trace = rt.build_trace(model, topo, mats[:, None], tokens_per_gpu=0)
     pol_name = "static" if policy == "balanced_oracle" else policy
     bundle, _ = pol.build_policy_bundle(trace, pol_name, topo, model, hw, cfgs)
-    return step_plan_from_bundle(policy, bundle, mats, shape, layer=0, slots=cfgs.replica.slots_per_gpu)
+    return step_plan_from_bundle(policy, bundle, mats, shape, layer=0, slots=cfgs.replica.slots_per_gpu,
+                                 device_tables=device_tables)
+
+
+def _device_dispatch_tables(x: np.ndarray, home: np.ndarray, placement, split, maxc: int, max_slots: int):
+    """mb_dispatch_tables for one micro-batch: (counts dict, host tables..., device tables)."""
+    g, e = x.shape
+    dev = torch.device("cuda", torch.cuda.current_device())
+    order = list(placement.replicas.keys())
+    ptrs, gpus, fr = [0], [], []
+    for ex in order:
+        cps = placement.copies(ex)
+        frac = np.asarray(split.fractions[ex], dtype=np.float64)
+        if frac.shape != (g, len(cps)):
+            raise ValueError(f"fractions of expert {ex} have shape {frac.shape}, placement has {len(cps)} copies")
+        gpus.extend(cps[1:])
+        ptrs.append(len(gpus))
+        fr.append(frac.ravel())
+    i32 = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32).reshape(-1), device=dev)
+    xd, hd = i32(x), i32(home)
+    rep_e, rep_p, rep_g = i32(order if order else [0]), i32(ptrs), i32(gpus if gpus else [0])
+    frac_d = torch.as_tensor(np.concatenate(fr) if fr else np.zeros(1), dtype=torch.float64, device=dev)
+    ncnt = sum(g * (1 + len(placement.replicas[ex])) for ex in order)
+    out = {"counts": torch.zeros(max(1, ncnt), dtype=torch.int64, device=dev),
+           "route_tab": torch.empty((g, e, maxc, 4), dtype=torch.int32, device=dev),
+           "ncopies": torch.empty(e, dtype=torch.int32, device=dev),
+           "slot_tab": torch.empty((g, max_slots, 4), dtype=torch.int32, device=dev),
+           "slot_w": torch.empty((g, max_slots, 2), dtype=torch.int32, device=dev),
+           "nslots": torch.empty(g, dtype=torch.int32, device=dev),
+           "total_rows": torch.empty(g, dtype=torch.int64, device=dev),
+           "flow": torch.empty((g, g), dtype=torch.int64, device=dev),
+           "error": torch.zeros(1, dtype=torch.int32, device=dev)}
+    lib = nat.kernels()
+    nat.check(lib.mb_dispatch_tables(g, e, xd.data_ptr(), hd.data_ptr(), len(order), rep_e.data_ptr(),
+                                     rep_p.data_ptr(), rep_g.data_ptr(), frac_d.data_ptr(), PAD, maxc, max_slots,
+                                     out["counts"].data_ptr(), out["route_tab"].data_ptr(), out["ncopies"].data_ptr(),
+                                     out["slot_tab"].data_ptr(), out["slot_w"].data_ptr(), out["nslots"].data_ptr(),
+                                     out["total_rows"].data_ptr(), out["flow"].data_ptr(), out["error"].data_ptr(),
+                                     nat.stream_ptr()), lib, "mb_dispatch_tables")
+    host = {k: v.cpu().numpy() for k, v in out.items()}
+    if int(host["error"][0]):
+        raise ValueError(f"mb_dispatch_tables: inconsistent plan (error bits {int(host['error'][0])})")
+    counts, off = {}, 0
+    for ex in order:
+        k = 1 + len(placement.replicas[ex])
+        counts[ex] = host["counts"][off:off + g * k].reshape(g, k).astype(np.int64)
+        off += g * k
+    return counts, host, out
 
 
 def step_plan_from_bundle(policy: str, bundle: pol.PlanBundle, mats: np.ndarray, shape: LayerShape,
-                          layer: int = 0, slots: int = 0) -> StepPlan:
+                          layer: int = 0, slots: int = 0, device_tables: bool = False) -> StepPlan:
     """Device tables of one layer's step from a PlanBundle (planned here, or loaded from the
     reorder.json / replication.json files of planio.solve or the reference's `solve`)."""
     mbs_n, g, e = mats.shape
@@ -178,13 +229,25 @@ def step_plan_from_bundle(policy: str, bundle: pol.PlanBundle, mats: np.ndarray,
             placement, split = rep.ReplicaPlacement(home=home.copy()), rep.SplitPlan()
         else:
             placement, split = entry.placement, entry.split
-        counts = rep.round_split(split, placement, x)
+        counts = None if device_tables else rep.round_split(split, placement, x)
         entries.append((placement, counts))
     plan.maxc = max([1] + [1 + len(p.replicas.get(ex, [])) for p, _ in entries for ex in p.replicas])
     per_gpu_rep = max([0] + [int(p.slot_usage(g).max()) for p, _ in entries])
     plan.max_slots = e // g + max(1, slots, per_gpu_rep)
     lib = nat.planner()
-    for mb, (placement, counts) in enumerate(entries):
+    if device_tables:
+        for mb in range(mbs_n):
+            entry = bundle.replication.entries.get((mb, layer))
+            placement = entries[mb][0]
+            split = entry.split if entry is not None else rep.SplitPlan()
+            counts, h, d = _device_dispatch_tables(np.asarray(mats[mb]), home, placement, split, plan.maxc,
+                                                   plan.max_slots)
+            mbp = MicroBatchPlan(placement, counts, h["route_tab"], h["ncopies"], h["slot_tab"], h["slot_w"],
+                                 h["nslots"], h["total_rows"], h["flow"])
+            mbp.device = d          # the tables the kernels consume, computed on the GPU
+            plan.mbs.append(mbp)
+        plan.tables = "device"
+    for mb, (placement, counts) in enumerate(entries if not device_tables else []):
         x = np.ascontiguousarray(mats[mb], dtype=np.int64)
         order = list(placement.replicas.keys())
         rep_e = nat.i32(order)
@@ -625,11 +688,19 @@ class MoEDataPlane:
                     if sww[s, 1] and stt[s, 1] > 0:
                         rr[(p, int(stt[s, 3]))] = (int(sww[s, 0]), int(stt[s, 1]))
             rep_rows.append(rr)
+        devs = [getattr(mbp, "device", None) for mbp in plan.mbs]
+        if all(t is not None for t in devs):   # tables computed on the GPU (mb_dispatch_tables): use them as is
+            route_dev = torch.stack([t["route_tab"][d] for t in devs])
+            ncop_dev = torch.stack([t["ncopies"] for t in devs])
+            slot_dev = torch.stack([t["slot_tab"][d] for t in devs])
+        else:
+            route_dev = torch.from_numpy(np.stack(route)).to(dev)
+            ncop_dev = torch.from_numpy(np.stack(ncop)).to(dev)
+            slot_dev = torch.from_numpy(np.stack(slots)).to(dev)
         at = {"home_experts": home_experts, "mb_rep": mb_rep, "nslots": nsl,
-              "route_tab": torch.from_numpy(np.stack(route)).to(dev),
-              "ncopies": torch.from_numpy(np.stack(ncop)).to(dev),
+              "route_tab": route_dev, "ncopies": ncop_dev,
               "groups": torch.from_numpy(np.stack(groups)).to(dev),
-              "slot_tab": torch.from_numpy(np.stack(slots)).to(dev),
+              "slot_tab": slot_dev,
               "expected": (torch.from_numpy(np.ascontiguousarray(plan.mats[:, d], dtype=np.int32)).to(dev)
                            if plan.mats is not None else None)}
 
