@@ -42,26 +42,19 @@ def load_peaks():
         return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
 
 
-K4_TRAFFIC = os.path.join(ROOT, "profiles", "r01_launches_step2_summary.json")
+K4_TRAFFIC = os.path.join(ROOT, "profiles", "r02_launches_step_summary.json")
 
 
 def k4_traffic_per_step(config: str, world: int, tokens: int, mbs: int):
-    """DRAM bytes (read + write) of every K4 launch of one step, from the committed ncu launch
-    list of this same bench command (dram__bytes_read.sum + dram__bytes_write.sum per launch);
-    None for other configurations (no capture)."""
+    """DRAM bytes (read + write) of every K4 launch of ONE step, from the committed ncu launch list
+    of that step of this bench command (the NVTX range "mb_step", dram__bytes_read.sum +
+    dram__bytes_write.sum per launch, tools/ncu_step.sh); None for other configurations."""
     if (config, world, tokens, mbs) != ("qwen3-30b-a3b", 1, 8192, 8):
         return None
     try:
-        rows = json.load(open(K4_TRAFFIC))
-    except (OSError, ValueError):
+        return float(json.load(open(K4_TRAFFIC))["totals"]["k4_dram_bytes"])
+    except (OSError, ValueError, KeyError):
         return None
-    total = 0.0
-    for key, r in rows.items():
-        if not key.startswith("K4"):
-            continue
-        per_step = 2 if key.endswith("<1, 1, 1, 3>") else mbs   # wgrad: 2 launches per step
-        total += (r["dram_read_per_launch"] + r["dram_write_per_launch"]) * per_step
-    return total
 
 
 class ClockSampler:
@@ -313,6 +306,13 @@ def measure_detail(args, comm, dp, dev, plan, topo, model):
                                   "gb_per_s": round(v[1] / v[0] / 1e6, 1) if v[0] > 0 else 0.0}
                          for kd, v in kinds.items() if kd.startswith("comm_")}
     res["gemm_launches"] = len(gev) // args.steps
+    if os.environ.get("MB_NVTX_STEP") == "1":
+        # one more step inside an NVTX range: ncu --nvtx --nvtx-include "mb_step/" profiles exactly it
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_push("mb_step")
+        _step(dp, dev)
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
     # e2e through the host-buffer API (pinned host tensors, copies inside the timed region)
     host = {k: v.cpu().pin_memory() for k, v in dev.items()}
     for _ in range(2):
@@ -494,7 +494,7 @@ def run_ours(args, comm):
     model = ModelProfile(1, shape.num_experts, shape.top_k, shape.hidden, shape.ffn)
     slots = cfg["slots"] if args.slots is None else args.slots
     cfgs = SimConfigs(anneal=AnnealConfig(seeds=tuple(range(args.sa_chains))), replica=ReplicaConfig(slots),
-                      threads=min(8, os.cpu_count() or 1), device_anneal=args.device_planner)
+                      threads=1, device_anneal=args.device_planner)   # tasks in parallel threads measured slower (numpy BLAS lock)
     trace, bundle = None, None
     if args.trace:
         # replay a recorded count trace (routing.bin + manifest.json, either implementation):

@@ -67,6 +67,15 @@ int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t a_cols, con
                     const void* aux, int64_t ld_aux, const float* row_scale, float* row_partial, int32_t gemm_sms,
                     void* stream);
 
+/* Both weight gradients of the expert FFN in ONE persistent launch (one dynamically scheduled tile
+ * list): groups without flag 4 compute C0_slot[M0][N0] (+)= A0[K_g, M0]^T . B0[K_g, N0] (dW2 =
+ * dY^T Act), groups with flag 4 compute C1_slot[M1][N1] (+)= A1^T . B1 (dW1 = dH^T X); A*, B* are
+ * [k_rows, .] bf16 row-major, C* fp32 [slots][M][N]; groups / segs as MB_GEMM_WGRAD (flag 1 =
+ * accumulate).  Replaces: the wgrad third of costmodel.comp_time (12 h h' of the 18 per row). */
+int mb_grouped_wgrad2(const void* A0, const void* B0, int32_t M0, int32_t N0, void* C0, const void* A1,
+                      const void* B1, int32_t M1, int32_t N1, void* C1, int64_t k_rows, const void* groups,
+                      const void* segs, int num_groups, int32_t gemm_sms, void* stream);
+
 /* ---------------------------------------------------------------- K2 permutation
  * chunk_base[b][c][e] = exclusive prefix over chunks of chunk_counts (from mb_expert_histogram). */
 int mb_chunk_scan(const uint32_t* chunk_counts, uint32_t* chunk_base, int64_t nb, int32_t chunks, int32_t E,

@@ -46,6 +46,8 @@ _KERNEL_SIGS = {
 }
 
 _KERNEL_SIGS.update({
+    "mb_grouped_wgrad2": (c_int, [c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_i64, c_vp, c_vp,
+                                  c_int, c_i32, c_vp]),
     "mb_chunk_scan": (c_int, [c_vp, c_vp, c_i64, c_i32, c_i32, c_vp]),
     "mb_permute_rank": (c_int, [c_vp, c_i64, c_i32, c_vp, c_i32, c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp,
                                 c_vp]),

@@ -104,6 +104,40 @@ static bool pair_enabled() {
 
 using namespace mb;
 
+extern "C" int mb_grouped_wgrad2(const void* A0, const void* B0, int32_t M0, int32_t N0, void* C0, const void* A1,
+                                 const void* B1, int32_t M1, int32_t N1, void* C1, int64_t k_rows,
+                                 const void* groups, const void* segs, int num_groups, int32_t gemm_sms,
+                                 void* stream) {
+  MB_CHECK_ARG(num_groups >= 0 && num_groups <= kMaxGroups, "num_groups %d outside [0, %d]", num_groups, kMaxGroups);
+  MB_CHECK_ARG(A0 && B0 && C0 && A1 && B1 && C1 && groups && k_rows > 0, "null wgrad operand");
+  MB_CHECK_ARG(M0 % 256 == 0 && N0 % 256 == 0 && M1 % 256 == 0 && N1 % 256 == 0,
+               "two-problem wgrad needs M and N multiples of 256 (M0=%d N0=%d M1=%d N1=%d)", M0, N0, M1, N1);
+  if (num_groups == 0) return MB_OK;
+  GemmParams p{};
+  p.groups = reinterpret_cast<const GemmGroup*>(groups);
+  p.segs = reinterpret_cast<const GemmSeg*>(segs);
+  p.num_groups = num_groups;
+  p.M = M0; p.N = N0; p.M2 = M1; p.N2 = N1; p.K = 0;
+  p.C = C0; p.ldc = N0; p.c_slot_stride = static_cast<int64_t>(M0) * N0;
+  if (const char* dbg = std::getenv("MB_GEMM_DEBUG")) p.debug = std::atoi(dbg);
+  int rc;
+  // problem 0 (groups without flag 4): A0 [k_rows, M0], B0 [k_rows, N0] -> C0 [slots][M0][N0]
+  if ((rc = make_tmap_bf16_2d(&p.tmA, A0, M0, k_rows, int64_t(M0) * 2, 64, 64))) return rc;
+  if ((rc = make_tmap_bf16_2d(&p.tmB0, B0, N0, k_rows, int64_t(N0) * 2, 64, 64))) return rc;
+  if ((rc = make_tmap_2d(&p.tmC, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, C0, N0, static_cast<uint64_t>(M0) * kMaxGroups,
+                         int64_t(N0) * 4, 32, 32)))
+    return rc;
+  // problem 1 (flag 4): A1 [k_rows, M1], B1 [k_rows, N1] -> C1 [slots][M1][N1]
+  if ((rc = make_tmap_bf16_2d(&p.tmAh, A1, M1, k_rows, int64_t(M1) * 2, 64, 64))) return rc;
+  if ((rc = make_tmap_bf16_2d(&p.tmB0h, B1, N1, k_rows, int64_t(N1) * 2, 64, 64))) return rc;
+  if ((rc = make_tmap_2d(&p.tmC2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, C1, N1, static_cast<uint64_t>(M1) * kMaxGroups,
+                         int64_t(N1) * 4, 32, 32)))
+    return rc;
+  p.tmB1 = p.tmB0;
+  p.tmB1h = p.tmB0h;
+  return launch_pair<true, true, true, EPI_ACC_F32>(p, reinterpret_cast<cudaStream_t>(stream), gemm_sms);
+}
+
 extern "C" int mb_set_gemm_sms(int sms) {
   MB_CHECK_ARG(sms >= 0, "sms must be >= 0 (0 = all)");
   g_gemm_sms = sms;

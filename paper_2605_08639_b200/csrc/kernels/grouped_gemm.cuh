@@ -102,6 +102,7 @@ struct GemmParams {
   float* rpart;         // per-row partial sums [rows][N/64] for EPI_DSWIGLU_GATED
   unsigned long long* prof;  // optional wait-cycle counters (MB_GEMM_PROF): producer/MMA/epilogue
   int* tile_counter;    // CTA-pair kernel: zeroed counter for dynamic tile scheduling (nullptr = static)
+  int M2, N2;           // W mode, groups with flag 4: the second problem (A = tmAh, B = tmB0h, C = tmC2)
   int debug;            // bit0: skip the epilogue (TMEM drained, nothing stored) -- profiling only
 };
 

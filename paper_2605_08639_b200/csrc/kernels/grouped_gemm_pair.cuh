@@ -75,7 +75,7 @@ __device__ __forceinline__ TileCoord decode_tile_pair(int t, const int* tile_sta
   TileCoord c;
   c.g = lo;
   const int local = t - tile_start[lo];
-  const int n_tiles = p.N / PairTile::TN;
+  const int n_tiles = (kW && (sg[lo].flags & 4) ? p.N2 : p.N) / PairTile::TN;
   c.mb = local / n_tiles;
   c.nb = local - c.mb * n_tiles;
   c.kblocks = kW ? w_kblocks(sg[lo]) : (p.K / BK);
@@ -200,7 +200,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
       int cnt = 0;
       if (i < ng) {
         const GemmGroup gg = sg[i];
-        if (kW) cnt = (gg.rows > 0) ? (p.M / TM) * n_tiles : 0;
+        if (kW) cnt = (gg.rows > 0) ? ((gg.flags & 4) ? (p.M2 / TM) * (p.N2 / TN) : (p.M / TM) * n_tiles) : 0;
         else cnt = ((gg.rows + TM - 1) / TM) * n_tiles;
       }
       int incl = cnt;
@@ -267,7 +267,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
         }
         const TileCoord tc = decode_tile_pair<kW>(t, tile_start, sg, ng, p);
         const GemmGroup gg = sg[tc.g];
-        const CUtensorMap* tmB = (gg.flags & 2) ? &p.tmB1 : &p.tmB0;
+        const CUtensorMap* tmB = (gg.flags & 2) ? &p.tmB1 : ((kW && (gg.flags & 4)) ? &p.tmB0h : &p.tmB0);
         const CUtensorMap* tmBh = (gg.flags & 2) ? &p.tmB1h : &p.tmB0h;
         const bool half = !kW && half_tile(gg, tc, p.debug);
         const int bytes = half ? 2 * (Cfg::kABytes / 2 + Cfg::kBBytes) : 2 * Cfg::kStageBytes;
@@ -294,9 +294,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
             else tma_load_2d_pair(a_dst, &p.tmA, lbar, (p.debug & 64) ? 0 : kb * BK,
                                   (p.debug & 64) ? rank * 128 : gg.a0 + tc.mb * TM + rank * 128);
           } else {
+            const CUtensorMap* tmA_w = (kW && (gg.flags & 4)) ? &p.tmAh : &p.tmA;   // W: second problem
 #pragma unroll
             for (int j = 0; j < 2; ++j)
-              tma_load_2d_pair(a_dst + j * 8192, &p.tmA, lbar, tc.mb * TM + rank * 128 + j * 64, krow);
+              tma_load_2d_pair(a_dst + j * 8192, tmA_w, lbar, tc.mb * TM + rank * 128 + j * 64, krow);
           }
           if (!kBmn) {
             if (half) {
@@ -439,7 +440,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
       // dSwiGLU epilogues); the SwiGLU epilogue needs gate and up of a feature in one warp, so
       // there the ch2 = 1 warps idle
       const bool valid = (kW || warp_row0 < gg.rows) && !(half && ch2 && kEpi == EPI_SWIGLU);
-      const int32_t out_row0 = kW ? gg.slot * p.M + warp_row0 : gg.a0 + warp_row0;
+      const int32_t out_row0 = kW ? gg.slot * ((gg.flags & 4) ? p.M2 : p.M) + warp_row0 : gg.a0 + warp_row0;
 
       if (p.debug & 1) {
         uint32_t r[32];
@@ -599,6 +600,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
           }
         } else {  // EPI_ACC_F32: fp32 boxes of 32 columns, reduce-add into the accumulator or store
           const bool accumulate = (gg.flags & 1) != 0;
+          const CUtensorMap* tmCw = (gg.flags & 4) ? &p.tmC2 : &p.tmC;   // second wgrad problem
           uint32_t r0[32], r1[32], r2[32], r3[32];
           tmem_ld_32x32b_x32(t_acc + ch2 * 128, r0);
           tmem_ld_32x32b_x32(t_acc + ch2 * 128 + 32, r1);
@@ -608,15 +610,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
           release();
           const int32_t c0 = tc.nb * TN + ch2 * 128;
           if (accumulate) {
-            st.template put<true>(r0, &p.tmC, c0, out_row0);
-            st.template put<true>(r1, &p.tmC, c0 + 32, out_row0);
-            st.template put<true>(r2, &p.tmC, c0 + 64, out_row0);
-            st.template put<true>(r3, &p.tmC, c0 + 96, out_row0);
+            st.template put<true>(r0, tmCw, c0, out_row0);
+            st.template put<true>(r1, tmCw, c0 + 32, out_row0);
+            st.template put<true>(r2, tmCw, c0 + 64, out_row0);
+            st.template put<true>(r3, tmCw, c0 + 96, out_row0);
           } else {
-            st.template put<false>(r0, &p.tmC, c0, out_row0);
-            st.template put<false>(r1, &p.tmC, c0 + 32, out_row0);
-            st.template put<false>(r2, &p.tmC, c0 + 64, out_row0);
-            st.template put<false>(r3, &p.tmC, c0 + 96, out_row0);
+            st.template put<false>(r0, tmCw, c0, out_row0);
+            st.template put<false>(r1, tmCw, c0 + 32, out_row0);
+            st.template put<false>(r2, tmCw, c0 + 64, out_row0);
+            st.template put<false>(r3, tmCw, c0 + 96, out_row0);
           }
         }
       }

@@ -21,6 +21,8 @@ GEMM_DGRAD_DSWIGLU_GATED = 5
 GROUP_FIELDS = 8  # int32 rows, a0, slot, flags, seg_begin, seg_count, pad, pad
 FLAG_ACCUMULATE = 1
 FLAG_REPLICA = 2
+FLAG_PROBLEM2 = 4   # grouped_wgrad2: the group belongs to the second problem (dW1)
+MAX_GROUPS = 256    # groups per launch (kMaxGroups)
 
 
 def _lib():
@@ -100,3 +102,27 @@ def grouped_gemm(mode: int, A: torch.Tensor, B0: torch.Tensor, groups: torch.Ten
                                   C.data_ptr(), ldc, c_slot_stride, nat.ptr(C2), ldc2, nat.ptr(aux), ld_aux,
                                   nat.ptr(row_scale), nat.ptr(row_partial), int(sms), nat.stream_ptr(stream)),
               lib, "mb_grouped_gemm")
+
+
+def grouped_wgrad2(A0: torch.Tensor, B0: torch.Tensor, C0: torch.Tensor, A1: torch.Tensor, B1: torch.Tensor,
+                   C1: torch.Tensor, groups: torch.Tensor, segs: torch.Tensor | None = None, sms: int = 0,
+                   stream=None) -> None:
+    """K4 wgrad of both FFN weights in one launch: groups without FLAG_PROBLEM2 give
+    C0[slot] (+)= A0^T B0 (A0 [K, M0], B0 [K, N0]), groups with it C1[slot] (+)= A1^T B1."""
+    _need_cuda(A0, B0, C0, A1, B1, C1, groups)
+    for t in (A0, B0, A1, B1):
+        if t.dtype != torch.bfloat16 or not t.is_contiguous():
+            raise ValueError("wgrad operands must be contiguous bf16")
+    for t in (C0, C1):
+        if t.dtype != torch.float32 or not t.is_contiguous():
+            raise ValueError("wgrad outputs must be contiguous fp32")
+    if groups.dtype != torch.int32 or groups.dim() != 2 or groups.shape[1] != GROUP_FIELDS:
+        raise ValueError("groups must be an int32 [G, 8] table")
+    k_rows = A0.numel() // A0.shape[-1]
+    if any(t.numel() // t.shape[-1] != k_rows for t in (B0, A1, B1)):
+        raise ValueError("wgrad operands must have the same number of K rows")
+    M0, N0, M1, N1 = A0.shape[-1], B0.shape[-1], A1.shape[-1], B1.shape[-1]
+    lib = _lib()
+    nat.check(lib.mb_grouped_wgrad2(A0.data_ptr(), B0.data_ptr(), M0, N0, C0.data_ptr(), A1.data_ptr(),
+                                    B1.data_ptr(), M1, N1, C1.data_ptr(), k_rows, groups.data_ptr(), nat.ptr(segs),
+                                    groups.shape[0], int(sms), nat.stream_ptr(stream)), lib, "mb_grouped_wgrad2")

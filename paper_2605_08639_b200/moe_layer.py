@@ -72,6 +72,8 @@ ROW_MOVERS_MULTI = "tma"
 # is idle (N=4: 18.9-19.0 -> 18.7-18.9 ms; at N=1 widening the single launch measured 3% slower).
 # MB_WGRAD_ALL_SMS=0: A/B.
 WGRAD_ALL_SMS = os.environ.get("MB_WGRAD_ALL_SMS", "1") == "1"
+# both weight gradients in one two-problem launch (mb_grouped_wgrad2); MB_WGRAD_MERGED=0: A/B
+WGRAD_MERGED = os.environ.get("MB_WGRAD_MERGED", "1") == "1"
 # overlap=False runs every phase in issue order on one stream with all SMs in the GEMM: at world 1
 # (local row movers) it measured the same step time as the overlapped schedule (19.6 vs 19.4 ms).
 CHUNK = 32      # tokens per permutation chunk
@@ -388,6 +390,16 @@ GRAD_RING = 2
 ACC_TASK = np.dtype([("dst", "<u8"), ("src", "<u8", (8,)), ("n", "<i8"), ("nsrc", "<i4"), ("store", "<i4")])
 ERR_BITS = {1: "routing has more tokens for an expert than the step plan's counts (perm dropped them)",
             2: "device histogram differs from the counts the step plan was built for"}
+
+
+def _wgrad_tables(tab: np.ndarray, dev) -> tuple:
+    """(single-problem table, two-problem table) of a wgrad group table: the second lists every
+    group twice, the copy flagged FLAG_PROBLEM2 (dW1 beside dW2 in one launch)."""
+    t2 = tab.copy()
+    t2[:, 3] |= K.FLAG_PROBLEM2
+    merged = np.concatenate([tab, t2]) if len(tab) * 2 <= K.MAX_GROUPS else None
+    return (torch.from_numpy(np.ascontiguousarray(tab)).to(dev),
+            None if merged is None else torch.from_numpy(np.ascontiguousarray(merged)).to(dev))
 
 
 def _wgrad_table(rows: list) -> np.ndarray:
@@ -743,7 +755,7 @@ class MoEDataPlane:
                 rows.append(group_row(segs, [(r0, r16(real))], q, 0))
                 a_rows += real
             if rows:
-                rw_mb[m] = (torch.from_numpy(_wgrad_table(rows)).to(dev), seg_tensor(segs), a_rows)
+                rw_mb[m] = (_wgrad_tables(_wgrad_table(rows), dev), seg_tensor(segs), a_rows)
             if self.wgrad_mode == "micro_batch":
                 segs, rows_f, real = [], [], 0
                 for ex, (r0, rr_) in sorted(home_slots[m].items()):
@@ -755,8 +767,7 @@ class MoEDataPlane:
                     tab_f = _wgrad_table(rows_f)
                     tab_a = tab_f.copy()
                     tab_a[:, 3] |= K.FLAG_ACCUMULATE   # an accumulating step adds every contribution
-                    w_mb[m] = (torch.from_numpy(tab_f).to(dev), torch.from_numpy(tab_a).to(dev), seg_tensor(segs),
-                               real)
+                    w_mb[m] = (_wgrad_tables(tab_f, dev), _wgrad_tables(tab_a, dev), seg_tensor(segs), real)
             # owner push-back tasks of micro-batch m (fresh variant: first contribution stores)
             if srcs_of[m]:
                 tasks = np.zeros(2 * len(srcs_of[m]), dtype=ACC_TASK)
@@ -810,7 +821,7 @@ class MoEDataPlane:
                 tab_acc[:, 3] |= K.FLAG_ACCUMULATE
                 if part == "A":      # replica gradients were pushed back first: always accumulate
                     tab_fresh[:, 3] |= K.FLAG_ACCUMULATE
-                wparts.append((torch.from_numpy(tab_fresh).to(dev), torch.from_numpy(tab_acc).to(dev), segs_t,
+                wparts.append((_wgrad_tables(tab_fresh, dev), _wgrad_tables(tab_acc, dev), segs_t,
                                float(sum(r for _, r in part_rows)), part))
         else:
             idle_home = [loc for loc in range(nh) if not written[loc]]
@@ -1378,13 +1389,27 @@ class _StepOps:
         self.rep_done.add(m)
         rw = dp.rw_mb[m]
         if rw is not None:
-            tab, segs, rrows = rw
+            tabs, segs, rrows = rw
             a, q = dp.set_index(m), m % GRAD_RING
             with dp._timed(6.0 * rrows * h * hp, "wgrad_replica"):
-                dp._gemm(K.GEMM_WGRAD, dp.dYr[a], dp.Act[a], tab, M=h, N=hp, C=dp.rgW2[q], c_slot_stride=h * hp,
-                         segs=segs)
-                dp._gemm(K.GEMM_WGRAD, dp.dH[a], dp.Xr[a], tab, M=2 * hp, N=h, C=dp.rgW1[q],
-                         c_slot_stride=2 * hp * h, segs=segs)
+                self._wgrad_launch(tabs, segs, dp.dYr[a], dp.Act[a], dp.rgW2[q], dp.dH[a], dp.Xr[a], dp.rgW1[q])
+
+    def _wgrad_launch(self, tabs, segs, dY, act, c2, dh, xr, c1, sms=None):
+        """dW2 (C2 (+)= dY^T act) and dW1 (C1 (+)= dH^T X) of the groups in `tabs`: one two-problem
+        launch (mb_grouped_wgrad2) unless MB_WGRAD_MERGED=0 or the doubled table is too long."""
+        dp = self.dp
+        h, hp = dp.shape.hidden, dp.shape.ffn
+        single, merged = tabs
+        R = dY.numel() // h
+        if WGRAD_MERGED and merged is not None:
+            K.grouped_wgrad2(dY.view(R, h), act.view(R, hp), c2, dh.view(R, 2 * hp), xr.view(R, h), c1, merged,
+                             segs=segs, sms=dp.gemm_sms if sms is None else sms)
+            dp.launches += 1
+            return
+        dp._gemm(K.GEMM_WGRAD, dY.view(R, h), act.view(R, hp), single, M=h, N=hp, C=c2, c_slot_stride=h * hp,
+                 segs=segs, sms=sms)
+        dp._gemm(K.GEMM_WGRAD, dh.view(R, 2 * hp), xr.view(R, h), single, M=2 * hp, N=h, C=c1,
+                 c_slot_stride=2 * hp * h, segs=segs, sms=sms)
 
     def wgrad_mb(self, m):
         """W(m) (wgrad_mode "micro_batch"): home weight gradients of micro-batch m, K = its rows."""
@@ -1392,28 +1417,20 @@ class _StepOps:
         w = dp.w_mb[m]
         if w is None:
             return
-        tab_fresh, tab_acc, segs, rows = w
-        tab = tab_fresh if self.fresh else tab_acc
+        tabs_fresh, tabs_acc, segs, rows = w
         h, hp = dp.shape.hidden, dp.shape.ffn
         a = dp.set_index(m)
-        with dp._timed(2.0 * rows * h * hp, "wgrad_down"):
-            dp._gemm(K.GEMM_WGRAD, dp.dYr[a], dp.Act[a], tab, M=h, N=hp, C=dp.gW2, c_slot_stride=h * hp, segs=segs)
-        with dp._timed(4.0 * rows * h * hp, "wgrad_gate_up"):
-            dp._gemm(K.GEMM_WGRAD, dp.dH[a], dp.Xr[a], tab, M=2 * hp, N=h, C=dp.gW1, c_slot_stride=2 * hp * h,
-                     segs=segs)
+        with dp._timed(6.0 * rows * h * hp, "wgrad"):
+            self._wgrad_launch(tabs_fresh if self.fresh else tabs_acc, segs, dp.dYr[a], dp.Act[a], dp.gW2, dp.dH[a],
+                               dp.Xr[a], dp.gW1)
 
     def _wgrad_step(self, part, sms):
         dp = self.dp
-        tab_fresh, tab_acc, segs, rows, _ = part
-        tab = tab_fresh if self.fresh else tab_acc
+        tabs_fresh, tabs_acc, segs, rows, _ = part
         h, hp = dp.shape.hidden, dp.shape.ffn
-        NA, R = dp.NA, dp.R
-        with dp._timed(2.0 * rows * h * hp, "wgrad_down"):
-            dp._gemm(K.GEMM_WGRAD, dp.dYr.view(NA * R, h), dp.Act.view(NA * R, hp), tab, M=h, N=hp, C=dp.gW2,
-                     c_slot_stride=h * hp, segs=segs, sms=sms)
-        with dp._timed(4.0 * rows * h * hp, "wgrad_gate_up"):
-            dp._gemm(K.GEMM_WGRAD, dp.dH.view(NA * R, 2 * hp), dp.Xr.view(NA * R, h), tab, M=2 * hp, N=h, C=dp.gW1,
-                     c_slot_stride=2 * hp * h, segs=segs, sms=sms)
+        with dp._timed(6.0 * rows * h * hp, "wgrad"):
+            self._wgrad_launch(tabs_fresh if self.fresh else tabs_acc, segs, dp.dYr, dp.Act, dp.gW2, dp.dH, dp.Xr,
+                               dp.gW1, sms=sms)
 
     def finish(self, last_x_ev):
         """Step mode: home weight gradients over every micro-batch (part B: experts without

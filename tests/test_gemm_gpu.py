@@ -276,3 +276,37 @@ def test_fused_combine_backward_matches_unfused_path():
         assert rel_err(part[sl].sum(1), dgate[sl]) < 2e-2
         pad = slice(a0[i] + real[i], a0[i] + rows[i])
         assert torch.all(dH1[pad] == 0) and torch.all(dy[pad] == 0)
+
+
+def test_wgrad_two_problems_one_launch():
+    """mb_grouped_wgrad2: dW2 and dW1 of every group in one dynamically scheduled launch are
+    bit-identical to the two single-problem launches (same tiles, same K order)."""
+    torch.manual_seed(11)
+    h, hp = 512, 256
+    R = 1024
+    dY = torch.randn(R, h, device=DEV).bfloat16()
+    act = torch.randn(R, hp, device=DEV).bfloat16()
+    dH = torch.randn(R, 2 * hp, device=DEV).bfloat16()
+    X = torch.randn(R, h, device=DEV).bfloat16()
+    segs_g = [[(0, 48), (512, 112)], [(256, 64), (640, 208)], [(900, 16)]]
+    segs, seg_begin, seg_count, tot, kblocks = [], [], [], [], []
+    for sg in segs_g:
+        seg_begin.append(len(segs))
+        seg_count.append(len(sg))
+        segs.extend(sg)
+        tot.append(sum(r for _, r in sg))
+        kblocks.append(sum((r + 63) // 64 for _, r in sg))
+    flags = [0, K.FLAG_ACCUMULATE, 0]
+    single = K.make_groups(tot, [0] * 3, [2, 0, 1], flags, seg_begin, seg_count, kblocks=kblocks)
+    merged = torch.cat([single, single.clone()])
+    merged[3:, 3] |= K.FLAG_PROBLEM2
+    segs_t = torch.tensor(segs, dtype=torch.int32, device=DEV)
+    C2a, C1a = torch.randn(3, h, hp, device=DEV), torch.randn(3, 2 * hp, h, device=DEV)
+    C2b, C1b = C2a.clone(), C1a.clone()
+    K.grouped_gemm(K.GEMM_WGRAD, dY, act, single, M=h, N=hp, C=C2a, c_slot_stride=h * hp, segs=segs_t)
+    K.grouped_gemm(K.GEMM_WGRAD, dH, X, single, M=2 * hp, N=h, C=C1a, c_slot_stride=2 * hp * h, segs=segs_t)
+    K.grouped_wgrad2(dY, act, C2b, dH, X, C1b, merged, segs=segs_t)
+    torch.cuda.synchronize()
+    assert torch.equal(C2a, C2b) and torch.equal(C1a, C1b)
+    ref = sum(dY[a:a + r].float().T @ act[a:a + r].float() for a, r in segs_g[2])
+    assert rel_err(C2b[1], ref) < 1e-3

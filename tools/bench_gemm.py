@@ -80,6 +80,19 @@ def main():
     if not only or "dgrad_dx" in only: res["dgrad_dx"] = (timeit(lambda: K.grouped_gemm(K.GEMM_DGRAD_STORE, dH, W1, groups, N=h, K=2 * hp, C=dX)), 2 * flop)
     if not only or "wgrad_w2" in only: res["wgrad_w2"] = (timeit(lambda: K.grouped_gemm(K.GEMM_WGRAD, dY, Act, wg, M=h, N=hp, C=gW2, c_slot_stride=h * hp)), flop)
     if not only or "wgrad_w1" in only: res["wgrad_w1"] = (timeit(lambda: K.grouped_gemm(K.GEMM_WGRAD, dH, X, wg, M=2 * hp, N=h, C=gW1, c_slot_stride=2 * hp * h)), 2 * flop)
+    if only and "wgrad2" in only:
+        # the step's weight-gradient launch: both weights of every group in one two-problem launch,
+        # K = the group's rows over 8 micro-batches (wgrad_mode "step")
+        R8 = 8 * R
+        dY8 = torch.randn(R8, h, device=dev).bfloat16()
+        act8 = torch.randn(R8, hp, device=dev).bfloat16()
+        dH8 = torch.randn(R8, 2 * hp, device=dev).bfloat16()
+        X8 = torch.randn(R8, h, device=dev).bfloat16()
+        tab = K.make_groups([8 * r for r in rows], [8 * a for a in a0], list(range(G)))
+        tab2 = tab.clone()
+        tab2[:, 3] |= K.FLAG_PROBLEM2
+        merged = torch.cat([tab, tab2])
+        res["wgrad2"] = (timeit(lambda: K.grouped_wgrad2(dY8, act8, gW2, dH8, X8, gW1, merged)), 3 * 8 * flop)
     out = {k: {"ms": round(v[0], 4), "tflops": round(v[1] / v[0] / 1e9, 1)} for k, v in res.items()}
     tot_ms = sum(v[0] for v in res.values())
     if not only:

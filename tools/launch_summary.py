@@ -45,8 +45,14 @@ def main(path, json_out=None):
         print(f"{k:50s} {n:8d} {t / n * 1e6:9.1f} {t / tot:7.1%} {rd / n / 1e6:9.1f} {wr / n / 1e6:9.1f} {gbs:7.0f}")
         rows[k] = {"launches": n, "avg_us": t / n * 1e6, "share": t / tot, "dram_read_per_launch": rd / n,
                    "dram_write_per_launch": wr / n}
+    k4 = {k: r for k, r in rows.items() if k.startswith("K4")}
+    totals = {"k4_dram_bytes": sum((r["dram_read_per_launch"] + r["dram_write_per_launch"]) * r["launches"]
+                                   for r in k4.values()),
+              "k4_launches": sum(r["launches"] for r in k4.values()),
+              "k4_share": sum(r["share"] for r in k4.values()), "kernels": sum(a[0] for a in agg.values())}
+    print(json.dumps(totals))
     if json_out:
-        json.dump(rows, open(json_out, "w"), indent=1)
+        json.dump({"per_kernel": rows, "totals": totals}, open(json_out, "w"), indent=1)
 
 
 if __name__ == "__main__":

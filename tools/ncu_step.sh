@@ -1,6 +1,16 @@
-# launch list of our kernels over the bench step (one GPU) + DRAM bytes per launch
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -k regex:"grouped_gemm|histogram|permute|scatter|combine|zero_pad|chunk_scan|accumulate|peer_barrier" \
-    -c 1500 --csv --log-file gpurun_out/r01_launches_step2.csv \
-    python bench.py --steps 1 --warmup 1 --no-cpu-baseline --policies relibra > gpurun_out/ncu_step.log 2>&1
-echo rc=$?
+# launch list of our kernels over ONE bench step (NVTX range "mb_step", one GPU) + DRAM bytes per
+# launch; then one ncu --set full capture per K4 mode at the step's shape.  Writes gpurun_out/.
+export MB_NVTX_STEP=1
+ncu --nvtx --nvtx-include "mb_step/" --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+    --clock-control none --csv --log-file gpurun_out/r02_launches_step.csv \
+    python bench.py --steps 1 --warmup 3 --repeats 1 --batches 1 --no-cpu-baseline --policies relibra \
+    > gpurun_out/ncu_step.log 2>&1
+echo launches_rc=$?
+python tools/launch_summary.py gpurun_out/r02_launches_step.csv gpurun_out/r02_launches_step_summary.json \
+    > gpurun_out/r02_launches_step_summary.txt 2>&1
+for m in fwd1_swiglu dgrad_gated dgrad_dx wgrad2; do
+  ncu --set full --clock-control none --import-source on -k regex:grouped_gemm -s 3 -c 1 \
+      -o gpurun_out/r02_${m}_zipf -f python tools/bench_gemm.py --zipf-rows --only $m --iters 1 --warmup 3 \
+      > gpurun_out/ncu_${m}.log 2>&1
+  echo full_${m}_rc=$?
+done
