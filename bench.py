@@ -727,6 +727,8 @@ def main():
         print("bench: --warmup < 3 is below the timing rules; using 3", file=sys.stderr)
         args.warmup = 3
     env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1 and args.impl == "reference":
+        env_world = str(args.gpus)    # the CPU arm runs on rank 0 only: nothing to launch
     if env_world is None and args.gpus > 1:
         # `python bench.py --gpus N`: launch N ranks (one process per GPU, NCCL) ourselves
         import socket
