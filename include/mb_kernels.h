@@ -57,7 +57,9 @@ enum {
                                      C2 = gate*act, row_partial[row][N/64] = partial <dout.W2, act>
                                      whose sum is dgate = <dout, Y> (replaces the combine backward) */
 };
-/* mode | 0x100 forces the 1-CTA kernel (default: CTA-pair 256x256 tiles when the shape allows).
+/* mode | 0x100 forces the 1-CTA kernel (default: CTA-pair 256x256 tiles when the shape allows);
+ * mode | 0x200 runs the single-CTA member of the pair family (cta_group::1, 128 x 256 tiles, every
+ * F-mode epilogue incl. the gated dSwiGLU) -- the 128-row tail blocks of odd groups.
  * gemm_sms > 0: SMs this launch's persistent grid covers (each data plane passes its own split;
  * <= 0 = the process default of mb_set_gemm_sms). */
 int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t a_cols, const void* B0, int64_t b0_rows,

@@ -25,15 +25,16 @@ static int launch_gemm(const GemmParams& p, cudaStream_t stream) {
   return MB_OK;
 }
 
-template <bool kW, bool kAmn, bool kBmn, int kEpi>
+template <bool kW, bool kAmn, bool kBmn, int kEpi, bool kPair = true>
 static int launch_pair(const GemmParams& p, cudaStream_t stream, int sms) {
-  auto kern = grouped_gemm_pair_kernel<kW, kAmn, kBmn, kEpi>;
+  auto kern = kPair ? grouped_gemm_pair_kernel<kW, kAmn, kBmn, kEpi> : grouped_gemm_single_kernel<kW, kAmn, kBmn, kEpi>;
+  using Cfg = PairCfg<kEpi, kPair>;
   static bool attr_set = false;
   if (!attr_set) {
-    MB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<kEpi>::kSmemBytes));
+    MB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes));
     attr_set = true;
   }
-  const int grid = gemm_sms(sms) & ~1;
+  const int grid = kPair ? (gemm_sms(sms) & ~1) : gemm_sms(sms);
   static unsigned long long* prof = nullptr;
 #ifdef MB_GEMM_PROFILE
   const bool profile = std::getenv("MB_GEMM_PROF") != nullptr;
@@ -65,7 +66,7 @@ static int launch_pair(const GemmParams& p, cudaStream_t stream, int sms) {
     MB_CUDA_TRY(cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), stream));
     q.prof = prof;
   }
-  kern<<<grid, PairCfg<kEpi>::kThreads, PairCfg<kEpi>::kSmemBytes, stream>>>(q);
+  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, stream>>>(q);
   MB_CUDA_TRY(cudaGetLastError());
   if (profile) {  // profiling only: synchronous readback, per-cluster averages in cycles
     unsigned long long h[8];
@@ -151,7 +152,11 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
                                int64_t ld_aux, const float* row_scale, float* row_partial, int32_t gemm_sms,
                                void* stream) {
   const bool force_single = (mode & 0x100) != 0 || !pair_enabled();
+  // 0x200: the single-CTA member of the pair family (cta_group::1, 128 x 256 tiles) -- the tail
+  // blocks of groups with an odd number of 128-row blocks run at full tensor efficiency there
+  const bool tail = (mode & 0x200) != 0;
   mode &= 0xff;
+  MB_CHECK_ARG(!tail || (mode != MB_GEMM_WGRAD && N % 256 == 0), "single-CTA tail launches are F-mode, N %% 256 == 0");
   MB_CHECK_ARG(num_groups >= 0 && num_groups <= kMaxGroups, "num_groups %d outside [0, %d]", num_groups, kMaxGroups);
   MB_CHECK_ARG(A && B0 && C && groups, "null operand pointer");
   MB_CHECK_ARG(a_cols % 64 == 0 && b_cols % 64 == 0, "operand widths must be multiples of 64");
@@ -169,7 +174,7 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const bool pair = !force_single && N % 256 == 0 && (mode != MB_GEMM_WGRAD || M % 256 == 0);
   int rc;
-  if (pair || mode == MB_GEMM_DGRAD_DSWIGLU_GATED) {
+  if (pair || tail || mode == MB_GEMM_DGRAD_DSWIGLU_GATED) {
     // epilogue TMA store maps: 32-row x 128-byte boxes (64 bf16 / 32 fp32 columns)
     if (mode == MB_GEMM_WGRAD) {
       MB_CHECK_ARG(c_slot_stride == static_cast<int64_t>(M) * ldc, "wgrad output must be [slots][M][ldc]");
@@ -192,7 +197,7 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
     case MB_GEMM_FWD_STORE:
     case MB_GEMM_FWD_SWIGLU: {
       MB_CHECK_ARG(N % 256 == 0 && K % 64 == 0 && a_cols == K && b_cols == K, "fwd GEMM shape N=%d K=%d", N, K);
-      const uint32_t bbox = pair ? 128 : 256;
+      const uint32_t bbox = (pair || tail) ? 128 : 256;
       if ((rc = make_tmap_bf16_2d(&p.tmA, A, a_cols, a_rows, a_cols * 2, 64, 128))) return rc;
       if ((rc = make_tmap_bf16_2d(&p.tmB0, B0, b_cols, b0_rows, b_cols * 2, 64, bbox))) return rc;
       if ((rc = make_tmap_bf16_2d(&p.tmB1, B1, b_cols, b1_rows, b_cols * 2, 64, bbox))) return rc;
@@ -202,21 +207,24 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
         if ((rc = make_tmap_bf16_2d(&p.tmB1h, B1, b_cols, b1_rows, b_cols * 2, 64, 64))) return rc;
       }
       if (mode == MB_GEMM_FWD_STORE)
-        return pair ? launch_pair<false, false, false, EPI_STORE_BF16>(p, s, gemm_sms)
-                    : launch_gemm<false, false, false, 256, EPI_STORE_BF16>(p, s);
+        return tail ? launch_pair<false, false, false, EPI_STORE_BF16, false>(p, s, gemm_sms)
+               : pair ? launch_pair<false, false, false, EPI_STORE_BF16>(p, s, gemm_sms)
+                      : launch_gemm<false, false, false, 256, EPI_STORE_BF16>(p, s);
       MB_CHECK_ARG(C2 != nullptr, "SwiGLU epilogue needs the activation output");
-      return pair ? launch_pair<false, false, false, EPI_SWIGLU>(p, s, gemm_sms)
-                  : launch_gemm<false, false, false, 256, EPI_SWIGLU>(p, s);
+      return tail ? launch_pair<false, false, false, EPI_SWIGLU, false>(p, s, gemm_sms)
+             : pair ? launch_pair<false, false, false, EPI_SWIGLU>(p, s, gemm_sms)
+                    : launch_gemm<false, false, false, 256, EPI_SWIGLU>(p, s);
     }
     case MB_GEMM_DGRAD_DSWIGLU_GATED: {
-      MB_CHECK_ARG(!force_single && N % 256 == 0 && K % 64 == 0 && a_cols == K && b_cols == N,
-                   "gated dSwiGLU GEMM needs the CTA-pair kernel and N %% 256 == 0 (N=%d K=%d)", N, K);
+      MB_CHECK_ARG((!force_single || tail) && N % 256 == 0 && K % 64 == 0 && a_cols == K && b_cols == N,
+                   "gated dSwiGLU GEMM needs the CTA-pair kernel family and N %% 256 == 0 (N=%d K=%d)", N, K);
       MB_CHECK_ARG(aux && C2 && row_scale && row_partial, "gated dSwiGLU needs H, Act out, gate and partials");
       if ((rc = make_tmap_bf16_2d(&p.tmA, A, a_cols, a_rows, a_cols * 2, 64, 128))) return rc;
       if ((rc = make_tmap_bf16_2d(&p.tmAh, A, a_cols, a_rows, a_cols * 2, 64, 64))) return rc;
       if ((rc = make_tmap_bf16_2d(&p.tmB0, B0, b_cols, b0_rows, b_cols * 2, 64, 64))) return rc;
       if ((rc = make_tmap_bf16_2d(&p.tmB1, B1, b_cols, b1_rows, b_cols * 2, 64, 64))) return rc;
-      return launch_pair<false, false, true, EPI_DSWIGLU_GATED>(p, s, gemm_sms);
+      return tail ? launch_pair<false, false, true, EPI_DSWIGLU_GATED, false>(p, s, gemm_sms)
+                  : launch_pair<false, false, true, EPI_DSWIGLU_GATED>(p, s, gemm_sms);
     }
     case MB_GEMM_DGRAD_STORE:
     case MB_GEMM_DGRAD_DSWIGLU: {
@@ -227,12 +235,14 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
       if ((rc = make_tmap_bf16_2d(&p.tmB1, B1, b_cols, b1_rows, b_cols * 2, 64, 64))) return rc;
       if (mode == MB_GEMM_DGRAD_STORE) {
         MB_CHECK_ARG(N % 256 == 0, "dgrad N=%d must be a multiple of 256", N);
-        return pair ? launch_pair<false, false, true, EPI_STORE_BF16>(p, s, gemm_sms)
-                    : launch_gemm<false, false, true, 256, EPI_STORE_BF16>(p, s);
+        return tail ? launch_pair<false, false, true, EPI_STORE_BF16, false>(p, s, gemm_sms)
+               : pair ? launch_pair<false, false, true, EPI_STORE_BF16>(p, s, gemm_sms)
+                      : launch_gemm<false, false, true, 256, EPI_STORE_BF16>(p, s);
       }
       MB_CHECK_ARG(N % 128 == 0 && aux != nullptr, "dSwiGLU epilogue needs N%%128==0 and H");
-      return pair ? launch_pair<false, false, true, EPI_DSWIGLU>(p, s, gemm_sms)
-                  : launch_gemm<false, false, true, 128, EPI_DSWIGLU>(p, s);
+      return tail ? launch_pair<false, false, true, EPI_DSWIGLU, false>(p, s, gemm_sms)
+             : pair ? launch_pair<false, false, true, EPI_DSWIGLU>(p, s, gemm_sms)
+                    : launch_gemm<false, false, true, 128, EPI_DSWIGLU>(p, s);
     }
     case MB_GEMM_WGRAD: {
       MB_CHECK_ARG(M % 128 == 0 && N % 256 == 0 && a_cols == M && b_cols == N, "wgrad GEMM shape M=%d N=%d", M, N);

@@ -38,14 +38,21 @@ struct PairTile {
 // (light epilogues: one 32-row x 128-byte output box; dSwiGLU epilogues: two 32-row x 64-byte
 // boxes -- 32 features of gate and of up -- that carry H in and dH / gate*act out), and a small
 // meta block (barriers + tile starts; the group table is read from global memory).
-template <int kEpi>
+#ifndef MB_SINGLE_STAGES
+#define MB_SINGLE_STAGES 4      // single-CTA variant: 48 KB stages (A 128 rows + all 256 columns of B)
+#endif
+// kPair = false: the single-CTA (cta_group::1) variant for the 128-row tail blocks of odd groups:
+// a 128 x 256 tile per CTA at full tensor-core efficiency (M=128 N=256 MMAs), the same roles,
+// epilogues and tile scheduler, no cluster.
+template <int kEpi, bool kPair = true>
 struct PairCfg : PairTile {
   static constexpr bool kHeavy = kEpi == EPI_DSWIGLU || kEpi == EPI_DSWIGLU_GATED;
   static constexpr int kEpiWarps = MB_PAIR_EPI_WARPS;
   static constexpr int kThreads = 64 + 32 * kEpiWarps;
-  static constexpr int kStages = MB_PAIR_STAGES;
+  static constexpr int TM = kPair ? 256 : 128;  // tile rows (per cluster)
+  static constexpr int kStages = kPair ? MB_PAIR_STAGES : MB_SINGLE_STAGES;
   static constexpr int kABytes = 128 * BK * 2;  // this CTA's 128 rows of A
-  static constexpr int kBBytes = 128 * BK * 2;  // this CTA's 128 columns of B
+  static constexpr int kBBytes = (kPair ? 128 : 256) * BK * 2;  // this CTA's columns of B
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStagingBytes = kEpiWarps * kBoxBytes;
   static constexpr int kMetaBytes = 512 + 4 * (kMaxGroups + 8);
@@ -82,7 +89,7 @@ __device__ __forceinline__ TileCoord decode_tile_pair(int t, const int* tile_sta
   return c;
 }
 
-// F-mode tail tile: the last 128 padded rows of a group whose row count is an odd multiple of 128.
+// F-mode tail tile (pair kernel): the last 128 padded rows of a group whose row count is an odd multiple of 128.
 // It runs as M=128 cta_group::2 MMAs (64 rows per CTA) issued twice with N=128 (the two 128-wide
 // column blocks of the 256-wide tile), so no tensor-core work is spent on a half-empty pair tile.
 // TMEM layout of such an MMA (the "2x2" datapath layout): lanes 0-63 hold columns [0, 64) and
@@ -137,10 +144,9 @@ __device__ __forceinline__ void pack_bf16_words(const uint32_t (&a)[32], const u
   for (int i = 0; i < 16; ++i) w[16 + i] = pack_bf16x2(__uint_as_float(b[2 * i]), __uint_as_float(b[2 * i + 1]));
 }
 
-template <bool kW, bool kAmn, bool kBmn, int kEpi>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThreads, 1)
-    grouped_gemm_pair_kernel(const __grid_constant__ GemmParams p) {
-  using Cfg = PairCfg<kEpi>;
+template <bool kW, bool kAmn, bool kBmn, int kEpi, bool kPair>
+__device__ __forceinline__ void grouped_gemm_body(const GemmParams& p) {
+  using Cfg = PairCfg<kEpi, kPair>;
   constexpr int S = Cfg::kStages;
   constexpr int TM = Cfg::TM, TN = Cfg::TN;
   extern __shared__ uint8_t smem_raw[];
@@ -164,10 +170,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
   const int warp = warp_id();
   const int lane = lane_id();
   const int ng = p.num_groups;
-  const uint32_t rank = cluster_ctarank();
+  const uint32_t rank = kPair ? cluster_ctarank() : 0u;
   const bool leader = rank == 0;
-  const int cluster = blockIdx.x >> 1;
-  const int nclusters = gridDim.x >> 1;
+  const int cluster = kPair ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int nclusters = kPair ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&p.tmA);
@@ -180,17 +186,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
-      mbar_init(&tempty_bar[i], 2 * Cfg::kEpiWarps);  // every epilogue warp of both CTAs
+      mbar_init(&tempty_bar[i], (kPair ? 2 : 1) * Cfg::kEpiWarps);  // every epilogue warp of the cluster
     }
     for (int i = 0; i < Cfg::kEpiWarps; ++i) mbar_init(&hbar_base[i], 1);
     for (int i = 0; i < kTileRing; ++i) {
       mbar_init(&tr_full[i], 1);
-      mbar_init(&tr_empty[i], kTileConsumers);
+      mbar_init(&tr_empty[i], kPair ? kTileConsumers : 1 + Cfg::kEpiWarps);
     }
     fence_barrier_init();
     fence_proxy_async_smem();
   }
-  if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (kPair) tmem_alloc_pair<512>(tmem_slot);
+    else tmem_alloc<512>(tmem_slot);
+  }
   __syncthreads();
   if (warp == 0) {
     const int n_tiles = p.N / TN;
@@ -216,14 +225,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
   }
   tc_fence_before();
   __syncthreads();
-  cluster_sync_all();
+  if constexpr (kPair) cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total_tiles = tile_start[ng];
   // i-th tile id of this cluster (consumer side); the caller's lane 0 frees the slot
   auto take_tile = [&](int i) -> int {
     const int slot = i % kTileRing;
-    mbar_wait_cluster(&tr_full[slot], (i / kTileRing) & 1);
+    if constexpr (kPair) mbar_wait_cluster(&tr_full[slot], (i / kTileRing) & 1);
+    else mbar_wait(&tr_full[slot], (i / kTileRing) & 1);
     const int t = *reinterpret_cast<volatile int*>(&ring[slot]);
     __syncwarp();
     if (lane == 0) {
@@ -252,10 +262,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
           t = t_next;
           const int slot = i % kTileRing;
           mbar_wait(&tr_empty[slot], ((i / kTileRing) & 1) ^ 1);
-          st_shared_cluster_u32(mapa_shared(smem_u32(&ring[slot]), 0), static_cast<uint32_t>(t));
-          st_shared_cluster_u32(mapa_shared(smem_u32(&ring[slot]), 1), static_cast<uint32_t>(t));
-          mbar_arrive_cluster(mapa_shared(smem_u32(&tr_full[slot]), 0));
-          mbar_arrive_cluster(mapa_shared(smem_u32(&tr_full[slot]), 1));
+          if constexpr (kPair) {
+            st_shared_cluster_u32(mapa_shared(smem_u32(&ring[slot]), 0), static_cast<uint32_t>(t));
+            st_shared_cluster_u32(mapa_shared(smem_u32(&ring[slot]), 1), static_cast<uint32_t>(t));
+            mbar_arrive_cluster(mapa_shared(smem_u32(&tr_full[slot]), 0));
+            mbar_arrive_cluster(mapa_shared(smem_u32(&tr_full[slot]), 1));
+          } else {
+            *reinterpret_cast<volatile int*>(&ring[slot]) = t;
+            mbar_arrive(&tr_full[slot]);   // release.cta: orders the id store for this CTA's roles
+          }
           if (t >= total_tiles) break;
           t_next = p.tile_counter ? nclusters + atomicAdd(p.tile_counter, 1) : t + nclusters;  // fetched early
         } else {
@@ -269,8 +284,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
         const GemmGroup gg = sg[tc.g];
         const CUtensorMap* tmB = (gg.flags & 2) ? &p.tmB1 : ((kW && (gg.flags & 4)) ? &p.tmB0h : &p.tmB0);
         const CUtensorMap* tmBh = (gg.flags & 2) ? &p.tmB1h : &p.tmB0h;
-        const bool half = !kW && half_tile(gg, tc, p.debug);
-        const int bytes = half ? 2 * (Cfg::kABytes / 2 + Cfg::kBBytes) : 2 * Cfg::kStageBytes;
+        const bool half = kPair && !kW && half_tile(gg, tc, p.debug);
+        const int bytes = !kPair ? Cfg::kStageBytes : half ? 2 * (Cfg::kABytes / 2 + Cfg::kBBytes) : 2 * Cfg::kStageBytes;
         KWalker kw(gg, p.segs);
         for (int kb = 0; kb < tc.kblocks; ++kb) {
           int nk16 = BK / 16;
@@ -280,7 +295,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
             mbar_wait(&empty_bar[stage], phase ^ 1);
             if (kProf) w_empty += clock64() - t0;
           }
-          const uint32_t lbar = mapa_shared(smem_u32(&full_bar[stage]), 0);
+          const uint32_t lbar = kPair ? mapa_shared(smem_u32(&full_bar[stage]), 0) : smem_u32(&full_bar[stage]);
           if (p.debug & 32) {  // profiling only: no operand loads (MMAs read stale smem)
             if (leader) mbar_arrive(&full_bar[stage]);
             if (++stage == S) { stage = 0; phase ^= 1; }
@@ -289,32 +304,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
           if (leader) mbar_arrive_expect_tx(&full_bar[stage], bytes);
           uint8_t* a_dst = sA + stage * Cfg::kABytes;
           uint8_t* b_dst = sB + stage * Cfg::kBBytes;
+          // pair: bytes complete on the leader's barrier (cta_group::2 form); single: own barrier
+          auto load2d = [&](void* dst, const CUtensorMap* map, int32_t c0, int32_t c1) {
+            if constexpr (kPair) tma_load_2d_pair(dst, map, lbar, c0, c1);
+            else tma_load_2d(dst, map, &full_bar[stage], c0, c1);
+          };
           if (!kAmn) {
-            if (half) tma_load_2d_pair(a_dst, &p.tmAh, lbar, kb * BK, gg.a0 + tc.mb * TM + rank * 64);
-            else tma_load_2d_pair(a_dst, &p.tmA, lbar, (p.debug & 64) ? 0 : kb * BK,
-                                  (p.debug & 64) ? rank * 128 : gg.a0 + tc.mb * TM + rank * 128);
+            if (half) load2d(a_dst, &p.tmAh, kb * BK, gg.a0 + tc.mb * TM + rank * 64);
+            else load2d(a_dst, &p.tmA, (p.debug & 64) ? 0 : kb * BK,
+                        (p.debug & 64) ? rank * 128 : gg.a0 + tc.mb * TM + rank * 128);
           } else {
             const CUtensorMap* tmA_w = (kW && (gg.flags & 4)) ? &p.tmAh : &p.tmA;   // W: second problem
 #pragma unroll
-            for (int j = 0; j < 2; ++j)
-              tma_load_2d_pair(a_dst + j * 8192, tmA_w, lbar, tc.mb * TM + rank * 128 + j * 64, krow);
+            for (int j = 0; j < 2; ++j) load2d(a_dst + j * 8192, tmA_w, tc.mb * TM + rank * 128 + j * 64, krow);
           }
           if (!kBmn) {
             if (half) {
               // this CTA's 64-column halves of both 128-column blocks
 #pragma unroll
               for (int j = 0; j < 2; ++j)
-                tma_load_2d_pair(b_dst + j * 8192, tmBh, lbar, kb * BK, gg.slot * p.N + tc.nb * TN + j * 128 + rank * 64);
+                load2d(b_dst + j * 8192, tmBh, kb * BK, gg.slot * p.N + tc.nb * TN + j * 128 + rank * 64);
             } else {
-              tma_load_2d_pair(b_dst, tmB, lbar, kb * BK, gg.slot * p.N + tc.nb * TN + rank * 128);
+              // pair: this CTA's 128 columns; single: all 256 (two 128-row boxes)
+#pragma unroll
+              for (int j = 0; j < (kPair ? 1 : 2); ++j)
+                load2d(b_dst + j * 16384, tmB, kb * BK, gg.slot * p.N + tc.nb * TN + rank * 128 + j * 128);
             }
           } else {
             const int row0 = (p.debug & 64) ? 0 : (kW ? krow : (gg.slot * p.K + kb * BK));
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
+            for (int j = 0; j < (kPair ? 2 : 4); ++j) {
               const int col = (p.debug & 64) ? rank * 128 + j * 64
                               : half ? tc.nb * TN + j * 128 + rank * 64 : tc.nb * TN + rank * 128 + j * 64;
-              tma_load_2d_pair(b_dst + j * 8192, tmB, lbar, col, row0);
+              load2d(b_dst + j * 8192, tmB, col, row0);
             }
           }
           if (++stage == S) { stage = 0; phase ^= 1; }
@@ -331,7 +353,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
       uint32_t phase = 0;
       for (int it = 0;; ++it) {
         const int slot = it % kTileRing;
-        mbar_wait_cluster(&tr_full[slot], (it / kTileRing) & 1);
+        if constexpr (kPair) mbar_wait_cluster(&tr_full[slot], (it / kTileRing) & 1);
+        else mbar_wait(&tr_full[slot], (it / kTileRing) & 1);
         const int t = *reinterpret_cast<volatile int*>(&ring[slot]);
         mbar_arrive(&tr_empty[slot]);
         if (t >= total_tiles) break;
@@ -345,7 +368,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * 256;
         const GemmGroup gg = sg[tc.g];
-        const bool half = !kW && half_tile(gg, tc, p.debug);
+        const bool half = kPair && !kW && half_tile(gg, tc, p.debug);
         KWalker kw(gg, p.segs);
         for (int kb = 0; kb < tc.kblocks; ++kb) {
           int nk16 = BK / 16;
@@ -367,7 +390,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
             if (!half) {
               const uint64_t bdesc = kBmn ? make_sw128_desc(b_addr + k * 2048, 8192, 1024)
                                           : make_sw128_desc(b_addr + k * 32, 16, 1024);
-              umma_bf16_pair(d_tmem, adesc, bdesc, idesc, accum);
+              if constexpr (kPair) umma_bf16_pair(d_tmem, adesc, bdesc, idesc, accum);
+              else umma_bf16(d_tmem, adesc, bdesc, idesc, accum);
             } else {
 #pragma unroll
               for (int j = 0; j < 2; ++j) {
@@ -377,10 +401,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
               }
             }
           }
-          umma_commit_pair(&empty_bar[stage], 0x3);
+          if constexpr (kPair) umma_commit_pair(&empty_bar[stage], 0x3);
+          else umma_commit(&empty_bar[stage]);
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
-        umma_commit_pair(&tfull_bar[acc], 0x3);
+        if constexpr (kPair) umma_commit_pair(&tfull_bar[acc], 0x3);
+        else umma_commit(&tfull_bar[acc]);
       }
     }
     __syncwarp();
@@ -391,8 +417,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
     constexpr int kPasses = 8 / Cfg::kEpiWarps;
     const int q = warp & 3;
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
-    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
-    const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty_bar[1]), 0);
+    const uint32_t tempty_leader0 = kPair ? mapa_shared(smem_u32(&tempty_bar[0]), 0) : 0u;
+    const uint32_t tempty_leader1 = kPair ? mapa_shared(smem_u32(&tempty_bar[1]), 0) : 0u;
     BoxStager<1> st{sStage + (warp - 2) * Cfg::kBoxBytes, 0, lane, p.debug};
     uint64_t* hbar = hbar_base + (warp - 2);
     uint32_t hphase = 0;
@@ -429,7 +455,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
       // full tile: this warp owns rows q*32.. of the CTA's 128 and columns [ch2*128, +128);
       // tail tile (half_tile): rows (q&1)*32.. of the CTA's 64; lane group q>>1 holds columns
       // [(q>>1)*64, +64) of both 128-column blocks; the ch2 = 1 warps have nothing to do
-      const bool half = !kW && half_tile(gg, tc, p.debug);
+      const bool half = kPair && !kW && half_tile(gg, tc, p.debug);
       const int warp_row0 = half ? tc.mb * TM + static_cast<int>(rank) * 64 + (q & 1) * 32
                                  : tc.mb * TM + static_cast<int>(rank) * 128 + q * 32;
       const int tile_row = warp_row0 + lane;
@@ -635,11 +661,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThre
   }
   tc_fence_before();
   __syncthreads();
-  cluster_sync_all();
+  if constexpr (kPair) cluster_sync_all();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc_pair<512>(tmem_base);
+    if constexpr (kPair) tmem_dealloc_pair<512>(tmem_base);
+    else tmem_dealloc<512>(tmem_base);
   }
+}
+
+template <bool kW, bool kAmn, bool kBmn, int kEpi>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<kEpi>::kThreads, 1)
+    grouped_gemm_pair_kernel(const __grid_constant__ GemmParams p) {
+  grouped_gemm_body<kW, kAmn, kBmn, kEpi, true>(p);
+}
+
+template <bool kW, bool kAmn, bool kBmn, int kEpi>
+__global__ void __launch_bounds__(PairCfg<kEpi, false>::kThreads, 1)
+    grouped_gemm_single_kernel(const __grid_constant__ GemmParams p) {
+  grouped_gemm_body<kW, kAmn, kBmn, kEpi, false>(p);
 }
 
 }  // namespace mb

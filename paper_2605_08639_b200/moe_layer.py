@@ -72,6 +72,10 @@ ROW_MOVERS_MULTI = "tma"
 # is idle (N=4: 18.9-19.0 -> 18.7-18.9 ms; at N=1 widening the single launch measured 3% slower).
 # MB_WGRAD_ALL_SMS=0: A/B.
 WGRAD_ALL_SMS = os.environ.get("MB_WGRAD_ALL_SMS", "1") == "1"
+# 128-row tail blocks of odd groups in the single-CTA kernel beside the pair kernel (opt-in,
+# MB_TAIL_TILES=1): measured no faster at N=1 (18.55-18.88 vs 18.57-18.78 ms/step; the tail kernel's
+# 48 KB stages carry twice the B bytes per SM), so the pair kernel's half tiles stay the default
+TAIL_TILES = os.environ.get("MB_TAIL_TILES", "0") == "1"
 # both weight gradients in one two-problem launch (mb_grouped_wgrad2); MB_WGRAD_MERGED=0: A/B
 WGRAD_MERGED = os.environ.get("MB_WGRAD_MERGED", "1") == "1"
 # overlap=False runs every phase in issue order on one stream with all SMs in the GEMM: at world 1
@@ -663,7 +667,7 @@ class MoEDataPlane:
             mine = np.flatnonzero(home == g)
             local_of[mine] = np.arange(len(mine))
         loc_of_home = {int(ex): i for i, ex in enumerate(home_experts)}
-        route, ncop, groups, slots, nsl = [], [], [], [], []
+        route, ncop, groups, slots, nsl, tails = [], [], [], [], [], []
         max_slots = plan.max_slots
         mb_rep = []               # per micro-batch: [(slot q, expert, owner rank, owner local index)]
         rep_rows = []             # per micro-batch: {(holder rank, expert): (slot q, real rows)}
@@ -685,6 +689,19 @@ class MoEDataPlane:
             g[:n, 3] = np.where(sw[:n, 1] > 0, K.FLAG_REPLICA, 0)
             g[:n, 6] = st[:n, 1]
             groups.append(g)
+            # tail blocks: the last 128 rows of a slot with an odd number of 128-row blocks run in
+            # the single-CTA kernel beside the pair kernel (which then sees whole 256-row tiles)
+            pair_rows = (g[:n, 0] // 256) * 256
+            has_tail = (g[:n, 0] - pair_rows) > 0
+            gp = g.copy()
+            gp[:n, 0] = pair_rows
+            gt = g[:n][has_tail].copy()
+            gt[:, 1] += pair_rows[has_tail]
+            gt[:, 0] = 128
+            gt[:, 6] = np.maximum(0, g[:n, 6][has_tail] - pair_rows[has_tail])
+            n_pair_blocks, n_tail = int(pair_rows.sum()) // 256, int(has_tail.sum())
+            tail_share = n_tail / max(1, n_tail + 2 * n_pair_blocks)   # SM-time share of the tails
+            tails.append((gp, gt, tail_share))
             slots.append(st)
             nsl.append(n)
             mb_rep.append([(int(sw[s, 0]), int(st[s, 3]), int(home[st[s, 3]]), int(local_of[st[s, 3]]))
@@ -712,6 +729,9 @@ class MoEDataPlane:
         at = {"home_experts": home_experts, "mb_rep": mb_rep, "nslots": nsl,
               "route_tab": route_dev, "ncopies": ncop_dev,
               "groups": torch.from_numpy(np.stack(groups)).to(dev),
+              # per micro-batch (pair-kernel groups, tail groups or None, tail SM share)
+              "tail_groups": [(torch.from_numpy(gp).to(dev), torch.from_numpy(gt).to(dev) if len(gt) else None, sh)
+                              for gp, gt, sh in tails],
               "slot_tab": slot_dev,
               "expected": (torch.from_numpy(np.ascontiguousarray(plan.mats[:, d], dtype=np.int32)).to(dev)
                            if plan.mats is not None else None)}
@@ -1166,6 +1186,9 @@ class _StepOps:
         self.rep_done = set()
         self.seq = 0
         self.x_ev = {}
+        if not hasattr(dp, "_tail_stream"):
+            dp._tail_stream = torch.cuda.Stream(device=dp.device)
+        self.tail_stream = dp._tail_stream
 
     # -------------------------------------------------------------- replica weights (K5)
     def _replica_set(self, kind: str, m: int) -> int:
@@ -1345,23 +1368,40 @@ class _StepOps:
                       self.st_x)
 
     # -------------------------------------------------------------- compute stream
+    def _fgemm(self, m, mode, A, B0, **kw):
+        """One F-mode GEMM of micro-batch m: with TAIL_TILES, the 128-row tail blocks run in the
+        single-CTA kernel on a side stream (launched first, on a share of the SMs proportional to
+        their work) while the pair kernel -- dynamically scheduled, so it adapts -- takes the rest."""
+        dp = self.dp
+        ng = dp.nslots[m]
+        gp, gt, share = dp.tail_groups[m]
+        if not TAIL_TILES or gt is None:
+            dp._gemm(mode, A, B0, dp.groups[m][:ng], **kw)
+            return
+        ts = self.tail_stream
+        ts.wait_stream(self.cs)
+        tail_sms = int(min(64, max(2, round(dp.gemm_sms * share))))
+        K.grouped_gemm(mode, A, B0, gt, tail=True, sms=tail_sms, stream=ts, **kw)
+        dp.launches += 1
+        dp._gemm(mode, A, B0, gp[:ng], **kw)
+        self.cs.wait_stream(ts)
+
     def fwd_gemms(self, m):
         """F(m): gate/up GEMM + SwiGLU, down GEMM."""
         dp = self.dp
         h, hp = dp.shape.hidden, dp.shape.ffn
         ng = dp.nslots[m]
         if ng:
-            g = dp.groups[m][:ng]
             a = dp.set_index(m)
             rows = dp.real_rows(m)
             i1 = self._replica_set("w1", m)
             with dp._timed(4.0 * rows * h * hp, "fwd_swiglu"):
-                dp._gemm(K.GEMM_FWD_SWIGLU, dp.Xr[a], dp.W1, g, N=2 * hp, K=h, C=dp.H[a], C2=dp.Act[a],
-                         B1=dp.W1r[i1])
+                self._fgemm(m, K.GEMM_FWD_SWIGLU, dp.Xr[a], dp.W1, N=2 * hp, K=h, C=dp.H[a], C2=dp.Act[a],
+                            B1=dp.W1r[i1])
             self._replica_used("w1", i1, m)
             i2 = self._replica_set("w2", m)
             with dp._timed(2.0 * rows * h * hp, "fwd_down"):
-                dp._gemm(K.GEMM_FWD_STORE, dp.Act[a], dp.W2, g, N=h, K=hp, C=dp.Y[a], B1=dp.W2r[i2])
+                self._fgemm(m, K.GEMM_FWD_STORE, dp.Act[a], dp.W2, N=h, K=hp, C=dp.Y[a], B1=dp.W2r[i2])
             self._replica_used("w2", i2, m)
 
     def bwd_gemms(self, m):
@@ -1371,20 +1411,19 @@ class _StepOps:
         h, hp = dp.shape.hidden, dp.shape.ffn
         ng = dp.nslots[m]
         if ng:
-            g = dp.groups[m][:ng]
             a = dp.set_index(m)
             rows = dp.real_rows(m)
             i2 = self._replica_set("w2", m)
             # dAct = dout.W2 with the combine backward fused in the epilogue: gate applied per row,
             # dgate partials <dout.W2, act> = <dout, Y>, gate*act written over Act for dW2
             with dp._timed(2.0 * rows * h * hp, "dgrad_act_gated"):
-                dp._gemm(K.GEMM_DGRAD_DSWIGLU_GATED, dp.dYr[a], dp.W2, g, N=hp, K=h, C=dp.dH[a],
-                         C2=dp.Act[a], aux=dp.H[a], B1=dp.W2r[i2], row_scale=dp.gate_r[a],
-                         row_partial=dp.dgate_r[a])
+                self._fgemm(m, K.GEMM_DGRAD_DSWIGLU_GATED, dp.dYr[a], dp.W2, N=hp, K=h, C=dp.dH[a],
+                            C2=dp.Act[a], aux=dp.H[a], B1=dp.W2r[i2], row_scale=dp.gate_r[a],
+                            row_partial=dp.dgate_r[a])
             self._replica_used("w2", i2, m)
             i1 = self._replica_set("w1", m)
             with dp._timed(4.0 * rows * h * hp, "dgrad_x"):
-                dp._gemm(K.GEMM_DGRAD_STORE, dp.dH[a], dp.W1, g, N=h, K=2 * hp, C=dp.dXp[a], B1=dp.W1r[i1])
+                self._fgemm(m, K.GEMM_DGRAD_STORE, dp.dH[a], dp.W1, N=h, K=2 * hp, C=dp.dXp[a], B1=dp.W1r[i1])
             self._replica_used("w1", i1, m)
         self.rep_done.add(m)
         rw = dp.rw_mb[m]
