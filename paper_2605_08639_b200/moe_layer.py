@@ -413,6 +413,58 @@ def _wgrad_table(rows: list) -> np.ndarray:
     return tab[:len(rows)] if rows else tab[:0]
 
 
+class ReplicaBuffer:
+    """The paper's layer-shared replica buffer (replica_memory "layer-shared",
+    replicate.py:528-534): `sets` x r replica weight slots of one expert shape per GPU plus the fp32
+    replica-gradient ring, in their own symmetric arena, shared by every MoE layer
+    (MoEDataPlane(..., replica_buffer=buf)) of a model.  Layers take turns: each (layer,
+    micro-batch) phase pulls the replicas it needs into the slots right before its GEMM (after the
+    slot's last use by any layer) and pushes the replica gradients back within the same
+    micro-batch's backward, so the buffer never grows with the number of layers."""
+
+    def __init__(self, comm: Comm, shape: LayerShape, slots: int, sets: int = 1,
+                 device: torch.device | None = None):
+        if slots < 1 or sets < 1:
+            raise ValueError("a replica buffer needs >= 1 slot and >= 1 set")
+        self.shape, self.slots, self.sets = shape, slots, sets
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        h, hp = shape.hidden, shape.ffn
+        self.w1_bytes, self.w2_bytes = 2 * hp * h * 2, h * hp * 2
+        self.g1_bytes, self.g2_bytes = 2 * hp * h * 4, h * hp * 4
+        self.sizes = {"w1r": sets * slots * self.w1_bytes, "w2r": sets * slots * self.w2_bytes,
+                      "rg1": GRAD_RING * slots * self.g1_bytes, "rg2": GRAD_RING * slots * self.g2_bytes}
+        total = sum((v + 1023) // 1024 * 1024 for v in self.sizes.values()) + 4096
+        self.arena = SymmetricArena(comm, total, self.device)
+        self.off = {k: self.arena.alloc(v) for k, v in self.sizes.items()}
+        A = self.arena
+        self.W1r = A.local(self.off["w1r"], (sets, slots, 2 * hp, h), torch.bfloat16)
+        self.W2r = A.local(self.off["w2r"], (sets, slots, h, hp), torch.bfloat16)
+        self.rgW1 = A.local(self.off["rg1"], (GRAD_RING, slots, 2 * hp, h), torch.float32)
+        self.rgW2 = A.local(self.off["rg2"], (GRAD_RING, slots, h, hp), torch.float32)
+        # slot bookkeeping shared by the layers: per kind and set, the (layer, micro-batch) held,
+        # the event after its last use, the event after its pull, an LRU stamp
+        self.state = {kd: {"held": [None] * sets, "used": [None] * sets, "pulled": [None] * sets,
+                           "seq": [0] * sets} for kd in ("w1", "w2")}
+        self.done = set()      # (layer, micro-batch) whose backward is issued (no further use)
+        self.seq = 0
+        self.users = 0
+
+    def invalidate(self, layer_token) -> None:
+        """A new step of `layer_token`: its weights may have changed since the last pull."""
+        for st in self.state.values():
+            for i, tag in enumerate(st["held"]):
+                if tag is not None and tag[0] == layer_token:
+                    st["held"][i] = None
+        self.done = {t for t in self.done if t[0] != layer_token}
+
+    def nbytes(self) -> dict:
+        return {"replica_weight_slots": self.sizes["w1r"] + self.sizes["w2r"],
+                "replica_grad_ring": self.sizes["rg1"] + self.sizes["rg2"]}
+
+    def close(self) -> None:
+        self.arena.close()
+
+
 class PlanTables:
     """A step plan's device tables for one data plane (MoEDataPlane.build_tables): built ahead,
     installed by load_plan / migrate without host work on the step's critical path."""
@@ -437,12 +489,15 @@ class MoEDataPlane:
     def __init__(self, comm: Comm, shape: LayerShape, tokens: int, micro_batches: int, plan: StepPlan,
                  device: torch.device | None = None, comm_sms: int | None = None,
                  expert_state: dict | None = None, rows_cap: int = 0, overlap: bool | None = None,
-                 row_movers: str | None = None, wgrad_mode: str | None = None, replica_sets: int | None = None):
+                 row_movers: str | None = None, wgrad_mode: str | None = None, replica_sets: int | None = None,
+                 replica_buffer: "ReplicaBuffer | None" = None):
         """expert_state: optional per-expert tensors that follow their expert when the reorder
         plan migrates it (e.g. optimizer moments): {name: (per-expert shape, torch dtype)}.
         rows_cap: receive rows per micro-batch to allocate (>= every plan this layer will load).
         overlap: run dispatch / combine on their own stream beside the GEMMs (default).
-        row_movers: "regs" | "tma" scatter / combine engine (default per world size, ROW_MOVERS)."""
+        row_movers: "regs" | "tma" scatter / combine engine (default per world size, ROW_MOVERS).
+        replica_buffer: a ReplicaBuffer shared with the model's other MoE layers (default: this
+        layer allocates its own)."""
         shape.check()
         self.comm, self.shape, self.T, self.MB = comm, shape, tokens, micro_batches
         self.rank, self.world = comm.rank, comm.world
@@ -477,6 +532,17 @@ class MoEDataPlane:
         self.M = E // self.world
         self.R = max(plan.rows_cap, (rows_cap + PAD - 1) // PAD * PAD)
         self.slots = max(plan.slots, 1)
+        if replica_buffer is None:
+            replica_buffer = ReplicaBuffer(comm, shape, self.slots, replica_sets, self.device)
+            self._owns_rb = True
+        else:
+            if replica_buffer.shape != shape or replica_buffer.slots < self.slots:
+                raise ValueError("the shared replica buffer holds a different expert shape or fewer slots")
+            self.slots, self.replica_sets = replica_buffer.slots, replica_buffer.sets
+            self._owns_rb = False
+        self.rb = replica_buffer
+        self.rb.users += 1
+        self.token = object()   # identity of this layer in the shared buffer's slot tags
         self.NA = micro_batches if wgrad_mode == "step" else min(micro_batches, RING_SETS)
         bf, f4 = 2, 4
         self.npart = hp // 64    # dgate partials per row (one per 64 features of h')
@@ -487,10 +553,6 @@ class MoEDataPlane:
         sizes = {
             "xr": NA * R * h * bf, "y": NA * R * h * bf, "dyr": NA * R * h * bf, "dxp": NA * R * h * bf,
             "gate_r": NA * R * f4, "dgate_r": NA * R * self.npart * f4,
-            # layer-shared replica weight slots (pulled by this rank from the owners) and the
-            # replica-gradient ring the owners read back
-            "w1r": replica_sets * self.slots * self.w1_bytes, "w2r": replica_sets * self.slots * self.w2_bytes,
-            "rg1": GRAD_RING * self.slots * self.g1_bytes, "rg2": GRAD_RING * self.slots * self.g2_bytes,
             # home-expert weights, fp32 gradients and expert state live in two banks: a migration
             # (new reorder plan) pulls every new home expert into the idle bank, then swaps
             "w1": self.M * self.w1_bytes, "w2": self.M * self.w2_bytes,
@@ -514,10 +576,8 @@ class MoEDataPlane:
         self.dXp = A.local(self.off["dxp"], (NA, R, h), torch.bfloat16)
         self.gate_r = A.local(self.off["gate_r"], (NA, R), torch.float32)
         self.dgate_r = A.local(self.off["dgate_r"], (NA, R, self.npart), torch.float32)
-        self.W1r = A.local(self.off["w1r"], (replica_sets, self.slots, 2 * hp, h), torch.bfloat16)
-        self.W2r = A.local(self.off["w2r"], (replica_sets, self.slots, h, hp), torch.bfloat16)
-        self.rgW1 = A.local(self.off["rg1"], (GRAD_RING, self.slots, 2 * hp, h), torch.float32)
-        self.rgW2 = A.local(self.off["rg2"], (GRAD_RING, self.slots, h, hp), torch.float32)
+        # the layer-shared replica slots and replica-gradient ring (own, or shared by the layers)
+        self.W1r, self.W2r, self.rgW1, self.rgW2 = self.rb.W1r, self.rb.W2r, self.rb.rgW1, self.rb.rgW2
         self.bank = 0
         self._bind_bank()
         # ---- local activations
@@ -565,8 +625,8 @@ class MoEDataPlane:
         s = self.sizes
         act = sum(s[k] for k in ("xr", "y", "dyr", "dxp", "gate_r", "dgate_r"))
         act += sum(t.numel() * t.element_size() for t in (self.H, self.Act, self.dH))
-        return {"replica_weight_slots": s["w1r"] + s["w2r"], "replica_sets": self.replica_sets,
-                "replica_slots": self.slots, "replica_grad_ring": s["rg1"] + s["rg2"],
+        return {**self.rb.nbytes(), "replica_sets": self.replica_sets, "replica_slots": self.slots,
+                "replica_buffer_shared_by_layers": self.rb.users,
                 "activations": act, "activation_sets": self.NA, "wgrad_mode": self.wgrad_mode,
                 "home_weights_and_grads": sum(s[k] for k in ("w1", "w2", "gw1", "gw2", "w1b", "w2b", "gw1b", "gw2b")),
                 "arena_total": self.arena.nbytes}
@@ -798,7 +858,7 @@ class MoEDataPlane:
                         tasks[i]["dst"] = self.arena.peer_ptr(d, self.off[gkey]) + loc * size
                         dst_other[i] = self.arena.peer_ptr(d, self.off[gkey + "b"]) + loc * size
                         for j, (p, q) in enumerate(srcs_of[m][loc]):
-                            tasks[i]["src"][j] = (self.arena.peer_ptr(p, self.off[key])
+                            tasks[i]["src"][j] = (self.rb.arena.peer_ptr(p, self.rb.off[key])
                                                   + ((m % GRAD_RING) * self.slots + q) * size)
                         tasks[i]["n"], tasks[i]["nsrc"] = nfl[key], len(srcs_of[m][loc])
                         tasks[i]["store"] = 0 if written[loc] else 1
@@ -1150,6 +1210,9 @@ class MoEDataPlane:
     def close(self) -> None:
         torch.cuda.synchronize(self.device)
         self.arena.close()
+        self.rb.users -= 1
+        if self._owns_rb and self.rb.users == 0:
+            self.rb.close()
         if self._err_host:
             nat.kernels().mb_host_free(self._err_host)
             self._err_host = 0
@@ -1178,13 +1241,9 @@ class _StepOps:
         self.start_ev = None
         self.prepared = set()
         self.fresh = dp._wgrad_prepare()
-        # layer-shared replica weight slots: per kind ("w1" / "w2") and set, the micro-batch held,
-        # the event after its last use and after its pull; micro-batches whose backward is issued
-        n = dp.replica_sets
-        self.rep = {kd: {"held": [None] * n, "used": [None] * n, "pulled": [None] * n, "seq": [0] * n}
-                    for kd in ("w1", "w2")}
-        self.rep_done = set()
-        self.seq = 0
+        # layer-shared replica weight slots: the buffer's bookkeeping (shared by the layers), this
+        # layer's earlier pulls invalidated (its weights may have changed since)
+        dp.rb.invalidate(dp.token)
         self.x_ev = {}
         if not hasattr(dp, "_tail_stream"):
             dp._tail_stream = torch.cuda.Stream(device=dp.device)
@@ -1195,45 +1254,49 @@ class _StepOps:
         """Set of `kind` replica slots holding micro-batch m's replica weights: pulled by this rank
         from the owners over NVLink (copy engine) into the least useful set, after that set's last
         use; the compute stream waits for the pull."""
-        dp, st = self.dp, self.rep[kind]
+        dp = self.dp
+        rb = dp.rb
+        st = rb.state[kind]
         need = dp.mb_rep[m]
         if not need:
             return 0
-        if m in st["held"]:
-            i = st["held"].index(m)
+        tag = (dp.token, m)
+        if tag in st["held"]:
+            i = st["held"].index(tag)
         else:
-            cand = list(range(dp.replica_sets))
-            free = [i for i in cand if st["held"][i] is None or st["held"][i] in self.rep_done]
+            cand = list(range(rb.sets))
+            free = [i for i in cand if st["held"][i] is None or st["held"][i] in rb.done]
             pool = free if free else cand
             i = min(pool, key=lambda j: st["seq"][j])
             cps, A, lib = dp.cps, dp.arena, nat.kernels()
             if st["used"][i] is not None:
-                cps.wait_event(st["used"][i])
+                cps.wait_event(st["used"][i])    # the slot's last reader (any layer)
             if self.start_ev is not None:
                 cps.wait_event(self.start_ev)
             size = dp.w1_bytes if kind == "w1" else dp.w2_bytes
-            base = dp.off["w1r" if kind == "w1" else "w2r"] + i * dp.slots * size
+            base = rb.off["w1r" if kind == "w1" else "w2r"] + i * rb.slots * size
             with dp._timed(len(need) * size, "comm_replica_pull", cps):
                 for q, _, owner, loc in need:
                     src = A.peer_ptr(owner, dp.off_w[kind]) + loc * size
-                    nat.check(lib.mb_memcpy_async(A.peer_ptr(dp.rank, base) + q * size, src, size, cps.cuda_stream),
-                              lib, "replica pull")
+                    nat.check(lib.mb_memcpy_async(rb.arena.peer_ptr(dp.rank, base) + q * size, src, size,
+                                                  cps.cuda_stream), lib, "replica pull")
             ev = torch.cuda.Event()
             ev.record(cps)
             st["pulled"][i] = ev
-            st["held"][i] = m
+            st["held"][i] = tag
         self.cs.wait_event(st["pulled"][i])
         return i
 
     def _replica_used(self, kind: str, i: int, m: int) -> None:
         if not self.dp.mb_rep[m]:
             return
-        st = self.rep[kind]
+        rb = self.dp.rb
+        st = rb.state[kind]
         ev = torch.cuda.Event()
         ev.record(self.cs)
         st["used"][i] = ev
-        self.seq += 1
-        st["seq"][i] = self.seq
+        rb.seq += 1
+        st["seq"][i] = rb.seq
 
     # -------------------------------------------------------------- comm stream
     def _first_barrier(self):
@@ -1425,7 +1488,7 @@ class _StepOps:
             with dp._timed(4.0 * rows * h * hp, "dgrad_x"):
                 self._fgemm(m, K.GEMM_DGRAD_STORE, dp.dH[a], dp.W1, N=h, K=2 * hp, C=dp.dXp[a], B1=dp.W1r[i1])
             self._replica_used("w1", i1, m)
-        self.rep_done.add(m)
+        dp.rb.done.add((dp.token, m))
         rw = dp.rw_mb[m]
         if rw is not None:
             tabs, segs, rrows = rw

@@ -105,6 +105,8 @@ def main():
     ap.add_argument("--replica-sets", type=int, default=2)
     ap.add_argument("--migrate", action="store_true")
     ap.add_argument("--min-copies", type=int, default=0, help="fail unless some expert has this many copies")
+    ap.add_argument("--shared-layers", action="store_true",
+                    help="a second MoE layer (own routing and weights) shares the first one's replica buffer")
     args = ap.parse_args()
     comm = init_distributed()
     rank, world = comm.rank, comm.world
@@ -156,6 +158,23 @@ def main():
     ok_a, _ = step_and_check(dp, plan, comm, shape, routs, acts, wts, report, "", steps=args.steps)
     ok &= ok_a
     report["memory"] = dp.memory_report()
+    if args.shared_layers:
+        # layer 2: its own routing and weights, the SAME layer-shared replica buffer; then layer 1
+        # again (its replicas are pulled again after layer 2 used the slots)
+        routs2 = [make_routing(shape, T, MB, world, r, zipf_s=args.zipf, shift=cfg["shift"], seed=4242)
+                  for r in range(world)]
+        plan2 = build_step_plan(args.policy, routs2[0].mats, topo, model, topo.profile, cfgs, shape)
+        wts2 = make_weights(shape, seed=4321)
+        dp2 = MoEDataPlane(comm, shape, T, MB, plan2, wgrad_mode=args.wgrad_mode, replica_buffer=dp.rb)
+        home2 = np.flatnonzero(plan2.home == rank)
+        dp2.set_weights(wts2[0][home2].cuda(), wts2[1][home2].cuda(), wts2[2][home2].cuda())
+        acts2 = [make_activations(shape, T, MB, r, seed=123) for r in range(world)]
+        ok2, _ = step_and_check(dp2, plan2, comm, shape, routs2, acts2, wts2, report, "L2_")
+        ok3, _ = step_and_check(dp, plan, comm, shape, routs, acts, wts, report, "L1again_")
+        report["shared_buffer_users"] = dp.rb.users
+        report["layer2_replica_bytes_added"] = 0 if dp2.rb is dp.rb else -1
+        ok &= ok2 and ok3 and dp2.rb is dp.rb
+        dp2.close()
     if plan_b is not None:
         gW1, gW2 = dp.grads()
         mine = {int(e): (gW1[s].cpu(), gW2[s].cpu()) for s, e in enumerate(home_a)}

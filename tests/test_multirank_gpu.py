@@ -72,6 +72,16 @@ def test_oversubscribed_replica_step(world, config, tokens, zipf, mode, sets, mi
         assert sum(r["migration"]["moved"] for r in reports) > 0
 
 
+def test_oversubscribed_layers_share_the_replica_buffer():
+    """Two MoE layers (own routing, own weights) share one layer-shared replica buffer: each layer's
+    replicas are pulled into the same r slots right before use, gradients pushed back per
+    micro-batch; both layers and a repeat of the first match the oracle."""
+    args = ["--config", "qwen3-30b-a3b", "--tokens", 1024, "--micro-batches", 2, "--zipf", 1.5, "--group", 4,
+            "--replica-sets", 1, "--min-copies", 2, "--shared-layers"]
+    reports = _check(*_launch(4, args), 4)
+    assert all(r["shared_buffer_users"] == 2 for r in reports)
+
+
 def test_oversubscribed_two_groups():
     """EP=4 as two groups of 2: reordering across groups, replication inside a group."""
     args = ["--config", "qwen3-30b-a3b", "--tokens", 1024, "--micro-batches", 2, "--zipf", 1.5, "--group", 2,
