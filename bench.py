@@ -109,6 +109,9 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- CPU reference arm
 
+REF_SAMPLE_TOKENS = 8192   # fixed layer-port sample per CPU-arm step (2048 spread 21% over 10 steps)
+
+
 def cpu_reference_step(args, world, threads: int, reps: int = 1) -> dict:
     """One step of the CPU reference path on the host cores (oracle/ref_arm.py): the reference's
     own planners (moebalance from oracle/_ref: build_policy_bundle("relibra") over the step's
@@ -121,8 +124,9 @@ def cpu_reference_step(args, world, threads: int, reps: int = 1) -> dict:
     slots = cfg["slots"] if args.slots is None else args.slots
     group = min(world, args.group or cfg["group"])
     tokens_step = world * args.tokens * args.micro_batches
-    layer_tps = ref_arm.port_layer_tokens_per_s(args.config, args.zipf, threads, reps=reps)
-    out = {"layer_port_tokens_per_s": layer_tps, "layer_sample_tokens": 2048}
+    layer_tps = ref_arm.port_layer_tokens_per_s(args.config, args.zipf, threads, sample_tokens=REF_SAMPLE_TOKENS,
+                                                reps=reps)
+    out = {"layer_port_tokens_per_s": layer_tps, "layer_sample_tokens": REF_SAMPLE_TOKENS}
     mb = ref_arm.load_reference()
     if mb is not None:
         r = make_routing(shape, args.tokens, args.micro_batches, world, 0, zipf_s=args.zipf, shift=hot_shift(args, cfg))
@@ -140,7 +144,7 @@ def cpu_reference_step(args, world, threads: int, reps: int = 1) -> dict:
     out["kind"] = "reference" if mb is not None else "port"
     out["sample"] = (f"per step: the reference's planners on the step's routing ({args.micro_batches} micro-batches x "
                      f"{world} GPUs, {args.sa_chains} SA chains) + the fp32 layer port at the rate of a fixed "
-                     f"2048-token sample, scaled to the step's {tokens_step} tokens")
+                     f"{REF_SAMPLE_TOKENS}-token sample, scaled to the step's {tokens_step} tokens")
     return out
 
 
@@ -674,7 +678,7 @@ def run_ours(args, comm):
     if check is not None:
         line["check"] = check
     if rank == 0 and world == 1 and not args.no_cpu_baseline and trace is None:
-        r = cpu_reference_step(args, world, os.cpu_count() or 1, reps=3)
+        r = cpu_reference_step(args, world, os.cpu_count() or 1, reps=2)
         line["cpu_baseline"] = {"value": r["value"], "unit": "tokens/s", "cores": os.cpu_count(), "kind": r["kind"],
                                 "sample": r["sample"], "planner": r["planner"],
                                 **{k: r[k] for k in ("planner_s_threads1", "planner_s_threadsN",

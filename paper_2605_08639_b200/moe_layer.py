@@ -156,14 +156,22 @@ class StepPlan:
         return np.stack([mb.flow.sum(axis=1) - np.diag(mb.flow) for mb in self.mbs])
 
 
+def _device_tables_default() -> bool:
+    """Integer split + dispatch tables on the GPU whenever one is present (MB_DEVICE_TABLES=0: host)."""
+    return os.environ.get("MB_DEVICE_TABLES", "1") == "1" and torch.cuda.is_available()
+
+
 def build_step_plan(policy: str, mats: np.ndarray, topo: ClusterTopology, model: rt.ModelProfile,
                     hw: HardwareProfile, cfgs: pol.SimConfigs, shape: LayerShape,
-                    device_tables: bool = False) -> StepPlan:
+                    device_tables: bool | None = None) -> StepPlan:
     """Plan one step (one batch of MB micro-batches, one layer) from the gathered (MB, G, E)
     routing matrices, with the reference policies (sim.build_policy_bundle, sim.py:214-280).
     'balanced_oracle' is planned like 'static': its token routing must already be uniform.
     device_tables: the integer split and dispatch tables are computed on the GPU
-    (mb_dispatch_tables) instead of the host planner library (identical tables)."""
+    (mb_dispatch_tables) instead of the host planner library (identical tables); default: on
+    when a GPU is present."""
+    if device_tables is None:
+        device_tables = _device_tables_default()
     trace = rt.build_trace(model, topo, mats[:, None], tokens_per_gpu=0)
     pol_name = "static" if policy == "balanced_oracle" else policy
     bundle, _ = pol.build_policy_bundle(trace, pol_name, topo, model, hw, cfgs)
@@ -218,9 +226,11 @@ def _device_dispatch_tables(x: np.ndarray, home: np.ndarray, placement, split, m
 
 
 def step_plan_from_bundle(policy: str, bundle: pol.PlanBundle, mats: np.ndarray, shape: LayerShape,
-                          layer: int = 0, slots: int = 0, device_tables: bool = False) -> StepPlan:
+                          layer: int = 0, slots: int = 0, device_tables: bool | None = None) -> StepPlan:
     """Device tables of one layer's step from a PlanBundle (planned here, or loaded from the
     reorder.json / replication.json files of planio.solve or the reference's `solve`)."""
+    if device_tables is None:
+        device_tables = _device_tables_default()
     mbs_n, g, e = mats.shape
     home = np.asarray(bundle.reorder[layer].assignment, dtype=np.int64)
     if slots <= 0:  # loaded plans: the largest per-GPU replica count the files use
@@ -1244,7 +1254,6 @@ class _StepOps:
         # layer-shared replica weight slots: the buffer's bookkeeping (shared by the layers), this
         # layer's earlier pulls invalidated (its weights may have changed since)
         dp.rb.invalidate(dp.token)
-        self.x_ev = {}
         if not hasattr(dp, "_tail_stream"):
             dp._tail_stream = torch.cuda.Stream(device=dp.device)
         self.tail_stream = dp._tail_stream

@@ -44,7 +44,7 @@ def test_device_tables_match_host(name, world, group, zipf, policy):
     topo = b200_box_topology(world, group, b200_profile(shape.hidden))
     model = ModelProfile(1, shape.num_experts, shape.top_k, shape.hidden, shape.ffn)
     cfgs = SimConfigs(anneal=AnnealConfig(seeds=(0, 1, 2)), replica=ReplicaConfig(cfg["slots"]))
-    host = build_step_plan(policy, r.mats, topo, model, topo.profile, cfgs, shape)
+    host = build_step_plan(policy, r.mats, topo, model, topo.profile, cfgs, shape, device_tables=False)
     dev = build_step_plan(policy, r.mats, topo, model, topo.profile, cfgs, shape, device_tables=True)
     _same(host, dev)
 
@@ -60,6 +60,6 @@ def test_device_tables_on_reference_plan_files(case):
     mats_all = trace.matrices.astype(np.int64)
     for layer in range(min(2, tm.num_layers)):
         mats = mats_all[:, layer]
-        host = step_plan_from_bundle("relibra", bundle, mats, shape, layer=layer)
+        host = step_plan_from_bundle("relibra", bundle, mats, shape, layer=layer, device_tables=False)
         dev = step_plan_from_bundle("relibra", bundle, mats, shape, layer=layer, device_tables=True)
         _same(host, dev)
