@@ -178,7 +178,7 @@ def data_plane_config(world, shape, args=None):
     out = {"row_movers": movers, "comm_sms": ml.default_comm_sms(world, shape)}
     if args is not None:
         out["wgrad_mode"] = args.wgrad_mode
-        out["replica_sets"] = args.replica_sets or int(os.environ.get("MB_REPLICA_SETS", ml.REPLICA_SETS))
+        out["replica_sets"] = args.replica_sets or ml.default_replica_sets(shape)
     return out
 
 

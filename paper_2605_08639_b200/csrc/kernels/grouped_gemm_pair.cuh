@@ -38,6 +38,9 @@ struct PairTile {
 // (light epilogues: one 32-row x 128-byte output box; dSwiGLU epilogues: two 32-row x 64-byte
 // boxes -- 32 features of gate and of up -- that carry H in and dH / gate*act out), and a small
 // meta block (barriers + tile starts; the group table is read from global memory).
+#ifndef MB_PAIR_LIGHT_BOXES
+#define MB_PAIR_LIGHT_BOXES 1
+#endif
 #ifndef MB_SINGLE_STAGES
 #define MB_SINGLE_STAGES 4      // single-CTA variant: 48 KB stages (A 128 rows + all 256 columns of B)
 #endif
@@ -50,11 +53,13 @@ struct PairCfg : PairTile {
   static constexpr int kEpiWarps = MB_PAIR_EPI_WARPS;
   static constexpr int kThreads = 64 + 32 * kEpiWarps;
   static constexpr int TM = kPair ? 256 : 128;  // tile rows (per cluster)
-  static constexpr int kStages = kPair ? MB_PAIR_STAGES : MB_SINGLE_STAGES;
+  // MB_PAIR_LIGHT_BOXES=2: light epilogues double-buffer their output box (one operand stage less)
+  static constexpr int kOutBoxes = (kPair && !kHeavy) ? MB_PAIR_LIGHT_BOXES : 1;
+  static constexpr int kStages = kPair ? MB_PAIR_STAGES - (kOutBoxes - 1) : MB_SINGLE_STAGES;
   static constexpr int kABytes = 128 * BK * 2;  // this CTA's 128 rows of A
   static constexpr int kBBytes = (kPair ? 128 : 256) * BK * 2;  // this CTA's columns of B
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStagingBytes = kEpiWarps * kBoxBytes;
+  static constexpr int kStagingBytes = kEpiWarps * kBoxBytes * kOutBoxes;
   static constexpr int kMetaBytes = 512 + 4 * (kMaxGroups + 8);
   static constexpr int kSmemBytes = kStages * kStageBytes + kStagingBytes + kMetaBytes + 1024;
   static_assert(kSmemBytes <= 232448, "shared memory budget");
@@ -419,7 +424,7 @@ __device__ __forceinline__ void grouped_gemm_body(const GemmParams& p) {
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     const uint32_t tempty_leader0 = kPair ? mapa_shared(smem_u32(&tempty_bar[0]), 0) : 0u;
     const uint32_t tempty_leader1 = kPair ? mapa_shared(smem_u32(&tempty_bar[1]), 0) : 0u;
-    BoxStager<1> st{sStage + (warp - 2) * Cfg::kBoxBytes, 0, lane, p.debug};
+    BoxStager<Cfg::kOutBoxes> st{sStage + (warp - 2) * Cfg::kOutBoxes * Cfg::kBoxBytes, 0, lane, p.debug};
     uint64_t* hbar = hbar_base + (warp - 2);
     uint32_t hphase = 0;
     for (int it = 0;; ++it) {

@@ -59,8 +59,17 @@ WIDE_FFN = 4096
 WIDE_HIDDEN = 4096   # 4096-wide token rows (Qwen3-235B): its N=4 numbers were measured with 32 comm SMs
 # sets of the layer-shared replica weight slots (MoEDataPlane replica_sets; MB_REPLICA_SETS overrides):
 # one set = exactly the paper's layer-shared buffer (replica_memory "layer-shared"); the backward
-# pulls its replicas again.  N=4 Qwen3-30B-A3B: 19.40 ms/step with 1 set vs 19.30 with 2.
+# pulls its replicas again.  N=4 Qwen3-30B-A3B (9 MiB experts): 19.40 ms/step with 1 set vs 19.30
+# with 2.  Experts above REPLICA_SETS_BIG bytes (Mixtral-8x7B: 336 MiB) get a second set so the
+# backward reuses the forward's pull instead of moving the expert over NVLink again.
 REPLICA_SETS = 1
+REPLICA_SETS_BIG = 64 << 20
+
+
+def default_replica_sets(shape: "LayerShape") -> int:
+    if os.environ.get("MB_REPLICA_SETS"):
+        return int(os.environ["MB_REPLICA_SETS"])
+    return REPLICA_SETS if 6 * shape.hidden * shape.ffn <= REPLICA_SETS_BIG else 2
 # Row-mover engine per world size: "regs" = register-copy kernels (co-resident with the GEMM's
 # CTAs on every SM), "tma" = cp.async.bulk kernels, one block on each of the COMM_SMS SMs the
 # GEMM leaves free (bulk-copy scatter, register combine with a shared-memory reservation).
@@ -520,7 +529,7 @@ class MoEDataPlane:
             raise ValueError(f"wgrad_mode must be 'step' or 'micro_batch', got {wgrad_mode!r}")
         self.wgrad_mode = wgrad_mode
         if replica_sets is None:
-            replica_sets = int(os.environ.get("MB_REPLICA_SETS", REPLICA_SETS))
+            replica_sets = default_replica_sets(shape)
         if replica_sets < 1:
             raise ValueError("replica_sets must be >= 1")
         self.replica_sets = replica_sets

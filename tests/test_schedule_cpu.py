@@ -122,3 +122,14 @@ def test_comm_sm_defaults(monkeypatch):
     assert ml.default_comm_sms(4, SHAPES["qwen3-235b-a22b"]["shape"]) == 32
     assert ml.default_comm_sms(4, SHAPES["mixtral-8x7b"]["shape"]) == 8
     assert ml.ROW_MOVERS[1] == "regs" and ml.ROW_MOVERS_MULTI == "tma"
+
+
+def test_replica_set_defaults(monkeypatch):
+    """One layer-shared replica set (exactly replica_memory "layer-shared") unless an expert is big
+    enough that pulling it again for the backward costs more than a second set (Mixtral-8x7B)."""
+    from paper_2605_08639_b200 import moe_layer as ml
+    from paper_2605_08639_b200.workload import SHAPES
+    monkeypatch.delenv("MB_REPLICA_SETS", raising=False)
+    assert ml.default_replica_sets(SHAPES["qwen3-30b-a3b"]["shape"]) == 1
+    assert ml.default_replica_sets(SHAPES["qwen3-235b-a22b"]["shape"]) == 1
+    assert ml.default_replica_sets(SHAPES["mixtral-8x7b"]["shape"]) == 2
