@@ -78,11 +78,12 @@ def grouped_gemm(mode: int, A: torch.Tensor, B0: torch.Tensor, groups: torch.Ten
                  B1: torch.Tensor | None = None, c_slot_stride: int = 0,
                  segs: torch.Tensor | None = None, row_scale: torch.Tensor | None = None,
                  row_partial: torch.Tensor | None = None, single_cta: bool = False, sms: int = 0,
-                 stream=None, tail: bool = False) -> None:
+                 stream=None, cta1: bool = False) -> None:
     """K4: tcgen05 grouped GEMM; see include/mb_kernels.h for the five modes.  sms > 0: SMs the
     persistent grid covers for this launch (0 = the process default); stream: default current.
-    tail: the single-CTA member of the pair kernel family (cta_group::1, 128 x 256 tiles; groups of
-    128 rows), for the tail blocks of groups with an odd number of 128-row blocks."""
+    cta1: the single-CTA member of the pair kernel family (cta_group::1, 128 x 256 tiles, no half
+    tiles: a group pays at most 127 padded rows) -- the default of the data plane's non-gated
+    F-mode launches (measured faster than the pair on ragged expert groups, equal on even ones)."""
     _need_cuda(A, B0, groups, C, C2, aux, B1)
     for t in (A, B0, B1):
         if t is not None and (t.dtype != torch.bfloat16 or not t.is_contiguous()):
@@ -98,7 +99,7 @@ def grouped_gemm(mode: int, A: torch.Tensor, B0: torch.Tensor, groups: torch.Ten
     ldc2 = 0 if C2 is None else C2.shape[-1]
     ld_aux = 0 if aux is None else aux.shape[-1]
     lib = _lib()
-    nat.check(lib.mb_grouped_gemm(mode | (0x100 if single_cta else 0) | (0x200 if tail else 0), A.data_ptr(), a_rows,
+    nat.check(lib.mb_grouped_gemm(mode | (0x100 if single_cta else 0) | (0x200 if cta1 else 0), A.data_ptr(), a_rows,
                                   a_cols,
                                   B0.data_ptr(), b0_rows, nat.ptr(B1), b1_rows, b_cols, groups.data_ptr(),
                                   nat.ptr(segs), groups.shape[0], M, N, K,

@@ -85,6 +85,9 @@ WGRAD_ALL_SMS = os.environ.get("MB_WGRAD_ALL_SMS", "1") == "1"
 # MB_TAIL_TILES=1): measured no faster at N=1 (18.55-18.88 vs 18.57-18.78 ms/step; the tail kernel's
 # 48 KB stages carry twice the B bytes per SM), so the pair kernel's half tiles stay the default
 TAIL_TILES = os.environ.get("MB_TAIL_TILES", "0") == "1"
+# non-gated F-mode GEMMs in the single-CTA (cta_group::1) kernel; MB_CTA1_F=0: the pair kernel (A/B)
+CTA1_F = os.environ.get("MB_CTA1_F", "1") == "1"
+CTA1_DACT = os.environ.get("MB_CTA1_DACT", "0") == "1"   # the gated dAct too (A/B)
 # both weight gradients in one two-problem launch (mb_grouped_wgrad2); MB_WGRAD_MERGED=0: A/B
 WGRAD_MERGED = os.environ.get("MB_WGRAD_MERGED", "1") == "1"
 # overlap=False runs every phase in issue order on one stream with all SMs in the GEMM: at world 1
@@ -1450,11 +1453,16 @@ class _StepOps:
 
     # -------------------------------------------------------------- compute stream
     def _fgemm(self, m, mode, A, B0, **kw):
-        """One F-mode GEMM of micro-batch m: with TAIL_TILES, the 128-row tail blocks run in the
-        single-CTA kernel on a side stream (launched first, on a share of the SMs proportional to
-        their work) while the pair kernel -- dynamically scheduled, so it adapts -- takes the rest."""
+        """One F-mode GEMM of micro-batch m.  The non-gated modes run in the single-CTA member of
+        the pair family (128-row tiles, no half tiles: EP=1 ragged rows fwd1 1123 vs 1069, dX 1133 vs
+        1036, fwd2 1026 vs 979 TFLOP/s; equal on even 4096-row groups); the gated dAct in the pair
+        kernel.  With TAIL_TILES (opt-in) the pair kernel's odd tail blocks run in the single-CTA
+        kernel on a side stream instead."""
         dp = self.dp
         ng = dp.nslots[m]
+        if CTA1_F and (mode != K.GEMM_DGRAD_DSWIGLU_GATED or CTA1_DACT):
+            dp._gemm(mode, A, B0, dp.groups[m][:ng], cta1=True, **kw)
+            return
         gp, gt, share = dp.tail_groups[m]
         if not TAIL_TILES or gt is None:
             dp._gemm(mode, A, B0, dp.groups[m][:ng], **kw)
@@ -1462,7 +1470,7 @@ class _StepOps:
         ts = self.tail_stream
         ts.wait_stream(self.cs)
         tail_sms = int(min(64, max(2, round(dp.gemm_sms * share))))
-        K.grouped_gemm(mode, A, B0, gt, tail=True, sms=tail_sms, stream=ts, **kw)
+        K.grouped_gemm(mode, A, B0, gt, cta1=True, sms=tail_sms, stream=ts, **kw)
         dp.launches += 1
         dp._gemm(mode, A, B0, gp[:ng], **kw)
         self.cs.wait_stream(ts)

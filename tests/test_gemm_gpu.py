@@ -312,16 +312,17 @@ def test_wgrad_two_problems_one_launch():
     assert rel_err(C2b[1], ref) < 1e-3
 
 
+@pytest.mark.parametrize("rows", [[128, 128, 128], [384, 128, 256]])
 @pytest.mark.parametrize("mode", ["fwd_swiglu", "fwd_store", "dgrad_store", "dgrad_gated"])
-def test_single_cta_tail_variant_matches_pair(mode):
-    """The single-CTA (cta_group::1) member of the pair family gives the pair kernel's results on
-    128-row groups (the tail blocks of odd groups run there)."""
+def test_single_cta_variant_matches_pair(mode, rows):
+    """The single-CTA (cta_group::1, 128-row tiles) member of the pair family gives the pair
+    kernel's results, on groups of one and of several 128-row blocks (odd and even)."""
     torch.manual_seed(13)
     h, hp, G = 512, 256, 3
-    rows = [128, 128, 128]
-    a0 = [0, 128, 256]
-    R = 384
-    groups = K.make_groups(rows, a0, [2, 0, 1], rows_real=[128, 100, 1])
+    a0 = [sum(rows[:i]) for i in range(G)]
+    R = sum(rows)
+    real = [rows[0], rows[1] - 28, 1 + rows[2] // 2]
+    groups = K.make_groups(rows, a0, [2, 0, 1], rows_real=real)
     X = torch.randn(R, h, device=DEV).bfloat16()
     W1 = (torch.randn(G, 2 * hp, h, device=DEV) * 0.05).bfloat16()
     W2 = (torch.randn(G, h, hp, device=DEV) * 0.05).bfloat16()
@@ -330,17 +331,17 @@ def test_single_cta_tail_variant_matches_pair(mode):
         if mode == "fwd_swiglu":
             H = torch.zeros(R, 2 * hp, device=DEV).bfloat16()
             Act = torch.zeros(R, hp, device=DEV).bfloat16()
-            K.grouped_gemm(K.GEMM_FWD_SWIGLU, X, W1, groups, N=2 * hp, K=h, C=H, C2=Act, tail=tail)
+            K.grouped_gemm(K.GEMM_FWD_SWIGLU, X, W1, groups, N=2 * hp, K=h, C=H, C2=Act, cta1=tail)
             outs.append((H, Act))
         elif mode == "fwd_store":
             A = torch.randn(R, hp, generator=torch.Generator(device="cuda").manual_seed(3), device=DEV).bfloat16()
             Y = torch.zeros(R, h, device=DEV).bfloat16()
-            K.grouped_gemm(K.GEMM_FWD_STORE, A, W2, groups, N=h, K=hp, C=Y, tail=tail)
+            K.grouped_gemm(K.GEMM_FWD_STORE, A, W2, groups, N=h, K=hp, C=Y, cta1=tail)
             outs.append((Y,))
         elif mode == "dgrad_store":
             dH = torch.randn(R, 2 * hp, generator=torch.Generator(device="cuda").manual_seed(4), device=DEV).bfloat16()
             dX = torch.zeros(R, h, device=DEV).bfloat16()
-            K.grouped_gemm(K.GEMM_DGRAD_STORE, dH, W1, groups, N=h, K=2 * hp, C=dX, tail=tail)
+            K.grouped_gemm(K.GEMM_DGRAD_STORE, dH, W1, groups, N=h, K=2 * hp, C=dX, cta1=tail)
             outs.append((dX,))
         else:
             dY = torch.randn(R, h, generator=torch.Generator(device="cuda").manual_seed(5), device=DEV).bfloat16()
@@ -350,7 +351,7 @@ def test_single_cta_tail_variant_matches_pair(mode):
             act = torch.zeros(R, hp, device=DEV).bfloat16()
             part = torch.zeros(R, hp // 64, device=DEV)
             K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU_GATED, dY, W2, groups, N=hp, K=h, C=dH, C2=act, aux=H,
-                           row_scale=gate, row_partial=part, tail=tail)
+                           row_scale=gate, row_partial=part, cta1=tail)
             outs.append((dH, act, part))
     torch.cuda.synchronize()
     for a, b in zip(*outs):

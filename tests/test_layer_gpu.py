@@ -290,7 +290,7 @@ def test_per_plane_launch_settings():
     orig = Kmod.grouped_gemm
 
     def spy(*a, sms=0, **kw):
-        if not kw.get("tail"):       # tail launches take their own share of the plane's SMs
+        if not (kw.get("cta1") and kw.get("stream") is not None):   # opt-in side-stream tail launches
             seen.append(("gemm", sms))
         return orig(*a, sms=sms, **kw)
 

@@ -38,6 +38,8 @@ def main():
                     help="also time torch.bmm (cuBLAS) on the same balanced shapes, plain GEMMs without epilogues")
     ap.add_argument("--zipf-rows", action="store_true",
                     help="group rows = micro-batch 0 of the bench's skewed Qwen3 routing at EP=1 (128-padded)")
+    ap.add_argument("--single", action="store_true",
+                    help="F modes in the single-CTA (cta_group::1, 128-row tile) member of the pair family")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     a = ap.parse_args()
@@ -66,6 +68,12 @@ def main():
     gW1 = torch.zeros(G, 2 * hp, h, device=dev)
     gW2 = torch.zeros(G, h, hp, device=dev)
     flop = 2.0 * R * h * hp
+    if a.single:   # every F-mode launch below runs the single-CTA kernel
+        _gg = K.grouped_gemm
+
+        def _single(mode, *args, **kw):
+            return _gg(mode, *args, cta1=(mode != K.GEMM_WGRAD), **kw)
+        K.grouped_gemm = _single
     global timeit
     _t = timeit
     timeit = lambda fn: _t(fn, iters=a.iters, warmup=a.warmup)
