@@ -22,8 +22,9 @@ def load(path):
         recs[(int(d["ID"]), d["Kernel Name"])][d["Metric Name"]] = v
     agg = collections.defaultdict(lambda: [0, 0.0, 0.0, 0.0])
     for (_, name), m in recs.items():
-        if "grouped_gemm_pair_kernel" in name:
-            key = "K4 grouped_gemm_pair " + name[name.index("<"):name.index(">") + 1]
+        if "grouped_gemm_pair_kernel" in name or "grouped_gemm_single_kernel" in name:
+            fam = "pair" if "pair_kernel" in name else "cta1"
+            key = f"K4 grouped_gemm_{fam} " + name[name.index("<"):name.index(">") + 1]
         else:
             key = name.split("(")[0].replace("void ", "").split("<")[0]
         a = agg[key]

@@ -9,8 +9,9 @@ echo launches_rc=$?
 python tools/launch_summary.py gpurun_out/r02_launches_step.csv gpurun_out/r02_launches_step_summary.json \
     > gpurun_out/r02_launches_step_summary.txt 2>&1
 for m in fwd1_swiglu dgrad_gated dgrad_dx wgrad2; do
+  f=""; case $m in fwd1_swiglu|dgrad_dx) f="--single";; esac   # the step's kernel family per mode
   ncu --set full --clock-control none --import-source on -k regex:grouped_gemm -s 3 -c 1 \
-      -o gpurun_out/r02_${m}_zipf -f python tools/bench_gemm.py --zipf-rows --only $m --iters 1 --warmup 3 \
+      -o gpurun_out/r02_${m}_zipf -f python tools/bench_gemm.py --zipf-rows --only $m --iters 1 --warmup 3 $f \
       > gpurun_out/ncu_${m}.log 2>&1
   echo full_${m}_rc=$?
 done
