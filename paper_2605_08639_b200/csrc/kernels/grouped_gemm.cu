@@ -136,6 +136,12 @@ extern "C" int mb_grouped_wgrad2(const void* A0, const void* B0, int32_t M0, int
     return rc;
   p.tmB1 = p.tmB0;
   p.tmB1h = p.tmB0h;
+  // MB_WGRAD_CTA1=1: the single-CTA (cta_group::1, 128-row tile) member of the family (A/B)
+  static const bool cta1 = [] {
+    const char* e = std::getenv("MB_WGRAD_CTA1");
+    return e && e[0] == '1';
+  }();
+  if (cta1) return launch_pair<true, true, true, EPI_ACC_F32, false>(p, reinterpret_cast<cudaStream_t>(stream), gemm_sms);
   return launch_pair<true, true, true, EPI_ACC_F32>(p, reinterpret_cast<cudaStream_t>(stream), gemm_sms);
 }
 
