@@ -627,6 +627,10 @@ class MoEDataPlane:
         self._err_host, self.err_dev = hp_.value, dp_.value
         self._err_view = (ctypes.c_int32 * 4).from_address(self._err_host)
         self.xs = torch.cuda.Stream(device=self.device)      # comm stream: dispatch / combine / barriers
+        # compute stream of the fused step: the caller's stream, or (MB_COMPUTE_PRIORITY=high) an own
+        # high-priority stream, so GEMM CTAs are scheduled ahead of pending row-mover blocks
+        self._ks = (torch.cuda.Stream(device=self.device, priority=-1)
+                    if os.environ.get("MB_COMPUTE_PRIORITY") == "high" else None)
         self.cps = torch.cuda.Stream(device=self.device)     # copy-engine stream: replica weight pulls
         self.launches = 0
         self.timing = False       # record CUDA events around every K4 launch (bench roofline)
@@ -1036,7 +1040,7 @@ class MoEDataPlane:
         micro-batch at a time through begin_step / forward_mb / backward_mb / end_step."""
         self._check_inputs(False, x=x, idx=idx, gates=gates, dout=dout, out=out, dx=dx, dgate=dgate)
         self.check(sync=False)
-        ops = _StepOps(self, hooks)
+        ops = _StepOps(self, hooks, own_compute_stream=True)
         comm_fn = {"D": lambda m: ops.dispatch(m, x[m], idx[m], gates[m], idx, gates),
                    "C": lambda m: (ops.combine(m, gates[m], out[m]), ops.dout_dispatch(m, dout[m])),
                    "X": lambda m: ops.unpermute(m, dx[m], dgate[m])}
@@ -1069,7 +1073,8 @@ class MoEDataPlane:
                 if dep not in ev_comm:
                     raise RuntimeError(f"step schedule deadlock at {op}{m}")
                 cs.wait_event(ev_comm[dep])
-            comp_fn[op](m)
+            with torch.cuda.stream(cs):
+                comp_fn[op](m)
             ev_comp[(op, m)] = torch.cuda.Event()
             ev_comp[(op, m)].record(cs)
             pi += 1
@@ -1252,17 +1257,22 @@ class _StepOps:
     barrier; copy: replica weight pulls).  Every rank must call the phases in the same order:
     each comm phase contains collective device barriers."""
 
-    def __init__(self, dp: "MoEDataPlane", hooks=None):
+    def __init__(self, dp: "MoEDataPlane", hooks=None, own_compute_stream: bool = False):
+        """own_compute_stream (the fused step): the GEMMs run on the plane's compute stream (high
+        priority with MB_COMPUTE_PRIORITY=high) joined to the caller's stream at both ends."""
         self.dp, self.hooks = dp, hooks
-        self.cs = torch.cuda.current_stream()
+        self.user = torch.cuda.current_stream()
+        self.fresh = dp._wgrad_prepare()    # (lazy zero of idle experts on the caller's stream)
+        self.cs = dp._ks if (own_compute_stream and dp._ks is not None) else self.user
+        if self.cs is not self.user:
+            self.cs.wait_stream(self.user)
         self.xs = dp.xs if dp.overlap else self.cs
         self.st_x = self.xs.cuda_stream
-        self.xs.wait_stream(self.cs)
-        dp.cps.wait_stream(self.cs)
+        self.xs.wait_stream(self.user)
+        dp.cps.wait_stream(self.user)
         self.first = True
         self.start_ev = None
         self.prepared = set()
-        self.fresh = dp._wgrad_prepare()
         # layer-shared replica weight slots: the buffer's bookkeeping (shared by the layers), this
         # layer's earlier pulls invalidated (its weights may have changed since)
         dp.rb.invalidate(dp.token)
@@ -1565,19 +1575,22 @@ class _StepOps:
         replica gradients, right after the last backward; part A: the rest, after the last
         replica-gradient push-back, on every SM); then every stream joins the current one."""
         dp, cs, xs = self.dp, self.cs, self.xs
-        if dp.wgrad_mode == "step":
-            part_b, part_a = dp.wparts
-            if part_b is not None:
-                self._wgrad_step(part_b, None)
-            if part_a is not None:
-                if last_x_ev is not None:
-                    cs.wait_event(last_x_ev)
-                else:
-                    cs.wait_stream(xs)
-                # the comm stream is idle by now: the last weight-gradient launch takes every SM
-                self._wgrad_step(part_a, dp.all_sms if (WGRAD_ALL_SMS and dp.overlap) else None)
+        with torch.cuda.stream(cs):
+            if dp.wgrad_mode == "step":
+                part_b, part_a = dp.wparts
+                if part_b is not None:
+                    self._wgrad_step(part_b, None)
+                if part_a is not None:
+                    if last_x_ev is not None:
+                        cs.wait_event(last_x_ev)
+                    else:
+                        cs.wait_stream(xs)
+                    # the comm stream is idle by now: the last weight-gradient launch takes every SM
+                    self._wgrad_step(part_a, dp.all_sms if (WGRAD_ALL_SMS and dp.overlap) else None)
         cs.wait_stream(xs)
         cs.wait_stream(dp.cps)
+        if cs is not self.user:
+            self.user.wait_stream(cs)
 
 
 class MoELayerFunction(torch.autograd.Function):
