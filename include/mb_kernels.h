@@ -49,12 +49,16 @@ int mb_set_gemm_sms(int sms);
  * kblocks = sum of ceil(rows / 64)), so one wgrad launch can contract over every micro-batch. */
 enum {
   MB_GEMM_FWD_STORE = 0,     /* C[rows_g,N] = A[rows_g,K] . B_slot[N,K]^T           (Y = Act W2^T) */
-  MB_GEMM_FWD_SWIGLU = 1,    /* as above, epilogue C=H, C2=silu(gate)*up             (H = X W1^T)   */
+  MB_GEMM_FWD_SWIGLU = 1,    /* as above, epilogue C=H, C2=silu(gate)*up             (H = X W1^T)   *
+                              * row_scale != NULL (pair family): C2 = row_scale[row]*silu(gate)*up,
+                              * 0 on pad rows -- the data plane's pre-gated activation, so the down
+                              * GEMM yields gate*Y and dW2 = dY^T C2 needs no rewrite            */
   MB_GEMM_DGRAD_STORE = 2,   /* C[rows_g,N] = A[rows_g,K] . B_slot[K,N]              (dX = dH W1)   */
   MB_GEMM_DGRAD_DSWIGLU = 3, /* as above, epilogue SwiGLU backward with aux=H -> C=dH (dAct = dY W2) */
   MB_GEMM_WGRAD = 4,         /* C_slot[M,N] (+)= A[K_g,M]^T . B[K_g,N]               (dW)           */
   MB_GEMM_DGRAD_DSWIGLU_GATED = 5 /* A = raw dout rows; epilogue applies row_scale (gate): C = dH,
-                                     C2 = gate*act, row_partial[row][N/64] = partial <dout.W2, act>
+                                     C2 (optional, NULL = not written) = gate*act,
+                                     row_partial[row][N/64] = partial <dout.W2, act>
                                      whose sum is dgate = <dout, Y> (replaces the combine backward) */
 };
 /* mode | 0x100 forces the 1-CTA kernel (default: CTA-pair 256x256 tiles when the shape allows);

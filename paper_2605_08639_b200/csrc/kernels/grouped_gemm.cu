@@ -217,6 +217,7 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
                : pair ? launch_pair<false, false, false, EPI_STORE_BF16>(p, s, gemm_sms)
                       : launch_gemm<false, false, false, 256, EPI_STORE_BF16>(p, s);
       MB_CHECK_ARG(C2 != nullptr, "SwiGLU epilogue needs the activation output");
+      MB_CHECK_ARG(!row_scale || pair || tail, "gate-scaled SwiGLU needs the CTA-pair kernel family");
       return tail ? launch_pair<false, false, false, EPI_SWIGLU, false>(p, s, gemm_sms)
              : pair ? launch_pair<false, false, false, EPI_SWIGLU>(p, s, gemm_sms)
                     : launch_gemm<false, false, false, 256, EPI_SWIGLU>(p, s);
@@ -224,7 +225,7 @@ extern "C" int mb_grouped_gemm(int mode, const void* A, int64_t a_rows, int64_t 
     case MB_GEMM_DGRAD_DSWIGLU_GATED: {
       MB_CHECK_ARG((!force_single || tail) && N % 256 == 0 && K % 64 == 0 && a_cols == K && b_cols == N,
                    "gated dSwiGLU GEMM needs the CTA-pair kernel family and N %% 256 == 0 (N=%d K=%d)", N, K);
-      MB_CHECK_ARG(aux && C2 && row_scale && row_partial, "gated dSwiGLU needs H, Act out, gate and partials");
+      MB_CHECK_ARG(aux && row_scale && row_partial, "gated dSwiGLU needs H, gate and partials");
       if ((rc = make_tmap_bf16_2d(&p.tmA, A, a_cols, a_rows, a_cols * 2, 64, 128))) return rc;
       if ((rc = make_tmap_bf16_2d(&p.tmAh, A, a_cols, a_rows, a_cols * 2, 64, 64))) return rc;
       if ((rc = make_tmap_bf16_2d(&p.tmB0, B0, b_cols, b0_rows, b_cols * 2, 64, 64))) return rc;

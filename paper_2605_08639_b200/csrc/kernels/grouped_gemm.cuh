@@ -23,10 +23,11 @@ namespace mb {
 enum GemmEpi : int {
   EPI_STORE_BF16 = 0,  // C = bf16(acc)
   EPI_SWIGLU = 1,      // C = bf16(acc) (H, gate|up blocks of BN/2), C2 = bf16(silu(g)*u)
+                       //   (pair family with rscale: C2 = bf16(gate * silu(g)*u), 0 on pad rows)
   EPI_DSWIGLU = 2,     // acc = dAct; aux = H; C = dH (gate|up blocks of 2*BN)
   EPI_ACC_F32 = 3,     // C_slot (+)= acc (fp32)
   EPI_DSWIGLU_GATED = 4,  // acc = dout.W2 (unscaled); aux = H; rscale = gate per row:
-                          //   C = dH of gate*acc, C2 = gate*act (in place of Act, feeds dW2),
+                          //   C = dH of gate*acc, C2 (optional) = gate*act (feeds dW2),
                           //   rpart[row][N/64] = partial <acc, act> (dgate = <dout, Y>)
 };
 
@@ -98,7 +99,7 @@ struct GemmParams {
   int64_t ldc2;
   const void* aux;
   int64_t ld_aux;
-  const float* rscale;  // per-row scale (gate) for EPI_DSWIGLU_GATED
+  const float* rscale;  // per-row scale (gate) for EPI_DSWIGLU_GATED and (optional) EPI_SWIGLU
   float* rpart;         // per-row partial sums [rows][N/64] for EPI_DSWIGLU_GATED
   unsigned long long* prof;  // optional wait-cycle counters (MB_GEMM_PROF): producer/MMA/epilogue
   int* tile_counter;    // CTA-pair kernel: zeroed counter for dynamic tile scheduling (nullptr = static)

@@ -41,6 +41,9 @@ struct PairTile {
 #ifndef MB_PAIR_LIGHT_BOXES
 #define MB_PAIR_LIGHT_BOXES 1
 #endif
+#ifndef MB_HEAVY_DBUF
+#define MB_HEAVY_DBUF 0
+#endif
 #ifndef MB_SINGLE_STAGES
 #define MB_SINGLE_STAGES 4      // single-CTA variant: 48 KB stages (A 128 rows + all 256 columns of B)
 #endif
@@ -55,11 +58,15 @@ struct PairCfg : PairTile {
   static constexpr int TM = kPair ? 256 : 128;  // tile rows (per cluster)
   // MB_PAIR_LIGHT_BOXES=2: light epilogues double-buffer their output box (one operand stage less)
   static constexpr int kOutBoxes = (kPair && !kHeavy) ? MB_PAIR_LIGHT_BOXES : 1;
-  static constexpr int kStages = kPair ? MB_PAIR_STAGES - (kOutBoxes - 1) : MB_SINGLE_STAGES;
+  // MB_HEAVY_DBUF: the dSwiGLU epilogues of the pair kernel double-buffer their H boxes (one
+  // operand stage less), so the next 32-feature chunk's H loads while this one computes
+  static constexpr bool kHDbuf = kPair && kHeavy && MB_HEAVY_DBUF;
+  static constexpr int kStages = kPair ? MB_PAIR_STAGES - (kOutBoxes - 1) - (kHDbuf ? 1 : 0) : MB_SINGLE_STAGES;
   static constexpr int kABytes = 128 * BK * 2;  // this CTA's 128 rows of A
   static constexpr int kBBytes = (kPair ? 128 : 256) * BK * 2;  // this CTA's columns of B
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStagingBytes = kEpiWarps * kBoxBytes * kOutBoxes;
+  static constexpr int kWarpBoxes = kHDbuf ? 2 : kOutBoxes;   // 4 KB staging boxes per epilogue warp
+  static constexpr int kStagingBytes = kEpiWarps * kBoxBytes * kWarpBoxes;
   static constexpr int kMetaBytes = 512 + 4 * (kMaxGroups + 8);
   static constexpr int kSmemBytes = kStages * kStageBytes + kStagingBytes + kMetaBytes + 1024;
   static_assert(kSmemBytes <= 232448, "shared memory budget");
@@ -424,7 +431,7 @@ __device__ __forceinline__ void grouped_gemm_body(const GemmParams& p) {
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     const uint32_t tempty_leader0 = kPair ? mapa_shared(smem_u32(&tempty_bar[0]), 0) : 0u;
     const uint32_t tempty_leader1 = kPair ? mapa_shared(smem_u32(&tempty_bar[1]), 0) : 0u;
-    BoxStager<Cfg::kOutBoxes> st{sStage + (warp - 2) * Cfg::kOutBoxes * Cfg::kBoxBytes, 0, lane, p.debug};
+    BoxStager<Cfg::kOutBoxes> st{sStage + (warp - 2) * Cfg::kWarpBoxes * Cfg::kBoxBytes, 0, lane, p.debug};
     uint64_t* hbar = hbar_base + (warp - 2);
     uint32_t hphase = 0;
     for (int it = 0;; ++it) {
@@ -526,12 +533,16 @@ __device__ __forceinline__ void grouped_gemm_body(const GemmParams& p) {
           }
           st.template put2<false>(g0, g1, &p.tmC, tc.nb * TN + f0, out_row0);
           st.template put2<false>(u0, u1, &p.tmC, tc.nb * TN + 128 + f0, out_row0);
+          // with rscale: the activation leaves pre-scaled by the row's gate (0 on pad rows), so the
+          // down GEMM yields gate*Y for the combine and dW2 reads gate*act without a rewrite
+          const float gs = p.rscale ? (tile_row < gg.rows_real ? p.rscale[gg.a0 + tile_row] : 0.0f) : 1.0f;
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const uint32_t gw = i < 16 ? g0[i] : g1[i - 16];
             const uint32_t uw = i < 16 ? u0[i] : u1[i - 16];
             const float a0 = bf16lo(gw), a1 = bf16hi(gw), b0 = bf16lo(uw), b1 = bf16hi(uw);
-            w[i] = pack_bf16x2(__fdividef(a0, 1.0f + __expf(-a0)) * b0, __fdividef(a1, 1.0f + __expf(-a1)) * b1);
+            w[i] = pack_bf16x2(gs * (__fdividef(a0, 1.0f + __expf(-a0)) * b0),
+                               gs * (__fdividef(a1, 1.0f + __expf(-a1)) * b1));
           }
           st.template put<false>(w, &p.tmC2, tc.nb * (TN / 2) + f0, out_row0);
         } else if constexpr (kEpi == EPI_DSWIGLU || kEpi == EPI_DSWIGLU_GATED) {
@@ -544,90 +555,107 @@ __device__ __forceinline__ void grouped_gemm_body(const GemmParams& p) {
           const int64_t row = gg.a0 + tile_row;
           const bool real = !kGated || tile_row < gg.rows_real;
           const float gate = kGated ? (real ? p.rscale[row] : 0.0f) : 1.0f;
-          uint8_t* bufA = st.base;
-          uint8_t* bufB = st.base + kHalfBox;
-          uint4* rowA = reinterpret_cast<uint4*>(bufA + lane * 64);
-          uint4* rowB = reinterpret_cast<uint4*>(bufB + lane * 64);
           const int sw = (lane >> 1) & 3;   // 64B swizzle: 16-byte chunk j of row r sits at j ^ ((r >> 1) & 3)
+          // the warp's chunks: i = 0 .. n-1 -> segment hh = hh0 + i / 2, chunk c = i % 2
+          const int hh0 = half ? ch2 : 0;
+          const int n = half ? 2 : 4;
+          auto chunk_cols = [&](int i, int& blk, int& f) {
+            const int hh = hh0 + (i >> 1);
+            blk = tc.nb * 2 + ocol(hh) / 128;
+            f = ocol(hh) % 128 + (i & 1) * 32;   // first feature of the chunk within the block
+          };
+          // box set of chunk i: with kHDbuf two sets alternate, so chunk i+1's H loads while chunk
+          // i computes; otherwise one set (load, wait, compute, store per chunk)
+          auto set_base = [&](int i) { return st.base + (Cfg::kHDbuf ? (i & 1) * PairTile::kBoxBytes : 0); };
+          auto issue_h = [&](int i) {   // lane 0: H gate / up columns of chunk i into its box set
+            int blk, f;
+            chunk_cols(i, blk, f);
+            uint8_t* b = set_base(i);
+            bulk_wait_read<0>();  // earlier stores have drained that set
+            mbar_arrive_expect_tx(hbar, PairTile::kBoxBytes);
+            tma_load_2d(b, &p.tmAux, hbar, blk * 256 + f, out_row0);
+            tma_load_2d(b + kHalfBox, &p.tmAux, hbar, blk * 256 + 128 + f, out_row0);
+          };
+          if (lane == 0) issue_h(0);
+          float part = 0.0f;
 #pragma unroll 1
-          for (int hh = half ? ch2 : 0; hh < (half ? ch2 + 1 : 2); ++hh) {
-            const int blk = tc.nb * 2 + ocol(hh) / 128;
-            const int fo = ocol(hh) % 128;
-            float part = 0.0f;
-#pragma unroll 1
-            for (int c = 0; c < 2; ++c) {
-              const int f = fo + c * 32;   // first feature of this chunk within the block
-              if (lane == 0) {
-                bulk_wait_read<0>();  // earlier stores have drained both boxes
-                mbar_arrive_expect_tx(hbar, PairTile::kBoxBytes);
-                tma_load_2d(bufA, &p.tmAux, hbar, blk * 256 + f, out_row0);
-                tma_load_2d(bufB, &p.tmAux, hbar, blk * 256 + 128 + f, out_row0);
-              }
-              uint32_t d[32];
-              tmem_ld_32x32b_x32(t_acc + tcol(hh) + c * 32, d);
-              mbar_wait(hbar, hphase);
-              hphase ^= 1;
-              uint4 hg[4], hu[4];
+          for (int i = 0; i < n; ++i) {
+            int blk, f;
+            chunk_cols(i, blk, f);
+            const int hh = hh0 + (i >> 1);
+            uint8_t* bufA = set_base(i);
+            uint8_t* bufB = bufA + kHalfBox;
+            uint4* rowA = reinterpret_cast<uint4*>(bufA + lane * 64);
+            uint4* rowB = reinterpret_cast<uint4*>(bufB + lane * 64);
+            if (!Cfg::kHDbuf && i > 0 && lane == 0) issue_h(i);
+            uint32_t d[32];
+            tmem_ld_32x32b_x32(t_acc + tcol(hh) + (i & 1) * 32, d);
+            mbar_wait(hbar, hphase);
+            hphase ^= 1;
+            uint4 hg[4], hu[4];
 #pragma unroll
-              for (int v = 0; v < 4; ++v) {
-                hg[v] = rowA[v ^ sw];
-                hu[v] = rowB[v ^ sw];
-              }
-              tmem_ld_wait();
-              __syncwarp();  // every lane holds its H row before the boxes are rewritten
-              uint32_t wa[16];
+            for (int v = 0; v < 4; ++v) {
+              hg[v] = rowA[v ^ sw];
+              hu[v] = rowB[v ^ sw];
+            }
+            tmem_ld_wait();
+            __syncwarp();  // every lane holds its H row before the boxes are rewritten
+            if (Cfg::kHDbuf && i + 1 < n && lane == 0) issue_h(i + 1);  // only one load in flight per barrier
+            uint32_t wa[16];
 #pragma unroll
-              for (int v = 0; v < 4; ++v) {
-                const uint32_t gw[4] = {hg[v].x, hg[v].y, hg[v].z, hg[v].w};
-                const uint32_t uw[4] = {hu[v].x, hu[v].y, hu[v].z, hu[v].w};
-                uint32_t og[4], ou[4];
+            for (int v = 0; v < 4; ++v) {
+              const uint32_t gw[4] = {hg[v].x, hg[v].y, hg[v].z, hg[v].w};
+              const uint32_t uw[4] = {hu[v].x, hu[v].y, hu[v].z, hu[v].w};
+              uint32_t og[4], ou[4];
 #pragma unroll
-                for (int x = 0; x < 4; ++x) {
-                  float dg2[2], du2[2], ag2[2];
+              for (int x = 0; x < 4; ++x) {
+                float dg2[2], du2[2], ag2[2];
 #pragma unroll
-                  for (int h2 = 0; h2 < 2; ++h2) {
-                    const int col = v * 8 + x * 2 + h2;  // 0..31 within this chunk
-                    const float gv = h2 ? bf16hi(gw[x]) : bf16lo(gw[x]);
-                    const float uv = h2 ? bf16hi(uw[x]) : bf16lo(uw[x]);
-                    const float raw = __uint_as_float(d[col]);
-                    const float s = __fdividef(1.0f, 1.0f + __expf(-gv));
-                    const float act = gv * s * uv;
-                    if (kGated) part += raw * act;
-                    const float dav = gate * raw;
-                    du2[h2] = real ? dav * gv * s : 0.0f;
-                    dg2[h2] = real ? dav * uv * s * (1.0f + gv * (1.0f - s)) : 0.0f;
-                    ag2[h2] = real ? gate * act : 0.0f;
-                  }
-                  og[x] = pack_bf16x2(dg2[0], dg2[1]);
-                  ou[x] = pack_bf16x2(du2[0], du2[1]);
-                  wa[v * 4 + x] = pack_bf16x2(ag2[0], ag2[1]);
+                for (int h2 = 0; h2 < 2; ++h2) {
+                  const int col = v * 8 + x * 2 + h2;  // 0..31 within this chunk
+                  const float gv = h2 ? bf16hi(gw[x]) : bf16lo(gw[x]);
+                  const float uv = h2 ? bf16hi(uw[x]) : bf16lo(uw[x]);
+                  const float raw = __uint_as_float(d[col]);
+                  const float s = __fdividef(1.0f, 1.0f + __expf(-gv));
+                  const float act = gv * s * uv;
+                  if (kGated) part += raw * act;
+                  const float dav = gate * raw;
+                  du2[h2] = real ? dav * gv * s : 0.0f;
+                  dg2[h2] = real ? dav * uv * s * (1.0f + gv * (1.0f - s)) : 0.0f;
+                  ag2[h2] = real ? gate * act : 0.0f;
                 }
-                rowA[v ^ sw] = make_uint4(og[0], og[1], og[2], og[3]);
-                rowB[v ^ sw] = make_uint4(ou[0], ou[1], ou[2], ou[3]);
+                og[x] = pack_bf16x2(dg2[0], dg2[1]);
+                ou[x] = pack_bf16x2(du2[0], du2[1]);
+                wa[v * 4 + x] = pack_bf16x2(ag2[0], ag2[1]);
               }
+              rowA[v ^ sw] = make_uint4(og[0], og[1], og[2], og[3]);
+              rowB[v ^ sw] = make_uint4(ou[0], ou[1], ou[2], ou[3]);
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              const uint64_t pol = l2_evict_first_policy();
+              tma_store_2d(&p.tmC, bufA, blk * 256 + f, out_row0, pol);
+              tma_store_2d(&p.tmC, bufB, blk * 256 + 128 + f, out_row0, pol);
+              bulk_commit();
+            }
+            if (kGated && p.C2) {  // gate*act over Act (unless the forward wrote it pre-scaled)
+              if (lane == 0) bulk_wait_read<0>();
+              __syncwarp();
+#pragma unroll
+              for (int j = 0; j < 4; ++j) rowA[j ^ sw] = make_uint4(wa[4 * j], wa[4 * j + 1], wa[4 * j + 2], wa[4 * j + 3]);
               fence_proxy_async_smem();
               __syncwarp();
               if (lane == 0) {
-                const uint64_t pol = l2_evict_first_policy();
-                tma_store_2d(&p.tmC, bufA, blk * 256 + f, out_row0, pol);
-                tma_store_2d(&p.tmC, bufB, blk * 256 + 128 + f, out_row0, pol);
+                tma_store_2d(&p.tmC2, bufA, blk * 128 + f, out_row0, l2_evict_first_policy());
                 bulk_commit();
               }
-              if (kGated) {
-                if (lane == 0) bulk_wait_read<0>();
-                __syncwarp();
-#pragma unroll
-                for (int j = 0; j < 4; ++j) rowA[j ^ sw] = make_uint4(wa[4 * j], wa[4 * j + 1], wa[4 * j + 2], wa[4 * j + 3]);
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                  tma_store_2d(&p.tmC2, bufA, blk * 128 + f, out_row0, l2_evict_first_policy());
-                  bulk_commit();
-                }
-              }
             }
-            // partial <dAct, act> over these 64 features: rpart[row][N/64]
-            if (kGated && real) p.rpart[row * (p.N / 64) + blk * 2 + fo / 64] = part;
+            // partial <dAct, act> over the segment's 64 features: rpart[row][N/64]
+            if (i & 1) {
+              if (kGated && real) p.rpart[row * (p.N / 64) + blk * 2 + (f - 32) / 64] = part;
+              part = 0.0f;
+            }
           }
         } else {  // EPI_ACC_F32: fp32 boxes of 32 columns, reduce-add into the accumulator or store
           const bool accumulate = (gg.flags & 1) != 0;

@@ -88,6 +88,10 @@ TAIL_TILES = os.environ.get("MB_TAIL_TILES", "0") == "1"
 # non-gated F-mode GEMMs in the single-CTA (cta_group::1) kernel; MB_CTA1_F=0: the pair kernel (A/B)
 CTA1_F = os.environ.get("MB_CTA1_F", "1") == "1"
 CTA1_DACT = os.environ.get("MB_CTA1_DACT", "0") == "1"   # the gated dAct too (A/B)
+# Pre-gated activation: the gate/up GEMM's epilogue writes gate*act, so the down GEMM yields gate*Y,
+# the combine is a plain sum and the dAct epilogue no longer rewrites Act for dW2 (MB_PREGATE=0: the
+# round-1 layout, gate applied in the combine and gate*act written by dAct)
+PREGATE = os.environ.get("MB_PREGATE", "1") != "0"
 # both weight gradients in one two-problem launch (mb_grouped_wgrad2); MB_WGRAD_MERGED=0: A/B
 WGRAD_MERGED = os.environ.get("MB_WGRAD_MERGED", "1") == "1"
 # overlap=False runs every phase in issue order on one stream with all SMs in the GEMM: at world 1
@@ -1417,12 +1421,14 @@ class _StepOps:
         self.prepared.add(m)
 
     def combine(self, m, gates, out):
-        """K6: out[t] = sum_i gate * Y[perm(t, i)] over peer loads."""
+        """K6: out[t] = sum_i gate * Y[perm(t, i)] over peer loads (PREGATE: the rows already
+        hold gate * Y, so a plain sum)."""
         dp, xs = self.dp, self.xs
         h = dp.shape.hidden
         with dp._timed(dp.remote_rows(m)[0] * 2 * h, "comm_combine", xs):
             dp.arena.barrier(xs)  # Y of micro-batch m complete on every rank
-            dp._k("mb_combine_rows", dp.ptr_y[m].data_ptr(), dp.perm[m].data_ptr(), gates.data_ptr(), dp.T,
+            dp._k("mb_combine_rows", dp.ptr_y[m].data_ptr(), dp.perm[m].data_ptr(),
+                  None if PREGATE else gates.data_ptr(), dp.T,
                   dp.shape.top_k, h, out.data_ptr(), None, None, 1, dp.comm_blocks, self.st_x)
             if self.hooks:
                 self.hooks.after_forward(m, xs)
@@ -1496,7 +1502,7 @@ class _StepOps:
             i1 = self._replica_set("w1", m)
             with dp._timed(4.0 * rows * h * hp, "fwd_swiglu"):
                 self._fgemm(m, K.GEMM_FWD_SWIGLU, dp.Xr[a], dp.W1, N=2 * hp, K=h, C=dp.H[a], C2=dp.Act[a],
-                            B1=dp.W1r[i1])
+                            B1=dp.W1r[i1], row_scale=dp.gate_r[a] if PREGATE else None)
             self._replica_used("w1", i1, m)
             i2 = self._replica_set("w2", m)
             with dp._timed(2.0 * rows * h * hp, "fwd_down"):
@@ -1514,10 +1520,11 @@ class _StepOps:
             rows = dp.real_rows(m)
             i2 = self._replica_set("w2", m)
             # dAct = dout.W2 with the combine backward fused in the epilogue: gate applied per row,
-            # dgate partials <dout.W2, act> = <dout, Y>, gate*act written over Act for dW2
+            # dgate partials <dout.W2, act> = <dout, Y>; Act already holds gate*act for dW2
+            # (PREGATE; otherwise the epilogue writes it over Act)
             with dp._timed(2.0 * rows * h * hp, "dgrad_act_gated"):
                 self._fgemm(m, K.GEMM_DGRAD_DSWIGLU_GATED, dp.dYr[a], dp.W2, N=hp, K=h, C=dp.dH[a],
-                            C2=dp.Act[a], aux=dp.H[a], B1=dp.W2r[i2], row_scale=dp.gate_r[a],
+                            C2=None if PREGATE else dp.Act[a], aux=dp.H[a], B1=dp.W2r[i2], row_scale=dp.gate_r[a],
                             row_partial=dp.dgate_r[a])
             self._replica_used("w2", i2, m)
             i1 = self._replica_set("w1", m)

@@ -79,6 +79,32 @@ def test_fwd_swiglu():
         assert rel_err(Act[a0[g]:a0[g] + r], act) < 2e-2
 
 
+@pytest.mark.parametrize("cta1", [False, True])
+def test_fwd_swiglu_pregated(cta1):
+    """row_scale: the activation leaves scaled by the row's gate, pad rows (past rows_real) zero;
+    H is unscaled.  Odd 128-row blocks exercise the pair kernel's half tiles."""
+    torch.manual_seed(12)
+    hp, Kd = 256, 256
+    rows, real = [384, 128], [300, 128]
+    a0, R = _row_groups(rows)
+    A = torch.randn(R, Kd, device=DEV).bfloat16()
+    W = (torch.randn(2, 2 * hp, Kd, device=DEV) * Kd ** -0.5).bfloat16()
+    gate = torch.rand(R, device=DEV)
+    H = torch.zeros(R, 2 * hp, device=DEV).bfloat16()
+    Act = torch.full((R, hp), float("nan"), device=DEV).bfloat16()
+    K.grouped_gemm(K.GEMM_FWD_SWIGLU, A, W, K.make_groups(rows, a0, [0, 1], rows_real=real), N=2 * hp, K=Kd,
+                   C=H, C2=Act, row_scale=gate, cta1=cta1)
+    torch.cuda.synchronize()
+    for g, r in enumerate(rows):
+        h = A[a0[g]:a0[g] + r].float() @ W[g].float().T
+        assert rel_err(H[a0[g]:a0[g] + r], h) < 2e-2
+        hb = H[a0[g]:a0[g] + r].float().view(r, -1, 2, 128)   # the act is computed from bf16 H
+        act = (torch.nn.functional.silu(hb[:, :, 0]) * hb[:, :, 1]).reshape(r, hp)
+        sl = slice(a0[g], a0[g] + real[g])
+        assert rel_err(Act[sl], gate[sl, None] * act[:real[g]]) < 2e-2
+        assert torch.all(Act[a0[g] + real[g]:a0[g] + r] == 0)
+
+
 def test_dgrad_store():
     torch.manual_seed(3)
     N, Kd = 512, 384
@@ -151,6 +177,15 @@ def test_dgrad_dswiglu_gated(rows, real):
         assert rel_err(part[sl].sum(1), (raw * act).sum(1)) < 2e-2
         pad = slice(a0[g] + real[g], a0[g] + rows[g])
         assert torch.all(dH[pad] == 0) and torch.all(actg[pad] == 0)
+    # without C2 (the data plane's pre-gated layout): same dH and partials, nothing else written
+    dH2 = torch.full_like(dH, float("nan"))
+    part2 = torch.zeros_like(part)
+    K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU_GATED, dout, W2, K.make_groups(rows, a0, list(range(S)), rows_real=real),
+                   N=hp, K=hd, C=dH2, aux=H, row_scale=gate, row_partial=part2)
+    torch.cuda.synchronize()
+    for g in range(S):
+        sl = slice(a0[g], a0[g] + real[g])
+        assert torch.equal(dH2[sl], dH[sl]) and torch.equal(part2[sl], part[sl])
 
 
 def test_single_cta_path_matches_pair():

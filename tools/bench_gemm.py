@@ -84,6 +84,10 @@ def main():
     if not only or "dgrad_dswiglu" in only: res["dgrad_dswiglu"] = (timeit(lambda: K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU, dY, W2, groups, N=hp, K=h, C=dH, aux=H)), flop)
     gate = torch.rand(R, device=dev)
     part = torch.empty(R, hp // 64, device=dev)
+    if only and "dgrad_gated_noact" in only:  # pre-gated layout: no gate*act rewrite
+        res["dgrad_gated_noact"] = (timeit(lambda: K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU_GATED, dY, W2, groups, N=hp, K=h, C=dH, aux=H, row_scale=gate, row_partial=part)), flop)
+    if only and "fwd1_pregated" in only:
+        res["fwd1_pregated"] = (timeit(lambda: K.grouped_gemm(K.GEMM_FWD_SWIGLU, X, W1, groups, N=2 * hp, K=h, C=H, C2=Act, row_scale=gate)), 2 * flop)
     if only and "dgrad_gated" in only: res["dgrad_gated"] = (timeit(lambda: K.grouped_gemm(K.GEMM_DGRAD_DSWIGLU_GATED, dY, W2, groups, N=hp, K=h, C=dH, C2=Act, aux=H, row_scale=gate, row_partial=part)), flop)
     if not only or "dgrad_dx" in only: res["dgrad_dx"] = (timeit(lambda: K.grouped_gemm(K.GEMM_DGRAD_STORE, dH, W1, groups, N=h, K=2 * hp, C=dX)), 2 * flop)
     if not only or "wgrad_w2" in only: res["wgrad_w2"] = (timeit(lambda: K.grouped_gemm(K.GEMM_WGRAD, dY, Act, wg, M=h, N=hp, C=gW2, c_slot_stride=h * hp)), flop)
