@@ -104,7 +104,8 @@ struct GemmParams {
   unsigned long long* prof;  // optional wait-cycle counters (MB_GEMM_PROF): producer/MMA/epilogue
   int* tile_counter;    // CTA-pair kernel: zeroed counter for dynamic tile scheduling (nullptr = static)
   int M2, N2;           // W mode, groups with flag 4: the second problem (A = tmAh, B = tmB0h, C = tmC2)
-  int debug;            // bit0: skip the epilogue (TMEM drained, nothing stored) -- profiling only
+  int debug;            // bit0: skip the epilogue (TMEM drained, nothing stored); 128 / 256: dSwiGLU
+                        // epilogue without its H loads / dH stores -- profiling only
 };
 
 template <int BN>

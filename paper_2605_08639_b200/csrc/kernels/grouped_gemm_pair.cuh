@@ -41,6 +41,9 @@ struct PairTile {
 #ifndef MB_PAIR_LIGHT_BOXES
 #define MB_PAIR_LIGHT_BOXES 1
 #endif
+#ifndef MB_W_EVICT_LAST
+#define MB_W_EVICT_LAST 0       // wgrad operand loads with an L2 evict_last hint (A/B)
+#endif
 #ifndef MB_HEAVY_DBUF
 #define MB_HEAVY_DBUF 0
 #endif
@@ -299,6 +302,8 @@ __device__ __forceinline__ void grouped_gemm_body(const GemmParams& p) {
         const bool half = kPair && !kW && half_tile(gg, tc, p.debug);
         const int bytes = !kPair ? Cfg::kStageBytes : half ? 2 * (Cfg::kABytes / 2 + Cfg::kBBytes) : 2 * Cfg::kStageBytes;
         KWalker kw(gg, p.segs);
+        // wgrad operands are re-read by every tile of the expert's other dimension: keep them in L2
+        const uint64_t w_policy = (kW && MB_W_EVICT_LAST) ? l2_evict_last_policy() : 0;
         for (int kb = 0; kb < tc.kblocks; ++kb) {
           int nk16 = BK / 16;
           const int krow = kW ? kw.step(nk16) : 0;
@@ -318,7 +323,8 @@ __device__ __forceinline__ void grouped_gemm_body(const GemmParams& p) {
           uint8_t* b_dst = sB + stage * Cfg::kBBytes;
           // pair: bytes complete on the leader's barrier (cta_group::2 form); single: own barrier
           auto load2d = [&](void* dst, const CUtensorMap* map, int32_t c0, int32_t c1) {
-            if constexpr (kPair) tma_load_2d_pair(dst, map, lbar, c0, c1);
+            if constexpr (kPair && kW && MB_W_EVICT_LAST) tma_load_2d_pair_hint(dst, map, lbar, c0, c1, w_policy);
+            else if constexpr (kPair) tma_load_2d_pair(dst, map, lbar, c0, c1);
             else tma_load_2d(dst, map, &full_bar[stage], c0, c1);
           };
           if (!kAmn) {
@@ -572,6 +578,10 @@ __device__ __forceinline__ void grouped_gemm_body(const GemmParams& p) {
             chunk_cols(i, blk, f);
             uint8_t* b = set_base(i);
             bulk_wait_read<0>();  // earlier stores have drained that set
+            if (p.debug & 128) {  // profiling only: no H loads (the boxes' stale contents are used)
+              mbar_arrive(hbar);
+              return;
+            }
             mbar_arrive_expect_tx(hbar, PairTile::kBoxBytes);
             tma_load_2d(b, &p.tmAux, hbar, blk * 256 + f, out_row0);
             tma_load_2d(b + kHalfBox, &p.tmAux, hbar, blk * 256 + 128 + f, out_row0);
@@ -633,7 +643,7 @@ __device__ __forceinline__ void grouped_gemm_body(const GemmParams& p) {
             }
             fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) {
+            if (lane == 0 && !(p.debug & 256)) {  // (debug 256, profiling only: no dH stores)
               const uint64_t pol = l2_evict_first_policy();
               tma_store_2d(&p.tmC, bufA, blk * 256 + f, out_row0, pol);
               tma_store_2d(&p.tmC, bufB, blk * 256 + 128 + f, out_row0, pol);
