@@ -81,6 +81,9 @@ ROW_MOVERS_MULTI = "tma"
 # is idle (N=4: 18.9-19.0 -> 18.7-18.9 ms; at N=1 widening the single launch measured 3% slower).
 # MB_WGRAD_ALL_SMS=0: A/B.
 WGRAD_ALL_SMS = os.environ.get("MB_WGRAD_ALL_SMS", "1") == "1"
+# per-micro-batch replica weight gradients on every SM instead of the GEMM's share (A/B: their
+# ~2.4 waves of long tiles on the 60 GEMM clusters leave the last wave 40% full)
+REPLICA_WGRAD_ALL_SMS = os.environ.get("MB_REPLICA_WGRAD_ALL_SMS", "0") == "1"
 # 128-row tail blocks of odd groups in the single-CTA kernel beside the pair kernel (opt-in,
 # MB_TAIL_TILES=1): measured no faster at N=1 (18.55-18.88 vs 18.57-18.78 ms/step; the tail kernel's
 # 48 KB stages carry twice the B bytes per SM), so the pair kernel's half tiles stay the default
@@ -1537,7 +1540,8 @@ class _StepOps:
             tabs, segs, rrows = rw
             a, q = dp.set_index(m), m % GRAD_RING
             with dp._timed(6.0 * rrows * h * hp, "wgrad_replica"):
-                self._wgrad_launch(tabs, segs, dp.dYr[a], dp.Act[a], dp.rgW2[q], dp.dH[a], dp.Xr[a], dp.rgW1[q])
+                self._wgrad_launch(tabs, segs, dp.dYr[a], dp.Act[a], dp.rgW2[q], dp.dH[a], dp.Xr[a], dp.rgW1[q],
+                                   sms=dp.all_sms if REPLICA_WGRAD_ALL_SMS else None)
 
     def _wgrad_launch(self, tabs, segs, dY, act, c2, dh, xr, c1, sms=None):
         """dW2 (C2 (+)= dY^T act) and dW1 (C1 (+)= dH^T X) of the groups in `tabs`: one two-problem
