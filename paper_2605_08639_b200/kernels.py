@@ -18,7 +18,7 @@ GEMM_DGRAD_DSWIGLU = 3
 GEMM_WGRAD = 4
 GEMM_DGRAD_DSWIGLU_GATED = 5
 
-GROUP_FIELDS = 8  # int32 rows, a0, slot, flags, seg_begin, seg_count, pad, pad
+GROUP_FIELDS = 8  # int32 rows, a0, slot, flags, seg_begin, seg_count, rows_real, kblocks
 FLAG_ACCUMULATE = 1
 FLAG_REPLICA = 2
 FLAG_PROBLEM2 = 4   # grouped_wgrad2: the group belongs to the second problem (dW1)

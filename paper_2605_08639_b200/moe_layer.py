@@ -425,12 +425,26 @@ ERR_BITS = {1: "routing has more tokens for an expert than the step plan's count
             2: "device histogram differs from the counts the step plan was built for"}
 
 
+# weight-gradient groups longest-K first (dW2 and dW1 of an expert side by side in the two-problem
+# table), so the dynamic tile scheduler ends a launch on the short tiles; MB_WGRAD_LPT=0: expert order
+WGRAD_LPT = os.environ.get("MB_WGRAD_LPT", "1") == "1"
+
+
 def _wgrad_tables(tab: np.ndarray, dev) -> tuple:
     """(single-problem table, two-problem table) of a wgrad group table: the second lists every
-    group twice, the copy flagged FLAG_PROBLEM2 (dW1 beside dW2 in one launch)."""
+    group twice, the copy flagged FLAG_PROBLEM2 (dW1 beside dW2 in one launch).  With WGRAD_LPT the
+    groups are ordered by K blocks, longest first (each output tile is still computed by exactly
+    one tile in a fixed K order, so the results do not depend on the order)."""
+    if WGRAD_LPT and len(tab) > 1:
+        tab = tab[np.argsort(-tab[:, 7].astype(np.int64), kind="stable")]
     t2 = tab.copy()
     t2[:, 3] |= K.FLAG_PROBLEM2
-    merged = np.concatenate([tab, t2]) if len(tab) * 2 <= K.MAX_GROUPS else None
+    if len(tab) * 2 > K.MAX_GROUPS:
+        merged = None
+    elif WGRAD_LPT:
+        merged = np.stack([tab, t2], axis=1).reshape(-1, tab.shape[1])
+    else:
+        merged = np.concatenate([tab, t2])
     return (torch.from_numpy(np.ascontiguousarray(tab)).to(dev),
             None if merged is None else torch.from_numpy(np.ascontiguousarray(merged)).to(dev))
 
