@@ -707,7 +707,7 @@ def main():
     ap.add_argument("--policies", default="relibra,static,eplb_like,balanced_oracle,relibra_box",
                     help="relibra_box = relibra with one replication group spanning all EP GPUs (run when EP > group)")
     ap.add_argument("--headline", default="relibra")
-    ap.add_argument("--repeats", type=int, default=3,
+    ap.add_argument("--repeats", type=int, default=5,
                     help="interleaved repetitions of every policy (rotated order); value = the headline's median")
     ap.add_argument("--batches", type=int, default=4,
                     help="batches of the shifting-routing sequence (new plan + expert migration per batch); 1 = off")
