@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--tokens", type=int, default=8192)
     ap.add_argument("--micro-batches", type=int, default=8)
     ap.add_argument("--policy", default="relibra")
+    ap.add_argument("--back-to-back", type=int, default=1,
+                    help="steps issued without a host sync; the last is reported (1 = synced single step)")
     args = ap.parse_args()
     comm = init_distributed()
     torch.cuda.set_device(local_device())
@@ -51,18 +53,24 @@ def main():
            "gates": torch.from_numpy(r.gates).cuda()}
     out, dx = torch.empty_like(dev["x"]), torch.empty_like(dev["x"])
     dgate = torch.empty(MB, T, shape.top_k, dtype=torch.float32, device="cuda")
-    for it in range(4):
+    # warm-up, then (--back-to-back) steps issued without a host sync between them, as in the bench:
+    # the last one is reported, so the host's lead over the GPU hides its launch work
+    for it in range(3):
         dp.zero_grads()
-        torch.cuda.synchronize()
-        comm.host_barrier()
-        dp.timing = it == 3
+        dp.step(dev["x"], dev["idx"], dev["gates"], dev["dout"], out, dx, dgate)
+    torch.cuda.synchronize()
+    comm.host_barrier()
+    n = max(1, args.back_to_back)
+    for it in range(n):
+        dp.zero_grads()
+        dp.timing = it == n - 1
         dp.gemm_events = []
         s0 = torch.cuda.Event(enable_timing=True)
         e0 = torch.cuda.Event(enable_timing=True)
         s0.record()
         dp.step(dev["x"], dev["idx"], dev["gates"], dev["dout"], out, dx, dgate)
         e0.record()
-        torch.cuda.synchronize()
+    torch.cuda.synchronize()
     ev = [(s0.elapsed_time(a), s0.elapsed_time(b), kd) for a, b, _, kd in dp.gemm_events]
     gemm = sorted([e for e in ev if not e[2].startswith("comm_")])
     gaps, prev = [], 0.0
