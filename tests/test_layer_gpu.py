@@ -4,6 +4,10 @@ Integer outputs (device histogram, canonical permutation) must be bit-exact; lay
 and gradients must be within the documented bf16 tolerance rel 2e-2 of the fp32 oracle.
 """
 
+import os
+import subprocess
+import sys
+
 import numpy as np
 import pytest
 import torch
@@ -320,3 +324,16 @@ def test_per_plane_launch_settings():
         Kmod.grouped_gemm = orig
     dpa.close()
     dpb.close()
+
+
+def test_layout_without_pregated_activation():
+    """MB_PREGATE=0 (the gate applied in the combine, gate*act written over Act by the dAct
+    epilogue for dW2) still matches the oracle: the layer tests in a fresh process."""
+    env = dict(os.environ, MB_PREGATE="0")
+    ids = [f"{__file__}::test_layer_step_matches_oracle[{c}]" for c in ("tiny-256-2-step", "qwen3-30b-a3b-512-2-step",
+                                                                       "tiny-256-4-micro_batch")]
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", *ids], env=env,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "3 passed" in r.stdout
