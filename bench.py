@@ -175,7 +175,9 @@ def data_plane_config(world, shape, args=None):
     sets (MoEDataPlane defaults / env overrides)."""
     from paper_2605_08639_b200 import moe_layer as ml
     movers = os.environ.get("MB_ROW_MOVERS") or ml.ROW_MOVERS.get(world, ml.ROW_MOVERS_MULTI)
-    out = {"row_movers": movers, "comm_sms": ml.default_comm_sms(world, shape)}
+    out = {"row_movers": movers, "comm_sms": ml.default_comm_sms(world, shape),
+           "dispatch_tables": "device" if os.environ.get("MB_DEVICE_TABLES", "1") == "1" else "host",
+           "activation": "pre-gated" if ml.PREGATE else "gate in combine"}
     if args is not None:
         out["wgrad_mode"] = args.wgrad_mode
         out["replica_sets"] = args.replica_sets or ml.default_replica_sets(shape)
