@@ -384,7 +384,13 @@ def default_comm_sms(world: int, shape: "LayerShape") -> int:
     return COMM_SMS.get(world, COMM_SMS_MULTI)
 
 
-def schedule(mb: int, wgrad_mode: str = "step"):
+# the last micro-batch's combine ahead of the third-to-last un-permute on the comm stream (step
+# mode): B(MB-1) is otherwise the one backward with no comm cover -- it waits for C(MB-1), queued
+# behind X(MB-3); MB_EARLY_LAST_COMBINE=0: the plain rotation
+EARLY_LAST_COMBINE = os.environ.get("MB_EARLY_LAST_COMBINE", "1") == "1"
+
+
+def schedule(mb: int, wgrad_mode: str = "step", early_last: bool | None = None):
     """Per-rank issue order of one step, two micro-batches in flight (the two-batch overlap of
     EP training systems): compute runs F0 F1 B0 F2 B1 ... F(n-1) B(n-2) B(n-1), the comm stream
     D0 D1 C0 [D(m) C(m-1) X(m-2)]... so every all-to-all overlaps a GEMM phase of the neighbouring
@@ -410,7 +416,29 @@ def schedule(mb: int, wgrad_mode: str = "step"):
     if mb > 1:
         comm += [("C", mb - 1), ("X", mb - 2)]
     comm.append(("X", mb - 1))
+    if (EARLY_LAST_COMBINE if early_last is None else early_last) and wgrad_mode == "step" and mb >= 3:
+        comm.remove(("X", mb - 3))
+        comm.insert(comm.index(("C", mb - 1)) + 1, ("X", mb - 3))
     return comm, comp
+
+
+def replica_ring_guards(comm: list, mb: int) -> dict:
+    """{m: x}: B(m)'s replica weight gradients overwrite ring set m % GRAD_RING, which the owners
+    read in X(m - GRAD_RING).  When C(m) -- whose barrier every rank reaches only after its earlier
+    comm phases -- does not follow X(m - GRAD_RING) on the comm stream, B(m) waits instead for the
+    start barrier of the next un-permute X(x) after it (every rank passes that barrier only after
+    its own X(m - GRAD_RING))."""
+    pos = {o: i for i, o in enumerate(comm)}
+    guards = {}
+    for m in range(GRAD_RING, mb):
+        src = ("X", m - GRAD_RING)
+        if pos[src] < pos[("C", m)]:
+            continue
+        later = [op for op in comm[pos[src] + 1:] if op[0] == "X"]
+        if not later:
+            raise RuntimeError(f"no un-permute barrier after X({m - GRAD_RING}) to guard B({m})")
+        guards[m] = later[0][1]
+    return guards
 
 
 # micro-batch activation / receive buffer sets in wgrad_mode "micro_batch": D(m + 3) is the first
@@ -1071,6 +1099,7 @@ class MoEDataPlane:
         comm_needs = {"C": ("F", 0), "X": ("W" if per_mb else "B", 0)}
         comp_needs = {"F": ("D", 0), "B": ("C", 0), "W": ("X", -1)}
         comm_ops, comp_ops = schedule(self.MB, self.wgrad_mode)
+        ops.ring_guard = replica_ring_guards(comm_ops, self.MB)
         ev_comm, ev_comp = {}, {}
         cs, xs = ops.cs, ops.xs
         ci = pi = 0
@@ -1294,6 +1323,7 @@ class _StepOps:
         self.first = True
         self.start_ev = None
         self.prepared = set()
+        self.ring_guard, self.x_barrier_ev = {}, {}   # see replica_ring_guards
         # layer-shared replica weight slots: the buffer's bookkeeping (shared by the layers), this
         # layer's earlier pulls invalidated (its weights may have changed since)
         dp.rb.invalidate(dp.token)
@@ -1468,6 +1498,9 @@ class _StepOps:
         h = dp.shape.hidden
         with dp._timed(dp.remote_rows(m)[0] * 2 * h, "comm_unpermute", xs):
             dp.arena.barrier(xs)  # dX rows / dgate partials / replica gradients of m complete everywhere
+            if m in self.ring_guard.values():
+                self.x_barrier_ev[m] = torch.cuda.Event()
+                self.x_barrier_ev[m].record(xs)
             # the host-buffer step reads the last micro-batch's dx back in parts, each as it is done
             parts = self.hooks.output_parts(m) if self.hooks and hasattr(self.hooks, "output_parts") else 1
             for p, (t0, t1) in enumerate(_token_parts(dp.T, parts)):
@@ -1553,6 +1586,11 @@ class _StepOps:
         if rw is not None:
             tabs, segs, rrows = rw
             a, q = dp.set_index(m), m % GRAD_RING
+            if m in self.ring_guard:   # ring set q: every owner has read it (X(m - GRAD_RING))
+                ev = self.x_barrier_ev.get(self.ring_guard[m])
+                if ev is None:
+                    raise RuntimeError(f"replica-gradient ring guard of B({m}) issued before X({self.ring_guard[m]})")
+                self.cs.wait_event(ev)
             with dp._timed(6.0 * rrows * h * hp, "wgrad_replica"):
                 self._wgrad_launch(tabs, segs, dp.dYr[a], dp.Act[a], dp.rgW2[q], dp.dH[a], dp.Xr[a], dp.rgW1[q],
                                    sms=dp.all_sms if REPLICA_WGRAD_ALL_SMS else None)

@@ -72,6 +72,16 @@ def test_oversubscribed_replica_step(world, config, tokens, zipf, mode, sets, mi
         assert sum(r["migration"]["moved"] for r in reports) > 0
 
 
+def test_oversubscribed_four_micro_batches_two_steps():
+    """Step mode with 4 micro-batches, two steps: the last combine runs ahead of the third-to-last
+    un-permute (schedule early_last), so B(3)'s replica gradients wait on a later un-permute's
+    barrier before overwriting the ring set X(1) reads (replica_ring_guards)."""
+    args = ["--config", "qwen3-30b-a3b", "--tokens", 1024, "--micro-batches", 4, "--zipf", 1.5, "--group", 4,
+            "--replica-sets", 1, "--min-copies", 2, "--steps", 2]
+    reports = _check(*_launch(4, args), 4)
+    assert sum(r["replica_contrib_experts"] for r in reports) > 0
+
+
 def test_oversubscribed_layers_share_the_replica_buffer():
     """Two MoE layers (own routing, own weights) share one layer-shared replica buffer: each layer's
     replicas are pulled into the same r slots right before use, gradients pushed back per

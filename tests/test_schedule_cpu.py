@@ -74,6 +74,43 @@ def test_ring_sets_reuse_after_all_ranks_finished(mb):
             assert pos[("X", m)] < pos[("C", m + GRAD_RING)]
 
 
+@pytest.mark.parametrize("mb", [1, 2, 3, 4, 8, 16])
+@pytest.mark.parametrize("early", [True, False])
+def test_replica_ring_guards(mb, early):
+    """Step mode: B(m) overwrites replica-gradient ring set m % 2, which the owners read in
+    X(m - 2).  Either C(m) (whose barrier B(m) waits for) follows X(m - 2) on the comm stream, or
+    B(m) carries a guard on the start barrier of a later un-permute, which every rank reaches only
+    after its X(m - 2); with the guard as an extra dependency the two streams still cannot deadlock."""
+    from paper_2605_08639_b200.moe_layer import GRAD_RING, replica_ring_guards
+    comm, comp = schedule(mb, "step", early_last=early)
+    guards = replica_ring_guards(comm, mb)
+    pos = {o: i for i, o in enumerate(comm)}
+    for m in range(GRAD_RING, mb):
+        if m in guards:
+            assert pos[("X", m - GRAD_RING)] < pos[("X", guards[m])] and pos[("C", m)] < pos[("X", m - GRAD_RING)]
+        else:
+            assert pos[("X", m - GRAD_RING)] < pos[("C", m)]
+    if early and mb >= 3:   # the last combine is ahead of the third-to-last un-permute
+        assert pos[("C", mb - 1)] < pos[("X", mb - 3)] and guards == {mb - 1: mb - 2}
+    else:
+        assert guards == {}
+    # B(m) also waits for X(guards[m]): simulate with that dependency added
+    done, ci, pi = set(), 0, 0
+    while ci < len(comm) or pi < len(comp):
+        progressed = False
+        if ci < len(comm):
+            op, m = comm[ci]
+            need = {"C": ("F", m), "X": ("B", m)}.get(op)
+            if need is None or need in done:
+                done.add((op, m)); ci += 1; progressed = True
+        if pi < len(comp):
+            op, m = comp[pi]
+            needs = [("D", m)] if op == "F" else [("C", m)] + ([("X", guards[m])] if m in guards else [])
+            if all(n in done for n in needs):
+                done.add((op, m)); pi += 1; progressed = True
+        assert progressed, f"deadlock at comm {comm[ci:ci + 1]} compute {comp[pi:pi + 1]}"
+
+
 def test_at_most_two_micro_batches_ahead():
     # the dispatch of micro-batch m is queued behind the combine of m-2: a rank can never start
     # the GEMMs of a micro-batch while two earlier ones have not been combined everywhere
