@@ -399,7 +399,9 @@ def schedule(mb: int, wgrad_mode: str = "step", early_last: bool | None = None):
     reference's cost model sums it, sim.py:89-110), not averaged over the step.
     F = fwd GEMMs, B = bwd GEMMs (+ replica weight gradients), W = home weight gradients of one
     micro-batch (wgrad_mode "micro_batch" only), D = dispatch, C = combine + dout dispatch,
-    X = dX un-permute + replica-gradient push-back to the owners."""
+    X = dX un-permute + replica-gradient push-back to the owners.  early_last (step mode, default
+    EARLY_LAST_COMBINE): the tail runs C(n-1) before X(n-3), so the last backward is not queued
+    behind an un-permute (see replica_ring_guards for the ring-set ordering this changes)."""
     comp = [("F", 0)]
     per_mb = wgrad_mode == "micro_batch"
     for m in range(1, mb):
@@ -446,7 +448,8 @@ def replica_ring_guards(comm: list, mb: int) -> dict:
 # barrier (all ranks finished B(m) / W(m)), so three sets suffice for the schedule above
 RING_SETS = 3
 # replica-gradient ring: B(m) writes set m % 2, the owners read it in X(m); B(m + 2) runs after
-# C(m + 2)'s barrier, which every rank reaches after its X(m) push-back
+# C(m + 2)'s barrier, which every rank reaches after its X(m) push-back -- or, where the schedule's
+# tail puts C(m + 2) first, after a later un-permute's barrier (replica_ring_guards)
 GRAD_RING = 2
 ACC_TASK = np.dtype([("dst", "<u8"), ("src", "<u8", (8,)), ("n", "<i8"), ("nsrc", "<i4"), ("store", "<i4")])
 ERR_BITS = {1: "routing has more tokens for an expert than the step plan's counts (perm dropped them)",
